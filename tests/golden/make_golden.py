@@ -1,0 +1,188 @@
+"""Generate golden fixtures by running the REFERENCE helmdef package.
+
+Container-only (imports /root/reference/pkg/src, read-only).  Writes small
+.npz/.json fixtures into tests/golden/; they are committed and travel to the
+GPU box, where the reference does not exist.
+
+    python tests/golden/make_golden.py            # unit-level fixtures (seconds)
+    python tests/golden/make_golden.py --solves   # + full-solve records (minutes)
+"""
+import json
+import os
+import sys
+
+os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_ref")
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+from helmdef import (CslpMultigrid, MadpSolver, StopRule, VelocityModel,  # noqa: E402
+                     build_hierarchy, fgmres, mp1_problem, point_source_rhs, preset,
+                     wedge_problem)
+from helmdef.operators import cslp_operator, helmholtz_operator  # noqa: E402
+from helmdef.parallel import reduce_dot  # noqa: E402
+from helmdef.stencils import REFERENCE_KERNELS  # noqa: E402
+from helmdef.transfers import prolong_array, restrict_array  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def rnd(rng, shape):
+    return rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+
+
+def kernel_tables():
+    out = {str(l): {k: [[list(map(int, r)) for r in v[0]], int(v[1])] for k, v in d.items()}
+           for l, d in REFERENCE_KERNELS.items()}
+    with open(os.path.join(HERE, "kernel_tables.json"), "w") as f:
+        json.dump(out, f)
+
+
+def operators():
+    rng = np.random.default_rng(1)
+    rec = {}
+    for bc in ("sommerfeld", "dirichlet"):
+        p = mp1_problem(k=25.0, n=33, ml=4, boundary=bc)
+        for l in (1, 2, 3, 4):
+            for kind in ("A", "M"):
+                op = helmholtz_operator(p.hierarchy, l) if kind == "A" else \
+                    cslp_operator(p.hierarchy, l, beta2=0.35)
+                u = rnd(rng, op.shape)
+                rec[f"mp1_{bc}_L{l}_{kind}_u"] = u
+                rec[f"mp1_{bc}_L{l}_{kind}_v"] = op.apply(u)
+    p = wedge_problem(f=4.0, nx=25, ml=3)
+    for l in (1, 2, 3):
+        op = helmholtz_operator(p.hierarchy, l)
+        u = rnd(rng, op.shape)
+        rec[f"wedge_L{l}_A_u"] = u
+        rec[f"wedge_L{l}_A_v"] = op.apply(u)
+        if l == 1:
+            op.diagonal()
+            rec["wedge_L1_diag"] = op.diagonal()
+    # mixed boundary, radius 1..3, heterogeneous k^2
+    hier = build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=25.0, ml=3,
+                           velocity=VelocityModel(kind="wedge", layers=[(-400.0, -200.0, 2000.0),
+                                                                        (-800.0, -600.0, 1500.0),
+                                                                        (0.0, 0.0, 3000.0)]),
+                           f=6.0, boundary=("dirichlet", "sommerfeld", "sommerfeld", "dirichlet"))
+    for l in (1, 2, 3):
+        op = cslp_operator(hier, l, beta2=0.5)
+        u = rnd(rng, op.shape)
+        rec[f"mixed_L{l}_M_u"] = u
+        rec[f"mixed_L{l}_M_v"] = op.apply(u)
+    np.savez_compressed(os.path.join(HERE, "operators.npz"), **rec)
+
+
+def transfers():
+    rng = np.random.default_rng(42)
+    rec = {}
+    for (ny, nx) in ((17, 17), (41, 25), (9, 65)):
+        v = rnd(rng, (ny, nx))
+        c = rnd(rng, ((ny - 1) // 2 + 1, (nx - 1) // 2 + 1))
+        rec[f"r_{ny}x{nx}_in"] = v
+        rec[f"r_{ny}x{nx}_out"] = restrict_array(v)
+        rec[f"p_{ny}x{nx}_in"] = c
+        rec[f"p_{ny}x{nx}_out"] = prolong_array(c, (ny, nx))
+    np.savez_compressed(os.path.join(HERE, "transfers.npz"), **rec)
+
+
+def multigrid():
+    rng = np.random.default_rng(8)
+    rec = {}
+    cases = (("mp1s65", mp1_problem(k=50.0, n=65, ml=2), 0.5, False),
+             ("mp1d65div", mp1_problem(k=20.0, n=65, ml=2, boundary="dirichlet"), 0.5, False),
+             ("poisson65", mp1_problem(k=1e-12, n=65, ml=2, boundary="dirichlet"), 0.0, True),
+             ("wedge145", wedge_problem(f=20.0, nx=145, ml=4), 0.5, False))
+    for name, prob, beta2, interior in cases:
+        lv = prob.hierarchy.level(1)
+        mg = CslpMultigrid(lv.nx, lv.ny, lv.h, prob.hierarchy.ksq_at(1), prob.hierarchy.boundary,
+                           beta2=beta2)
+        b = rnd(rng, lv.shape)
+        if interior:
+            b[0, :] = b[-1, :] = b[:, 0] = b[:, -1] = 0.0
+        rec[f"{name}_b"] = b
+        rec[f"{name}_beta2"] = np.array(beta2)
+        try:
+            rec[f"{name}_x"] = mg.vcycle(b)
+            rec[f"{name}_diverged"] = np.array(False)
+        except Exception as err:  # MgDivergence is part of the contract (mg.py:128-138)
+            assert type(err).__name__ == "MgDivergence"
+            rec[f"{name}_diverged"] = np.array(True)
+        rec[f"{name}_depth"] = np.array(mg.depth)
+        # one Jacobi sweep of the finest sub-level from a random x
+        x0 = rnd(rng, lv.shape)
+        rec[f"{name}_jx0"] = x0
+        rec[f"{name}_jx1"] = mg._smooth(0, x0, b, 1)
+    np.savez_compressed(os.path.join(HERE, "multigrid.npz"), **rec)
+
+
+def krylov():
+    rng = np.random.default_rng(11)
+    rec = {}
+    p = mp1_problem(k=5.0, n=9, ml=2, boundary="dirichlet")
+    op = helmholtz_operator(p.hierarchy, 1)
+    b = rnd(rng, (9, 9))
+    x, rep = fgmres(lambda u: op.apply(u), None, b, StopRule(1e-10, 100))
+    rec.update(d9_b=b, d9_x=x, d9_hist=np.array(rep.residual_history), d9_its=rep.iterations,
+               d9_final=rep.final_relres)
+    p = mp1_problem(k=30.0, n=65, ml=3)
+    op = cslp_operator(p.hierarchy, 1, beta2=0.5)
+    b = rnd(rng, op.shape)
+    x, rep = fgmres(lambda u: op.apply(u), None, b, StopRule(0.1, 49), dot=reduce_dot)
+    rec.update(c65_b=b, c65_x=x, c65_hist=np.array(rep.residual_history), c65_its=rep.iterations,
+               c65_final=rep.final_relres)
+    rec["dot_u"] = rnd(rng, (321, 33))
+    rec["dot_v"] = rnd(rng, (321, 33))
+    rec["dot_uv"] = np.array(reduce_dot(rec["dot_u"], rec["dot_v"]))
+    np.savez_compressed(os.path.join(HERE, "krylov.npz"), **rec)
+
+
+SOLVES = {
+    # name: (builder, max_outer, save full solution?)
+    "c1s": (lambda: mp1_problem(k=50.0, n=129, ml=2, boundary="sommerfeld"), 150, True),
+    "wedge20": (lambda: wedge_problem(f=20.0, nx=145, ml=4), 150, True),
+    "c1_cap20": (lambda: mp1_problem(k=50.0, n=129, ml=2, boundary="dirichlet"), 20, True),
+}
+
+
+def solves(names):
+    for name in names:
+        build, cap, save_x = SOLVES[name]
+        prob = build()
+        hier = prob.hierarchy
+        b = prob.rhs.grid_view(hier)
+        cfg = preset("MADP", hier, outer_stop=StopRule(1e-6, cap))
+        with MadpSolver(hier, cfg) as s:
+            u, rep = s.solve(b)
+            x = u.grid_view(hier)
+            # oracle self-sensitivity: b perturbed by 1e-15 relative
+            g = np.random.default_rng(0)
+            bp = b + 1e-15 * np.abs(b).max() * (g.standard_normal(b.shape) + 1j * g.standard_normal(b.shape))
+            up, repp = s.solve(bp)
+            xp = up.grid_view(hier)
+        h0, h1 = np.array(rep.residual_history), np.array(repp.residual_history)
+        n = min(len(h0), len(h1))
+        rec = dict(outer_iterations=rep.outer_iterations, converged=rep.converged,
+                   final_relres=rep.final_relres, residual_history=h0,
+                   cycle_iters=json.dumps({str(k): v for k, v in rep.cycle_iters.items()}),
+                   cslp_iters=json.dumps({str(k): v for k, v in rep.cslp_iters.items()}),
+                   solution_l2=np.linalg.norm(x),
+                   floor_hist_abs=np.abs(h0[:n] - h1[:n]).max(),
+                   floor_sol_rel=np.linalg.norm(x - xp) / np.linalg.norm(x),
+                   floor_its=repp.outer_iterations)
+        if save_x:
+            rec["solution"] = x
+        np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **rec)
+        print(name, rep.outer_iterations, rep.final_relres, rec["floor_hist_abs"], rec["floor_sol_rel"])
+
+
+if __name__ == "__main__":
+    kernel_tables()
+    operators()
+    transfers()
+    multigrid()
+    krylov()
+    if "--solves" in sys.argv:
+        solves([a for a in sys.argv[2:]] or list(SOLVES))
+    print("golden fixtures written to", HERE)
