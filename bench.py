@@ -1,0 +1,366 @@
+"""Benchmark: MADP-FGMRES time-to-solution on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Workload (default): BASELINE configs[1] — constant k=200 on the unit square,
+h = 1/4096 (4097^2 points), first-order Sommerfeld on all sides, centre point
+source, 7-level MADP (the coarse operator turns negative definite on level 7),
+outer FGMRES to 1e-6.  One step = one full solve.  Synthetic by construction
+(the reference's own problem generator; no dataset).
+
+Printed JSON (rank 0, one line):
+  value          device time of one solve (CUDA events on the library stream,
+                 b and x resident in HBM), mean over K timed steps, max over ranks
+  e2e            same solve through the public API  MadpSolver.solve(numpy b)
+                 with pinned host buffers: H2D of b + solve + D2H of x
+  roofline       dominant kernel (measured live with CUDA events on the library
+                 stream at the workload's fine-level shape): achieved algorithmic
+                 GB/s vs the measured HBM copy peak (MEASURED_PEAKS.json)
+  cpu_baseline   the CPU oracle (oracle/, restatement of the reference, bit-exact
+                 with it) on a bounded sample of the same workload, scaled
+  gpu_launches   kernels launched by libhdb200 inside the timed region
+Fine-level vectors are 268 MB (> 126 MB L2), so no explicit L2 flush is needed.
+N > 1: every rank solves its own copy (replicas; slab sharding is the next step,
+DESIGN.md §Multi-GPU) and the max device time over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "solve time & outer iters at 1/2/4/8 B200; stencil HBM GB/s vs roofline"
+CONFIGS = {
+    # name: (description, builder)
+    "c2": ("BASELINE configs[1]: k=200, 4097^2, Sommerfeld, ml=7, MADP",
+           lambda hdb: hdb.mp1_problem(k=200.0, n=4097, ml=7, boundary="sommerfeld")),
+    "c2a": ("config-2 analogue: k=100, 1025^2, Sommerfeld, ml=6, MADP",
+            lambda hdb: hdb.mp1_problem(k=100.0, n=1025, ml=6, boundary="sommerfeld")),
+    "c1s": ("config 1 with Sommerfeld: k=50, 129^2, ml=2, MADP",
+            lambda hdb: hdb.mp1_problem(k=50.0, n=129, ml=2, boundary="sommerfeld")),
+    "c3_40": ("BASELINE configs[2] @40 Hz: wedge 600x1000 m, h=0.5 m, 1201x2001, ml=5, MADP",
+              lambda hdb: hdb.wedge_problem(f=40.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS)),
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.proc, self.lines = index, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _allmax(val, ws):
+    if ws == 1:
+        return val
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([val], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def kernel_roofline(hdb, hier, reps=20):
+    """Time the fine-level 5-point apply (K1) and other path kernels live with CUDA
+    events on the library stream (= torch's current stream)."""
+    import torch
+    from paper_2412_04980_b200 import _lib
+    L = _lib.lib()
+    lv = hier.level(1)
+    op = hdb.helmholtz_operator(hier, 1)
+    n = lv.npoints
+    rng = np.random.default_rng(1234)
+    u = torch.from_numpy(rng.standard_normal(lv.shape) + 1j * rng.standard_normal(lv.shape)).cuda()
+    out = torch.empty_like(u)
+    b = torch.empty_like(u)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(reps):
+            fn()
+        ev1.record()
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / reps * 1e-3
+
+    res = {}
+    h = op.handle
+    t = timeit(lambda: _lib.check(L.hdb_op_apply(h, u.data_ptr(), out.data_ptr())))
+    res["stencil5_apply"] = (40.0 * n, t)
+    t = timeit(lambda: _lib.check(L.hdb_op_residual(h, b.data_ptr(), u.data_ptr(), out.data_ptr())))
+    res["stencil5_residual"] = (56.0 * n, t)
+    mg = hdb.CslpMultigrid(lv.nx, lv.ny, lv.h, hier.ksq_at(1), hier.boundary, beta2=0.5)
+    sop = mg.levels[0].op.handle
+    t = timeit(lambda: _lib.check(L.hdb_op_jacobi(sop, u.data_ptr(), b.data_ptr(), out.data_ptr(), 0.8)))
+    res["jacobi5"] = (56.0 * n, t)
+    c = torch.empty(hier.level(2).shape, dtype=torch.complex128, device="cuda")
+    t = timeit(lambda: _lib.check(L.hdb_restrict(u.data_ptr(), lv.ny, lv.nx, c.data_ptr(), 0)))
+    res["restrict"] = (20.0 * n, t)
+    t = timeit(lambda: _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr())))
+    res["prolong"] = (20.0 * n, t)
+    import ctypes as C
+    d = (C.c_double * 2)()
+    t = timeit(lambda: L.hdb_dot(u.data_ptr(), out.data_ptr(), n, d))  # includes a host sync per call
+    res["dot(sync)"] = (32.0 * n, t)
+    op3 = hdb.helmholtz_operator(hier, 3)
+    l3 = hier.level(3)
+    u3 = torch.from_numpy(rng.standard_normal(l3.shape) + 1j * rng.standard_normal(l3.shape)).cuda()
+    o3 = torch.empty_like(u3)
+    h3 = op3.handle
+    t = timeit(lambda: _lib.check(L.hdb_op_apply(h3, u3.data_ptr(), o3.data_ptr())))
+    res["stencil7_apply_L3"] = (40.0 * l3.npoints, t)
+    op2 = hdb.helmholtz_operator(hier, 2)
+    l2 = hier.level(2)
+    u2 = torch.from_numpy(rng.standard_normal(l2.shape) + 1j * rng.standard_normal(l2.shape)).cuda()
+    o2 = torch.empty_like(u2)
+    h2 = op2.handle
+    t = timeit(lambda: _lib.check(L.hdb_op_apply(h2, u2.data_ptr(), o2.data_ptr())))
+    res["stencil5x5_apply_L2"] = (40.0 * l2.npoints, t)
+    return {k: {"bytes": bts, "ms": tt * 1e3, "gbs": bts / tt / 1e9} for k, (bts, tt) in res.items()}
+
+
+def cpu_baseline(config, outer_its, max_outer=1):
+    """Oracle (bit-exact restatement of the reference) on a bounded sample: the
+    first `max_outer` outer iteration(s) of the same solve, scaled linearly to
+    the GPU's outer-iteration count."""
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_oracle")
+    import oracle
+    if config == "c2":
+        hier, b = oracle.mp1_problem(200.0, 4097, 7)
+    elif config == "c2a":
+        hier, b = oracle.mp1_problem(100.0, 1025, 6)
+    elif config == "c1s":
+        hier, b = oracle.mp1_problem(50.0, 129, 2)
+    else:
+        hier, b = oracle.baseline_wedge_problem(40.0)
+    pols, outer = oracle.madp_preset(hier)
+    s = oracle.CpuMadpSolver(hier, pols, outer)
+    # JIT warm-up on a tiny problem (numba compile is not part of the sample)
+    th, tb = oracle.mp1_problem(10.0, 33, 3)
+    tp, to = oracle.madp_preset(th)
+    oracle.CpuMadpSolver(th, tp, to).solve(tb)
+    t0 = time.perf_counter()
+    _, rep = s.solve(b, max_outer=max_outer)
+    dt = time.perf_counter() - t0
+    per_it = dt / max(1, rep.iterations)
+    return {"value": per_it * outer_its, "unit": "s", "cores": 1, "kind": "port",
+            "sample": f"oracle (bit-exact CPU restatement of helmdef, numba loops, 1 thread) on the first "
+                      f"{rep.iterations} outer iteration(s) of the same solve: {dt:.2f} s, scaled x{outer_its} "
+                      f"outer iterations"}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import oracle  # noqa: F401
+    steps = []
+    its = args.ref_outer_its
+    for k in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.config, its, max_outer=1)
+        if k >= args.warmup:
+            steps.append(cb["value"])
+    val = float(np.mean(steps))
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config][0]},
+            "cpu_baseline": {"value": val, "unit": "s", "cores": 1, "kind": "port", "sample": cb["sample"]},
+            "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--ref-outer-its", type=int, default=int(os.environ.get("HDB_REF_OUTER_ITS", "0")) or None)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        if args.ref_outer_its is None:
+            args.ref_outer_its = REF_OUTER_ITS.get(args.config, 1)
+        return run_reference(args)
+
+    ws, rank, local = _dist()
+    import torch
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_2412_04980_b200 as hdb
+    from paper_2412_04980_b200 import _lib
+    L = _lib.lib()
+
+    prob = CONFIGS[args.config][1](hdb)
+    hier = prob.hierarchy
+    cfg = hdb.preset("MADP", hier)
+    solver = hdb.MadpSolver(hier, cfg)
+    shape = hier.level(1).shape
+    b_host = prob.rhs.grid_view(hier)
+    b_dev = torch.from_numpy(b_host.copy()).cuda()
+    x_dev = torch.empty_like(b_dev)
+    # pinned host buffers for the end-to-end leg
+    b_pin = torch.empty(shape, dtype=torch.complex128, pin_memory=True)
+    b_pin.copy_(torch.from_numpy(b_host))
+    b_pin_np = b_pin.numpy()
+
+    for _ in range(args.warmup):
+        rep = solver.solve_device(b_dev, x_dev)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    l0 = C_launches(L)
+    times = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            rep = solver.solve_device(b_dev, x_dev)
+            times.append(rep.device_ms / 1e3)
+        torch.cuda.synchronize()
+    launches = C_launches(L) - l0
+    if ws > 1:
+        torch.distributed.barrier()
+    t_step = _allmax(float(np.mean(times)), ws)
+
+    # end-to-end through the public API (numpy in pinned memory -> numpy out)
+    e2e = []
+    for k in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        u, rep_e = solver.solve(b_pin_np)
+        e2e.append(time.perf_counter() - t0)
+    e2e_t = _allmax(float(np.mean(e2e)), ws)
+
+    kern = kernel_roofline(hdb, hier) if rank == 0 else {}
+    peak, peak_src = _peaks()
+    dom = kern.get("stencil5_apply")
+    out_line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu and ws == 1:
+            try:
+                cpu = cpu_baseline(args.config, rep.outer_iterations)
+            except Exception as err:  # noqa: BLE001
+                cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port", "sample": f"failed: {err}"}
+        out_line = {
+            "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config][0], "grid": f"{shape[1]}x{shape[0]}",
+                       "levels": hier.ml, "parallelism": "replicas" if ws > 1 else "single",
+                       "l2_flush": "inputs larger than L2 (268 MB per fine-level vector)"},
+            "outer_iters": rep.outer_iterations, "converged": rep.converged,
+            "final_relres": rep.final_relres,
+            "cycle_iters_max": {str(l): rep.cycle_max(l) for l in range(2, hier.ml + 1)},
+            "cslp_iters_max": {str(l): rep.cslp_max(l) for l in range(1, hier.ml + 1)},
+            "e2e": {"value": e2e_t, "unit": "s", "h2d_bytes_per_step": int(b_host.nbytes),
+                    "d2h_bytes_per_step": int(b_host.nbytes)},
+            "roofline": {"bound": "hbm", "kernel": "stencil5_apply (K1, fine level)",
+                         "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"]},
+            "kernels": {k: {"gbs": round(v["gbs"], 1), "ms": round(v["ms"], 4), "frac": round(v["gbs"] / peak, 3)}
+                        for k, v in kern.items()},
+            "gpu_launches": int(launches / max(1, args.steps)),
+            "gpu_launches_total": int(launches),
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out_line), flush=True)
+    solver.close()
+    if ws > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def C_launches(L):
+    import ctypes as C
+    a, b = C.c_longlong(), C.c_longlong()
+    L.hdb_stats(C.byref(a), C.byref(b))
+    return a.value
+
+
+# outer-iteration counts used to scale the reference arm's bounded sample
+# (GPU solve counts, equal to the oracle's where the oracle was run to the end)
+REF_OUTER_ITS = {"c2": 20, "c2a": 17, "c1s": 12, "c3_40": 19}
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,119 @@
+/*
+ * hdb200 — C ABI of the B200-native MADP-FGMRES library (libhdb200.so).
+ *
+ * Drop-in boundary for the reference package `helmdef` (arXiv 2412.04980
+ * reference implementation, /root/reference/pkg/src/helmdef).  The reference
+ * has no FFI of its own: its "plugin surface" is the Python API re-exported in
+ * __init__.py:9-62.  Each entry point below replaces the compute behind one
+ * reference call (file:line relative to pkg/src/helmdef/); the Python package
+ * paper_2412_04980_b200 binds them with ctypes and keeps the reference names
+ * and signatures.
+ *
+ * Conventions
+ *   - complex128 fields are interleaved (re, im) doubles, row-major (x fastest),
+ *     exactly numpy's complex128 layout; k^2 fields are float64.
+ *   - pointers are DEVICE pointers unless the argument name ends in _host.
+ *   - every function returns a status: 0 ok, 1 bad argument (ShapeError /
+ *     LevelError / ConfigError), 2 CUDA failure (HelmdefError), 3 non-finite
+ *     value (NumericalError), 4 multigrid divergence (MgDivergence);
+ *     hdb_last_error() returns the message of the last failure (thread-local).
+ *   - all work is ordered on one library stream per process (hdb_stream);
+ *     functions that return host scalars synchronise it.
+ *   - boundary kinds per side (west, east, south, north): 0 Sommerfeld, 1 Dirichlet.
+ */
+#ifndef HDB200_H
+#define HDB200_H
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDB_OK 0
+#define HDB_E_ARG 1
+#define HDB_E_CUDA 2
+#define HDB_E_NONFINITE 3
+#define HDB_E_MGDIV 4
+
+typedef struct hdb_op hdb_op;        /* one level operator  -Lap - shift*I(k^2)   */
+typedef struct hdb_mg hdb_mg;        /* CSLP multigrid (mg.py:51)                  */
+typedef struct hdb_solver hdb_solver;/* MADP solver (madp.py:220)                  */
+
+/* out = Op(in) on device buffers of the operator's level; return nonzero on failure */
+typedef int (*hdb_linop_fn)(void* user, const void* in, void* out);
+/* on_iteration(iteration, relres) hook (krylov.py:153-154); return nonzero to abort */
+typedef int (*hdb_iter_fn)(void* user, int iteration, double relres);
+
+/* ---- library ------------------------------------------------------------ */
+int hdb_version(void);
+const char* hdb_last_error(void);
+/* select the device and create the library stream (idempotent per device) */
+int hdb_init(int device);
+int hdb_stream(void** stream_out);
+/* order all library work on an external stream (e.g. torch's current stream) */
+int hdb_set_stream(void* stream);
+int hdb_sync(void);
+/* kernels launched through the library so far, device bytes allocated */
+int hdb_stats(long long* launches, long long* bytes_alloc);
+
+/* ---- level operators: replaces LevelOperator (operators.py:96-208) -------- */
+/* lap: (2r+1)^2 float coefficients = lap_coef (operators.py:111);
+ * mass_re/mass_im: mass_coef (operators.py:112-113); ksq_host: ny*nx k^2   */
+int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int* bc4,
+                  const double* lap, const double* mass_re, const double* mass_im,
+                  const double* ksq_host);
+int hdb_op_destroy(hdb_op* op);
+/* LevelOperator.apply (operators.py:130-147): out = A u, Dirichlet rows pinned */
+int hdb_op_apply(hdb_op* op, const void* u, void* out);
+/* out = b - A u  (MG residual mg.py:116, A-DEF1 v - A t madp.py:325-326) */
+int hdb_op_residual(hdb_op* op, const void* b, const void* u, void* out);
+/* one damped-Jacobi sweep (_kernels.py:53-68 + mg.py:88-102); x == NULL: from zero */
+int hdb_op_jacobi(hdb_op* op, const void* x, const void* b, void* out, double omega);
+
+/* ---- transfers: replaces restrict_array / prolong_array (transfers.py:59-88) */
+/* zero_mask bits 1 W, 2 E, 4 S, 8 N: coarse rows set to 0 (mg.py:118-119)  */
+int hdb_restrict(const void* fine, int nfy, int nfx, void* coarse, int zero_mask);
+/* fine = Z coarse  (base != NULL: fine = base + Z coarse, mg.py:121)          */
+int hdb_prolong(const void* coarse, int nfy, int nfx, const void* base, void* fine);
+
+/* ---- reductions: replaces reduce_dot (parallel.py:168-195) ---------------- */
+int hdb_dot(const void* u, const void* v, long long n, double* out2_host);
+
+/* ---- CSLP multigrid: replaces CslpMultigrid (mg.py:59-139) ---------------- */
+/* ops: sub-level operators finest first (radius 1); inv_host: dense inverse of
+ * the coarsest operator (ninv x ninv complex, row-major) or NULL for the GMRES
+ * fallback with (coarse_tol, coarse_max)                                      */
+int hdb_mg_create(hdb_mg** out, hdb_op* const* ops, int nlev, const double* inv_host, int ninv,
+                  double omega, int pre, int post, double guard, double coarse_tol, int coarse_max);
+int hdb_mg_destroy(hdb_mg* mg);
+/* one V-cycle (mg.py:125-139) from x0 (NULL: zero); HDB_E_MGDIV on the guard  */
+int hdb_mg_vcycle(hdb_mg* mg, const void* b, const void* x0, void* x);
+
+/* ---- Krylov: replaces fgmres / gmres (krylov.py:61-182) ------------------- */
+/* x0 may be NULL (zero initial guess); M may be NULL (GMRES); hook may be NULL */
+int hdb_fgmres(long long n, hdb_linop_fn A, void* A_user, hdb_linop_fn M, void* M_user,
+               const void* b, const void* x0, void* x, double rel_tol, int max_iters,
+               hdb_iter_fn hook, void* hook_user,
+               int* iterations, double* final_relres, int* converged,
+               double* history_host, int history_cap);
+
+/* ---- MADP solver: replaces MadpSolver (madp.py:220-371) ------------------- */
+int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max);
+/* cslp: 0 none, 1 mg, 2 gmres (madp.py:55-58); level 1 ignores the cycle rule */
+int hdb_solver_set_level(hdb_solver* s, int level, hdb_op* A, hdb_op* M, hdb_mg* mg, int cslp,
+                         double cslp_tol, int cslp_max, double cycle_tol, int cycle_max);
+/* MadpSolver.solve (madp.py:329-371); host_buffers != 0: b, x are host pointers
+ * (copies included in the call)                                              */
+int hdb_solver_solve(hdb_solver* s, const void* b, void* x, int host_buffers);
+int hdb_solver_report(hdb_solver* s, int* outer_iterations, int* converged, double* final_relres,
+                      double* wall_ms, int* history_len);
+int hdb_solver_history(hdb_solver* s, double* history_host, double* iteration_wall_ms_host, int cap);
+/* kind 0: deflation-cycle iterations, 1: CSLP iterations, per application    */
+int hdb_solver_counts(hdb_solver* s, int level, int kind, int* buf_host, int cap, int* count);
+int hdb_solver_matvecs(hdb_solver* s, long long* buf_host, int cap);
+/* MadpSolver.apply_preconditioner (madp.py:301-327) on device vectors */
+int hdb_solver_precond(hdb_solver* s, int level, const void* v, void* out);
+int hdb_solver_destroy(hdb_solver* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,312 @@
+// extern "C" boundary (declared in include/hdb200.h).  Every entry point
+// catches engine exceptions and turns them into a status + message.
+#include <cstring>
+#include <string>
+
+#include "../../include/hdb200.h"
+#include "engine.h"
+
+using namespace hdb;
+
+struct hdb_op { LevelOp op; };
+struct hdb_mg { Multigrid mg; };
+struct hdb_solver { MadpSolver s; };
+
+static thread_local std::string g_err;
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    f();
+    return HDB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HDB_E_CUDA;
+  } catch (...) {
+    g_err = "unknown error";
+    return HDB_E_CUDA;
+  }
+}
+
+static void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+extern "C" {
+
+int hdb_version(void) { return 100; }
+const char* hdb_last_error(void) { return g_err.c_str(); }
+
+int hdb_init(int device) {
+  return guarded([&] { engine_init(device); });
+}
+int hdb_stream(void** out) {
+  return guarded([&] { *out = (void*)engine().st; });
+}
+int hdb_set_stream(void* stream) {
+  return guarded([&] {
+    Engine& E = engine();
+    E.sync();
+    E.st = (cudaStream_t)stream;
+  });
+}
+int hdb_sync(void) {
+  return guarded([&] { engine().sync(); });
+}
+int hdb_stats(long long* launches, long long* bytes) {
+  return guarded([&] {
+    if (launches) *launches = engine().launches;
+    if (bytes) *bytes = (long long)engine().bytes_alloc;
+  });
+}
+
+int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int* bc4, const double* lap,
+                  const double* mass_re, const double* mass_im, const double* ksq_host) {
+  return guarded([&] {
+    if (nx < 2 || ny < 2) throw Error(E_ARG, "grid needs at least 2 points per direction");
+    if (radius < 1 || radius > 3) throw Error(E_ARG, "radius must be 1, 2 or 3");
+    Engine& E = engine();
+    auto* o = new hdb_op();
+    LevelOp& L = o->op;
+    std::memset(&L.c, 0, sizeof(L.c));
+    L.c.radius = radius;
+    for (int s = 0; s < 4; ++s) L.c.bc[s] = bc4[s];
+    L.c.h = h;
+    const int N = 2 * radius + 1;
+    for (int i = 0; i < N * N; ++i) {
+      L.c.lap[i] = lap[i];
+      L.c.mass[i] = mkc(mass_re[i], mass_im[i]);
+    }
+    if (radius == 1) {
+      L.c.s = lap[4] / 4.0;   // lap_coef[1,1] / 4   (operators.py:174, 186)
+      L.c.mc = L.c.mass[4];   // mass_coef[1,1]
+      L.c.E = (-L.c.s * 2.0) * h;  // -lap_scale*2i*h  (operators.py:198)
+    }
+    L.g.nx = nx; L.g.ny = ny; L.g.row0 = 0; L.g.nyg = ny;
+    L.n = (long long)nx * ny;
+    L.ksq = (double*)E.alloc_bytes(sizeof(double) * L.n);
+    HDB_CUDA(cudaMemcpyAsync(L.ksq, ksq_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, E.st));
+    HDB_CUDA(cudaStreamSynchronize(E.st));
+    *out = o;
+  });
+}
+
+int hdb_op_destroy(hdb_op* op) {
+  return guarded([&] {
+    if (!op) return;
+    if (engine_ready()) { engine().sync(); engine().free(op->op.ksq); }
+    delete op;
+  });
+}
+
+int hdb_op_apply(hdb_op* op, const void* u, void* out) {
+  return guarded([&] { op->op.apply((const cd*)u, (cd*)out); check_launch(); });
+}
+int hdb_op_residual(hdb_op* op, const void* b, const void* u, void* out) {
+  return guarded([&] { op->op.residual((const cd*)b, (const cd*)u, (cd*)out); check_launch(); });
+}
+int hdb_op_jacobi(hdb_op* op, const void* x, const void* b, void* out, double omega) {
+  return guarded([&] {
+    if (op->op.c.radius != 1) throw Error(E_ARG, "Jacobi is only defined for radius-1 operators");
+    op->op.jacobi((const cd*)x, (const cd*)b, (cd*)out, omega, x == nullptr);
+    check_launch();
+  });
+}
+
+int hdb_restrict(const void* fine, int nfy, int nfx, void* coarse, int zero_mask) {
+  return guarded([&] {
+    if ((nfx - 1) % 2 || (nfy - 1) % 2 || nfx < 3 || nfy < 3)
+      throw Error(E_ARG, "cannot coarsen: n-1 must be even (transfers.py:53-56)");
+    launch_restrict((const cd*)fine, (cd*)coarse, nfx, nfy, zero_mask, engine().st);
+    check_launch();
+  });
+}
+int hdb_prolong(const void* coarse, int nfy, int nfx, const void* base, void* fine) {
+  return guarded([&] {
+    if ((nfx - 1) % 2 || (nfy - 1) % 2) throw Error(E_ARG, "fine shape does not refine the coarse grid");
+    launch_prolong((const cd*)coarse, (const cd*)base, (cd*)fine, nfx, nfy, base != nullptr, engine().st);
+    check_launch();
+  });
+}
+
+int hdb_dot(const void* u, const void* v, long long n, double* out2) {
+  return guarded([&] {
+    Engine& E = engine();
+    launch_dot((const cd*)u, (const cd*)v, n, E.red, E.dscal + kSlotMisc, E.st);
+    check_launch();
+    HDB_CUDA(cudaMemcpyAsync(E.hscal + kSlotMisc, E.dscal + kSlotMisc, sizeof(cd), cudaMemcpyDeviceToHost, E.st));
+    E.sync();
+    out2[0] = E.hscal[kSlotMisc].x;
+    out2[1] = E.hscal[kSlotMisc].y;
+  });
+}
+
+int hdb_mg_create(hdb_mg** out, hdb_op* const* ops, int nlev, const double* inv_host, int ninv, double omega,
+                  int pre, int post, double guard, double coarse_tol, int coarse_max) {
+  return guarded([&] {
+    if (nlev < 1) throw Error(E_ARG, "multigrid needs at least one level");
+    if (pre < 0 || post < 0 || pre + post < 1) throw Error(E_ARG, "at least one smoothing step is required");
+    Engine& E = engine();
+    auto* m = new hdb_mg();
+    for (int i = 0; i < nlev; ++i) m->mg.ops.push_back(&ops[i]->op);
+    m->mg.omega = omega; m->mg.pre = pre; m->mg.post = post; m->mg.guard = guard;
+    m->mg.coarse_stop = Stop{coarse_tol, coarse_max};
+    if (inv_host) {
+      if ((long long)ninv != ops[nlev - 1]->op.n) { delete m; throw Error(E_ARG, "inverse size mismatch"); }
+      m->mg.ninv = ninv;
+      m->mg.Ainv = (cd*)E.alloc_bytes(sizeof(cd) * (size_t)ninv * ninv);
+      HDB_CUDA(cudaMemcpyAsync(m->mg.Ainv, inv_host, sizeof(cd) * (size_t)ninv * ninv, cudaMemcpyHostToDevice, E.st));
+    }
+    m->mg.setup();
+    E.sync();
+    *out = m;
+  });
+}
+int hdb_mg_destroy(hdb_mg* mg) {
+  return guarded([&] {
+    if (engine_ready()) engine().sync();
+    delete mg;
+  });
+}
+int hdb_mg_vcycle(hdb_mg* mg, const void* b, const void* x0, void* x) {
+  return guarded([&] {
+    Engine& E = engine();
+    HDB_CUDA(cudaMemsetAsync(E.dscal + kSlotFlag, 0, sizeof(cd), E.st));
+    mg->mg.vcycle((const cd*)b, (cd*)x, (const cd*)x0);
+    check_launch();
+    E.fetch(1);
+  });
+}
+
+int hdb_fgmres(long long n, hdb_linop_fn A, void* Au, hdb_linop_fn M, void* Mu, const void* b, const void* x0,
+               void* x, double rel_tol, int max_iters, hdb_iter_fn hook, void* hook_user, int* iterations,
+               double* final_relres, int* converged, double* hist, int hist_cap) {
+  return guarded([&] {
+    if (max_iters < 1) throw Error(E_ARG, "max_iters must be >= 1");
+    if (rel_tol < 0) throw Error(E_ARG, "rel_tol must be nonnegative");
+    LinOp Aop = [A, Au](const cd* in, cd* out) {
+      if (A(Au, in, out) != 0) throw Error(E_ARG, "operator callback failed");
+    };
+    LinOp Mop = [M, Mu](const cd* in, cd* out) {
+      if (M(Mu, in, out) != 0) throw Error(E_ARG, "preconditioner callback failed");
+    };
+    std::function<void(int, double)> H = [hook, hook_user](int it, double rel) {
+      if (hook(hook_user, it, rel) != 0) throw Error(E_ARG, "iteration callback failed");
+    };
+    KWS ws;
+    KReport r = fgmres(n, Aop, M ? &Mop : nullptr, (const cd*)b, (cd*)x, Stop{rel_tol, max_iters}, ws,
+                       hook ? &H : nullptr, (const cd*)x0);
+    engine().sync();
+    *iterations = r.iterations;
+    *final_relres = r.final_relres;
+    *converged = r.converged ? 1 : 0;
+    for (int i = 0; i < hist_cap && i < (int)r.history.size(); ++i) hist[i] = r.history[i];
+  });
+}
+
+int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max) {
+  return guarded([&] {
+    if (ml < 2) throw Error(E_ARG, "hierarchy needs at least two levels");
+    auto* s = new hdb_solver();
+    s->s.set_levels(ml);
+    s->s.outer = Stop{outer_tol, outer_max};
+    *out = s;
+  });
+}
+int hdb_solver_set_level(hdb_solver* s, int level, hdb_op* A, hdb_op* M, hdb_mg* mg, int cslp, double cslp_tol,
+                         int cslp_max, double cycle_tol, int cycle_max) {
+  return guarded([&] {
+    if (level < 1 || level > s->s.ml) throw Error(E_ARG, "level outside 1..ml");
+    MadpLevel& L = s->s.lv[level];
+    L.A = &A->op;
+    L.M = M ? &M->op : nullptr;
+    L.mg = mg ? &mg->mg : nullptr;
+    L.cslp = cslp;
+    if (cslp == CSLP_MG && !mg) throw Error(E_ARG, "cslp=mg needs a multigrid");
+    if (cslp == CSLP_GMRES && !M) throw Error(E_ARG, "cslp=gmres needs a CSLP operator");
+    L.cslp_stop = Stop{cslp_tol, cslp_max};
+    L.cycle_stop = Stop{cycle_tol, cycle_max};
+  });
+}
+int hdb_solver_solve(hdb_solver* s, const void* b, void* x, int host_buffers) {
+  return guarded([&] {
+    Engine& E = engine();
+    const long long n = s->s.lv[1].A->n;
+    if (!host_buffers) {
+      s->s.solve((const cd*)b, (cd*)x);
+      return;
+    }
+    cd* db = E.alloc(n);
+    cd* dx = E.alloc(n);
+    try {
+      HDB_CUDA(cudaMemcpyAsync(db, b, sizeof(cd) * n, cudaMemcpyHostToDevice, E.st));
+      s->s.solve(db, dx);
+      HDB_CUDA(cudaMemcpyAsync(x, dx, sizeof(cd) * n, cudaMemcpyDeviceToHost, E.st));
+      E.sync();
+    } catch (...) {
+      E.sync();
+      E.free(db);
+      E.free(dx);
+      throw;
+    }
+    E.free(db);
+    E.free(dx);
+  });
+}
+int hdb_solver_report(hdb_solver* s, int* its, int* conv, double* fin, double* wall, int* hl) {
+  return guarded([&] {
+    const SolveReport& r = s->s.rep;
+    *its = r.outer.iterations;
+    *conv = r.outer.converged ? 1 : 0;
+    *fin = r.outer.final_relres;
+    *wall = r.wall_ms;
+    *hl = (int)r.outer.history.size();
+  });
+}
+int hdb_solver_history(hdb_solver* s, double* hist, double* iw, int cap) {
+  return guarded([&] {
+    const SolveReport& r = s->s.rep;
+    for (int i = 0; i < cap && i < (int)r.outer.history.size(); ++i) hist[i] = r.outer.history[i];
+    if (iw)
+      for (int i = 0; i < cap && i < (int)r.iter_wall_ms.size(); ++i) iw[i] = r.iter_wall_ms[i];
+  });
+}
+int hdb_solver_counts(hdb_solver* s, int level, int kind, int* buf, int cap, int* count) {
+  return guarded([&] {
+    const SolveReport& r = s->s.rep;
+    if (level < 1 || level >= (int)r.cycle_iters.size()) throw Error(E_ARG, "level outside 1..ml");
+    const std::vector<int>& v = kind == 0 ? r.cycle_iters[level] : r.cslp_iters[level];
+    *count = (int)v.size();
+    for (int i = 0; i < cap && i < (int)v.size(); ++i) buf[i] = v[i];
+  });
+}
+int hdb_solver_matvecs(hdb_solver* s, long long* buf, int cap) {
+  return guarded([&] {
+    const SolveReport& r = s->s.rep;
+    for (int i = 0; i < cap && i < (int)r.matvecs.size(); ++i) buf[i] = r.matvecs[i];
+  });
+}
+int hdb_solver_precond(hdb_solver* s, int level, const void* v, void* out) {
+  return guarded([&] {
+    if (level < 1 || level >= s->s.ml) throw Error(E_ARG, "preconditioner level outside 1..ml-1");
+    Engine& E = engine();
+    s->s.setup();
+    s->s.reset_report();
+    HDB_CUDA(cudaMemsetAsync(E.dscal + kSlotFlag, 0, sizeof(cd), E.st));
+    s->s.precond(level, (const cd*)v, (cd*)out);
+    check_launch();
+    E.fetch(1);
+  });
+}
+int hdb_solver_destroy(hdb_solver* s) {
+  return guarded([&] {
+    if (engine_ready()) engine().sync();
+    delete s;
+  });
+}
+
+}  // extern "C"

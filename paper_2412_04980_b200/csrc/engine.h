@@ -1,0 +1,160 @@
+// Host-side engine: device buffers, level operators, Krylov driver (FGMRES with
+// host Givens), CSLP multigrid V-cycle and the recursive A-DEF1 (MADP) solver.
+#pragma once
+#include <complex>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+
+namespace hdb {
+
+enum Status { OK = 0, E_ARG = 1, E_CUDA = 2, E_NONFINITE = 3, E_MGDIV = 4, E_BREAKDOWN = 5 };
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define HDB_CUDA(x)                                                                         \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::hdb::Error(::hdb::E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+using cplx = std::complex<double>;
+
+// device scalar block layout (Engine::dscal)
+constexpr int kScal = 1024;
+constexpr int kSlotFlag = 0;        // .x = 1.0 once an MG divergence guard fired
+constexpr int kSlotH = 1;           // Hessenberg column h_0.. at kSlotH + i
+constexpr int kSlotMgPost = 1020;
+constexpr int kSlotMgB = 1021;
+constexpr int kSlotMisc = 1022;
+constexpr int kSlotMgR0 = 1019;
+
+struct Engine {
+  int device = 0;
+  cudaStream_t st = nullptr;      // stream all work is ordered on (may be external)
+  cudaStream_t own_st = nullptr;  // the stream created by the engine
+  RedWS red;
+  cd* dscal = nullptr;   // device scalars
+  cd* hscal = nullptr;   // pinned host mirror
+  size_t bytes_alloc = 0;
+  long long launches = 0;  // kernels launched through the engine (telemetry)
+
+  explicit Engine(int dev);
+  ~Engine();
+  cd* alloc(long long n);              // complex vector
+  void* alloc_bytes(size_t b);
+  void free(void* p);
+  void sync() { HDB_CUDA(cudaStreamSynchronize(st)); }
+  // read slots [0, count) to host (one copy + sync) and raise on a fired MG guard
+  void fetch(int count);
+  double fetch_norm(int slot);  // sqrt(max(re,0)) of a slot, after fetch
+};
+
+Engine& engine();            // process-wide engine of the selected device
+void engine_init(int device);
+bool engine_ready();
+
+struct Stop {
+  double rel_tol;
+  int max_iters;
+};
+
+struct KReport {
+  int iterations = 0;
+  double final_relres = 0.0;
+  std::vector<double> history;
+  bool converged = false;
+};
+
+// one level operator (A or CSLP M) on device
+struct LevelOp {
+  OpCoef c;
+  Geom g;
+  double* ksq = nullptr;  // device, ny*nx
+  long long n = 0;
+  void apply(const cd* u, cd* out) const;                 // out = A u
+  void residual(const cd* b, const cd* u, cd* out) const;  // out = b - A u
+  void jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const;
+};
+
+using LinOp = std::function<void(const cd* in, cd* out)>;
+
+// Krylov workspace: basis vectors grow on demand and are kept across calls
+struct KWS {
+  long long n = 0;
+  std::vector<cd*> V, Z;
+  cd* tmp = nullptr;
+  cd** dbasis = nullptr;  // device pointer table for the solution update
+  cd* dy = nullptr;
+  cd** hbasis = nullptr;  // pinned staging
+  cd* hy = nullptr;
+  int cap = 0;
+  void ensure(long long n_, int cap_, bool flexible);
+  cd* v(int i);
+  cd* z(int i);
+  ~KWS();
+};
+
+// right-preconditioned unrestarted FGMRES (krylov.py:61-177); M == nullptr -> GMRES
+KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
+               const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr);
+
+struct Multigrid {
+  std::vector<const LevelOp*> ops;  // sub-levels, finest first
+  std::vector<cd*> X, Y, R, B, O;   // per-level scratch (X,Y,R), rhs (B), output (O)
+  cd* Ainv = nullptr;               // coarsest dense inverse (n <= direct limit)
+  int ninv = 0;
+  KWS coarse_ws;
+  Stop coarse_stop{1e-8, 50};
+  double omega = 0.8, guard = 10.0;
+  int pre = 1, post = 1;
+  void setup();
+  void vcycle(const cd* b, cd* x, const cd* x0 = nullptr);  // mg.py:125-139 (guard -> device flag)
+  void cycle(int i, const cd* b, cd* x, const cd* x_init);
+  ~Multigrid();
+};
+
+enum { CSLP_NONE = 0, CSLP_MG = 1, CSLP_GMRES = 2 };
+
+struct MadpLevel {
+  const LevelOp* A = nullptr;
+  const LevelOp* M = nullptr;
+  Multigrid* mg = nullptr;
+  int cslp = CSLP_NONE;
+  Stop cslp_stop{0.1, 1}, cycle_stop{1.0, 1};
+  KWS ws_defl, ws_cslp;
+  cd *vhat = nullptr, *vtil = nullptr;        // this level's input / output as a deflation system
+  cd *t = nullptr, *rhs = nullptr, *r = nullptr;  // A-DEF1 temporaries of P_l
+};
+
+struct SolveReport {
+  KReport outer;
+  std::vector<std::vector<int>> cycle_iters, cslp_iters;  // index = level
+  std::vector<long long> matvecs;
+  std::vector<double> iter_wall_ms;
+  double wall_ms = 0.0;
+};
+
+struct MadpSolver {
+  int ml = 0;
+  std::vector<MadpLevel> lv;  // index 1..ml
+  Stop outer{1e-6, 150};
+  SolveReport rep;
+  void set_levels(int ml_);
+  void reset_report();
+  void setup();
+  void cslp_apply(int l, const cd* rhs, cd* out);
+  void precond(int l, const cd* v, cd* out);
+  void A(int l, const cd* u, cd* out);
+  void solve(const cd* b, cd* x);
+  ~MadpSolver();
+};
+
+}  // namespace hdb

@@ -1,0 +1,31 @@
+// Kernel launchers (internal C++ interface between the engine and the .cu files).
+#pragma once
+#include "hdb_common.cuh"
+
+namespace hdb {
+
+struct RedWS {  // per-stream reduction workspace
+  cd* partials = nullptr;   // kMaxReduceBlocks
+  unsigned* ticket = nullptr;
+};
+
+int reduce_blocks(long long n);
+
+// mode 0: out = A u ; mode 1: out = b - A u
+void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out, int mode,
+                  cudaStream_t st);
+void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out, double omega,
+                   bool from_zero, cudaStream_t st);
+void launch_restrict(const cd* fine, cd* coarse, int nfx, int nfy, int zero_mask, cudaStream_t st);
+void launch_prolong(const cd* coarse, const cd* base, cd* fine, int nfx, int nfy, int accumulate, cudaStream_t st);
+
+void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st);
+void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st);
+void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st);
+void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st);
+void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd* x, long long n, cudaStream_t st);
+void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st);
+void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st);
+void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st);
+
+}  // namespace hdb

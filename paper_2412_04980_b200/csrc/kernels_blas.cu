@@ -1,0 +1,193 @@
+// Krylov vector kernels: deterministic conj-dots, fused MGS steps, scaling,
+// solution update, combine.  Reference: krylov.py:121-174, parallel.py:168-199.
+//
+// Reductions are single-launch and deterministic: a fixed grid (function of
+// n only) writes per-block partials, the last block to finish (threadfence +
+// ticket) sums them in a fixed order and writes the scalar to device memory.
+// Nothing returns to the host here; the Krylov driver reads the Hessenberg
+// column once per Arnoldi step.
+#include "kernels.h"
+#include "hdb_common.cuh"
+
+namespace hdb {
+
+int reduce_blocks(long long n) {
+  long long b = (n + kReduceThreads * 4 - 1) / (kReduceThreads * 4);
+  if (b < 1) b = 1;
+  if (b > kMaxReduceBlocks) b = kMaxReduceBlocks;
+  return (int)b;
+}
+
+__device__ __forceinline__ cd warp_sum(cd v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// block-wide sum in fixed order; result valid in thread 0
+__device__ __forceinline__ cd block_sum(cd v) {
+  __shared__ cd sw[kReduceThreads / 32];
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sw[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    v = lane < kReduceThreads / 32 ? sw[lane] : mkc(0.0, 0.0);
+    v = warp_sum(v);
+  }
+  __syncthreads();
+  return v;
+}
+
+// finish a grid reduction: every block deposits its partial; the last one
+// sums partials[0..G) in order and stores to *dst (optionally only the real
+// part as a squared norm).
+__device__ __forceinline__ void grid_finish(cd part, cd* partials, unsigned* ticket, cd* dst) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = part;
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  cd v = mkc(0.0, 0.0);
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+    const volatile double* q = (const volatile double*)(partials + b);
+    v.x += q[0];
+    v.y += q[1];
+  }
+  v = block_sum(v);
+  if (threadIdx.x == 0) {
+    *dst = v;
+    *ticket = 0u;
+  }
+}
+
+// dst = <u, v> = sum conj(u) v
+__global__ void __launch_bounds__(kReduceThreads) k_dot(const cd* __restrict__ u, const cd* __restrict__ v,
+                                                        long long n, cd* partials, unsigned* ticket, cd* dst) {
+  cd acc = mkc(0.0, 0.0);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    acc = c_conjmul_acc(acc, u[p], v[p]);
+  acc = block_sum(acc);
+  grid_finish(acc, partials, ticket, dst);
+}
+
+// Fused MGS step (krylov.py:121-124):  w -= h * vi  (h = *hsrc, numpy complex
+// scalar*array then subtract);  then dst = <vn, w_new> (vn = w for the norm).
+// vi == nullptr skips the update (first dot of the chain).
+__global__ void __launch_bounds__(kReduceThreads) k_mgs(cd* __restrict__ w, const cd* __restrict__ vi,
+                                                        const cd* hsrc, const cd* __restrict__ vn, long long n,
+                                                        cd* partials, unsigned* ticket, cd* dst) {
+  const cd h = vi ? *hsrc : mkc(0.0, 0.0);
+  cd acc = mkc(0.0, 0.0);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    cd x = w[p];
+    if (vi) {
+      x = c_sub(x, c_mul_np(h, vi[p]));
+      w[p] = x;
+    }
+    const cd a = vn ? vn[p] : x;
+    acc = c_conjmul_acc(acc, a, x);
+  }
+  acc = block_sum(acc);
+  grid_finish(acc, partials, ticket, dst);
+}
+
+// dst = ||b - t||^2 (real part) without storing the difference (krylov.py:174)
+__global__ void __launch_bounds__(kReduceThreads) k_subnorm(const cd* __restrict__ b, const cd* __restrict__ t,
+                                                            long long n, cd* partials, unsigned* ticket, cd* dst) {
+  cd acc = mkc(0.0, 0.0);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const cd d = c_sub(b[p], t[p]);
+    acc = c_conjmul_acc(acc, d, d);
+  }
+  acc = block_sum(acc);
+  grid_finish(acc, partials, ticket, dst);
+}
+
+// out = x * inv   (numpy  x / beta  ==  (x.re * (1/beta), x.im * (1/beta)))
+__global__ void k_scale(const cd* __restrict__ x, cd* __restrict__ out, double inv, long long n) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const cd v = x[p];
+    out[p] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+  }
+}
+
+// x = x0 + sum_i y_i * B_i, terms added in order (krylov.py:169-172); x0 may be null (zeros)
+__global__ void k_lincomb(const cd* const* __restrict__ basis, const cd* __restrict__ y, int m,
+                          const cd* __restrict__ x0, cd* __restrict__ x, long long n) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    cd acc = x0 ? x0[p] : mkc(0.0, 0.0);
+    for (int i = 0; i < m; ++i) acc = c_add(acc, c_mul_np(y[i], basis[i][p]));
+    x[p] = acc;
+  }
+}
+
+// out = a + b   /  out = a - b
+__global__ void k_add(const cd* __restrict__ a, const cd* __restrict__ b, cd* __restrict__ out, long long n, int sub) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    out[p] = sub ? c_sub(a[p], b[p]) : c_add(a[p], b[p]);
+}
+
+// small dense complex GEMV  x = Ainv b  (MG coarsest solve, n <= 4096)
+__global__ void __launch_bounds__(256) k_gemv(const cd* __restrict__ A, const cd* __restrict__ b, cd* __restrict__ x,
+                                              int n) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= n) return;
+  const cd* row = A + (long long)warp * n;
+  cd acc = mkc(0.0, 0.0);
+  for (int c = lane; c < n; c += 32) {
+    const cd a = row[c], v = b[c];
+    acc.x = __fma_rn(a.x, v.x, acc.x); acc.x = __fma_rn(-a.y, v.y, acc.x);
+    acc.y = __fma_rn(a.x, v.y, acc.y); acc.y = __fma_rn(a.y, v.x, acc.y);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) x[warp] = acc;
+}
+
+// MG divergence guard (mg.py:133-138): flag |= sqrt(post2) > guard*sqrt(bn2)
+__global__ void k_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag) {
+  const double post = sqrt(fmax(post2->x, 0.0)), bn = sqrt(fmax(bn2->x, 0.0));
+  const double r0 = r02 ? sqrt(fmax(r02->x, 0.0)) : bn;
+  if (bn > 0.0 && post > guard * fmax(r0, bn)) flag->x = 1.0;
+}
+
+static inline int ew_blocks(long long n) {
+  long long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  return (int)(b < 1 ? 1 : b);
+}
+
+void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
+  k_dot<<<reduce_blocks(n), kReduceThreads, 0, st>>>(u, v, n, ws.partials, ws.ticket, dst);
+}
+void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
+  k_mgs<<<reduce_blocks(n), kReduceThreads, 0, st>>>(w, vi, hsrc, vn, n, ws.partials, ws.ticket, dst);
+}
+void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
+  k_subnorm<<<reduce_blocks(n), kReduceThreads, 0, st>>>(b, t, n, ws.partials, ws.ticket, dst);
+}
+void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st) {
+  k_scale<<<ew_blocks(n), 256, 0, st>>>(x, out, inv, n);
+}
+void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd* x, long long n, cudaStream_t st) {
+  k_lincomb<<<ew_blocks(n), 256, 0, st>>>(basis, y, m, x0, x, n);
+}
+void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st) {
+  k_add<<<ew_blocks(n), 256, 0, st>>>(a, b, out, n, sub);
+}
+void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st) {
+  k_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(A, b, x, n);
+}
+void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st) {
+  k_guard<<<1, 1, 0, st>>>(post2, bn2, r02, guard, flag);
+}
+
+}  // namespace hdb

@@ -1,0 +1,129 @@
+// Level-operator kernels: radius-1 (5-point) and radius-2/3 (Galerkin 5x5 /
+// 7x7) matrix-free applies with fused epilogues, and damped Jacobi.
+//
+// Reference: _kernels.py:14-68, operators.py:130-178, mg.py:88-102.
+// Memory-bound: 40 B/pt algorithmic for an apply (u 16 + k^2 8 + out 16),
+// 56 B/pt for the residual / A-DEF1 form (+ b 16), 56 B/pt per Jacobi sweep.
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace hdb {
+
+// ------------------------------------------------------------------------
+// radius 1.  One thread per point; neighbours come through L1 (32x8 tiles).
+// mode 0: out = A u            (pinned rows: u)
+// mode 1: out = b - A u        (pinned rows: b - u)          [residual / A-DEF1]
+// mode 2: out = u + (w dinv)(b - A u)   (pinned: u + w(b - u)) [Jacobi sweep]
+// mode 3: out = (w dinv) b     (pinned: w b)                  [Jacobi from x = 0]
+// ------------------------------------------------------------------------
+template <int MODE>
+__global__ void __launch_bounds__(256) k_r1(const cd* __restrict__ u, const cd* __restrict__ b,
+                                            const double* __restrict__ k, cd* __restrict__ out,
+                                            Geom g, OpCoef c, double omega) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;  // local row
+  if (i >= g.nx || j >= g.ny) return;
+  const int gj = j + g.row0;
+  const long long p = (long long)j * g.nx + i;
+  if (MODE == 3) {
+    const cd bb = b[p];
+    if (pinned(g, c, gj, i)) { out[p] = c_scale(omega, bb); return; }
+    const cd d = dinv_at(k, g, c, gj, i);
+    out[p] = c_mul(c_scale(omega, d), bb);
+    return;
+  }
+  const cd uc = u[p];
+  if (pinned(g, c, gj, i)) {
+    if (MODE == 0) out[p] = uc;
+    else if (MODE == 1) out[p] = c_sub(b[p], uc);
+    else out[p] = c_add(uc, c_scale(omega, c_sub(b[p], uc)));
+    return;
+  }
+  const cd w = upad(u, k, g, c, gj, i - 1);
+  const cd e = upad(u, k, g, c, gj, i + 1);
+  const cd so = upad(u, k, g, c, gj - 1, i);
+  const cd no = upad(u, k, g, c, gj + 1, i);
+  const cd Au = five_point(c.s, c.mc, k[p], uc, w, e, so, no);
+  if (MODE == 0) { out[p] = Au; return; }
+  const cd r = c_sub(b[p], Au);
+  if (MODE == 1) { out[p] = r; return; }
+  const cd d = dinv_at(k, g, c, gj, i);
+  out[p] = c_add(uc, c_mul(c_scale(omega, d), r));
+}
+
+// ------------------------------------------------------------------------
+// radius 2/3: shared-memory tile of the ghost-closed u and k^2 windows, then
+// the reference's row-major tap order (_kernels.py:44-50):
+//   acc += (lap[o] + mass[o]*kpad) * upad
+// mode 0: out = A u ; mode 1: out = b - A u (pinned rows: u / b - u)
+// ------------------------------------------------------------------------
+constexpr int TX = 32, TY = 8;
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const cd* __restrict__ b,
+                                               const double* __restrict__ k, cd* __restrict__ out,
+                                               Geom g, OpCoef c) {
+  constexpr int W = TX + 2 * R, H = TY + 2 * R, N = 2 * R + 1;
+  __shared__ cd su[H][W];
+  __shared__ double sk[H][W];
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * TY;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  for (int t = tid; t < H * W; t += TX * TY) {
+    const int ty = t / W, tx = t % W;
+    const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+    su[ty][tx] = upad(u, k, g, c, gj, gi);
+    sk[ty][tx] = kpad(k, g, c, gj, gi);
+  }
+  __syncthreads();
+  const int i = i0 + threadIdx.x, j = j0 + threadIdx.y;
+  if (i >= g.nx || j >= g.ny) return;
+  const int gj = j + g.row0;
+  const long long p = (long long)j * g.nx + i;
+  if (pinned(g, c, gj, i)) {
+    const cd uc = su[threadIdx.y + R][threadIdx.x + R];
+    out[p] = MODE == 0 ? uc : c_sub(b[p], uc);
+    return;
+  }
+  cd acc = mkc(0.0, 0.0);
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+#pragma unroll
+    for (int bb = 0; bb < N; ++bb) {
+      const double kp = sk[threadIdx.y + a][threadIdx.x + bb];
+      const cd m = c.mass[a * N + bb];
+      const cd coef = mkc(__dadd_rn(c.lap[a * N + bb], __dmul_rn(m.x, kp)), __dmul_rn(m.y, kp));
+      acc = c_add(acc, c_mul(coef, su[threadIdx.y + a][threadIdx.x + bb]));
+    }
+  }
+  out[p] = MODE == 0 ? acc : c_sub(b[p], acc);
+}
+
+// ------------------------------------------------------------------------
+static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny + 7) / 8); }
+
+void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
+                  int mode, cudaStream_t st) {
+  if (c.radius == 1) {
+    const dim3 blk(32, 8), grd = grid_r1(g);
+    if (mode == 0) k_r1<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+    else k_r1<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+    return;
+  }
+  const dim3 blk(TX, TY), grd((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
+  if (c.radius == 2) {
+    if (mode == 0) k_rg<2, 0><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+    else k_rg<2, 1><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+  } else {
+    if (mode == 0) k_rg<3, 0><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+    else k_rg<3, 1><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+  }
+}
+
+void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out,
+                   double omega, bool from_zero, cudaStream_t st) {
+  const dim3 blk(32, 8), grd = grid_r1(g);
+  if (from_zero) k_r1<3><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+  else k_r1<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+}
+
+}  // namespace hdb

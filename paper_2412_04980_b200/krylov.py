@@ -1,0 +1,138 @@
+"""Flexible GMRES / GMRES on the GPU (drop-in for reference krylov.py:31-182, 279-283).
+
+The Arnoldi process runs in the CUDA library (csrc/engine.cu): fused MGS
+launches (one per Hessenberg coefficient), deterministic device reductions,
+one device->host read of the Hessenberg column per iteration, Givens
+rotations and the least-squares update on the host (as in the reference).
+
+``apply_A`` / ``apply_M`` may be:
+  * a GPU ``LevelOperator.apply`` bound method, a ``CslpMultigrid.vcycle``
+    bound method, or any object with a ``_device_apply(in_ptr, out_ptr)``
+    method -> called on device buffers directly;
+  * any other callable -> called with arrays of ``b``'s kind (numpy in,
+    numpy out for numpy ``b``; torch CUDA tensors for a CUDA ``b``).
+``dot`` is accepted for signature compatibility; the library's deterministic
+conj-first device reduction is always used (the contract of reduce_dot,
+parallel.py:168-195: conj(u).v, independent of the number of workers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import device as dev
+from ._lib import ITER_FN, LINOP_FN, check, lib
+
+__all__ = ["StopRule", "KrylovReport", "fgmres", "gmres", "cslp_iteration_cap", "device_callable"]
+
+
+@dataclass(frozen=True)
+class StopRule:
+    """Relative tolerance plus iteration cap (tol >= 1 => exactly one iteration)."""
+
+    rel_tol: float
+    max_iters: int
+
+    def __post_init__(self):
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.rel_tol < 0:
+            raise ValueError("rel_tol must be nonnegative")
+
+
+@dataclass
+class KrylovReport:
+    iterations: int
+    final_relres: float
+    residual_history: list = field(default_factory=list)
+    converged: bool = False
+
+
+def cslp_iteration_cap(level_size: int, c_it: float = 6.0) -> int:
+    """ceil(c_it * N**(1/4)) (krylov.py:279-283)."""
+    if level_size < 1:
+        raise ValueError("level size must be >= 1")
+    return int(math.ceil(c_it * float(level_size) ** 0.25 - 1e-9))
+
+
+def device_callable(fn):
+    """Return f(in_ptr, out_ptr) running on device buffers, or None."""
+    obj = getattr(fn, "__self__", None)
+    name = getattr(fn, "__name__", "")
+    if obj is not None and hasattr(obj, "_device_apply") and name in ("apply", "vcycle", "_device_apply"):
+        return obj._device_apply
+    if hasattr(fn, "_device_apply"):
+        return fn._device_apply
+    return None
+
+
+class _Bridge:
+    """ctypes callback adapter that records the first Python exception."""
+
+    def __init__(self, fn, shape, host: bool):
+        self.fn, self.shape, self.host = fn, shape, host
+        self.dfn = device_callable(fn) if fn is not None else None
+        self.error = None
+        self.cfunc = LINOP_FN(self._call)
+
+    def _call(self, _user, pin, pout):
+        try:
+            if self.dfn is not None:
+                self.dfn(pin, pout)
+                return 0
+            vin = dev.raw_view(pin, self.shape)
+            vout = dev.raw_view(pout, self.shape)
+            if self.host:
+                res = self.fn(vin.cpu().numpy())
+                vout.copy_(dev.to_device(np.asarray(res, dtype=np.complex128).reshape(self.shape)))
+            else:
+                res = self.fn(vin.clone())
+                vout.copy_(res.reshape(self.shape))
+            return 0
+        except BaseException as err:  # noqa: BLE001 - re-raised after the C call
+            if self.error is None:
+                self.error = err
+            return 1
+
+
+def fgmres(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None, on_iteration=None):
+    """Right-preconditioned flexible GMRES without restarts (krylov.py:61-177)."""
+    host = not dev.is_device(b)
+    shape = tuple(b.shape)
+    db = dev.to_device(b)
+    dx = dev.empty(shape)
+    dx0 = dev.to_device(x0) if x0 is not None else None
+    A = _Bridge(apply_A, shape, host)
+    M = _Bridge(apply_M, shape, host) if apply_M is not None else None
+    hook_err = []
+
+    def _hook(_u, it, rel):
+        try:
+            on_iteration(it, rel)
+            return 0
+        except BaseException as err:  # noqa: BLE001
+            hook_err.append(err)
+            return 1
+
+    hook = ITER_FN(_hook) if on_iteration is not None else ITER_FN()
+    cap = stop.max_iters + 1
+    hist = (C.c_double * cap)()
+    its, fin, conv = C.c_int(), C.c_double(), C.c_int()
+    st = lib().hdb_fgmres(db.numel(), A.cfunc, None, M.cfunc if M else LINOP_FN(), None, db.data_ptr(),
+                          dx0.data_ptr() if dx0 is not None else None, dx.data_ptr(), float(stop.rel_tol),
+                          int(stop.max_iters), hook, None, C.byref(its), C.byref(fin), C.byref(conv), hist, cap)
+    for err in (A.error, M.error if M else None, hook_err[0] if hook_err else None):
+        if err is not None:
+            raise err
+    check(st)
+    history = list(hist[: min(its.value + 1, cap)])
+    rep = KrylovReport(its.value, fin.value, history, bool(conv.value))
+    return (dev.to_host(dx) if host else dx), rep
+
+
+def gmres(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None, on_iteration=None):
+    """GMRES with a fixed right preconditioner (same engine as fgmres)."""
+    return fgmres(apply_A, apply_M, b, stop, x0=x0, dot=dot, on_iteration=on_iteration)
