@@ -174,6 +174,8 @@ def kernel_roofline(hdb, hier, reps=20):
     d = (C.c_double * 2)()
     t = timeit(lambda: L.hdb_dot(u.data_ptr(), out.data_ptr(), n, d))  # includes a host sync per call
     res["dot(sync)"] = (32.0 * n, t)
+    if hier.ml < 3:
+        return {k: {"bytes": bts, "ms": tt * 1e3, "gbs": bts / tt / 1e9} for k, (bts, tt) in res.items()}
     op3 = hdb.helmholtz_operator(hier, 3)
     l3 = hier.level(3)
     u3 = torch.from_numpy(rng.standard_normal(l3.shape) + 1j * rng.standard_normal(l3.shape)).cuda()

@@ -111,6 +111,11 @@ int hdb_solver_counts(hdb_solver* s, int level, int kind, int* buf_host, int cap
 int hdb_solver_matvecs(hdb_solver* s, long long* buf_host, int cap);
 /* MadpSolver.apply_preconditioner (madp.py:301-327) on device vectors */
 int hdb_solver_precond(hdb_solver* s, int level, const void* v, void* out);
+/* telemetry of the last solve: inclusive host ms and call counts per
+ * (level, role) at index level*3 + role (0 deflation FGMRES, 1 CSLP, 2 A-DEF1),
+ * host synchronisations and kernel launches                                   */
+int hdb_solver_profile(hdb_solver* s, double* ms_host, long long* calls_host, int cap,
+                       long long* syncs, long long* launches);
 int hdb_solver_destroy(hdb_solver* s);
 
 #ifdef __cplusplus

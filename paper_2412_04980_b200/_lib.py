@@ -51,6 +51,7 @@ SIGNATURES = {
     "hdb_solver_counts": [vp, i32, i32, P(i32), i32, P(i32)],
     "hdb_solver_matvecs": [vp, P(i64), i32],
     "hdb_solver_precond": [vp, i32, vp, vp],
+    "hdb_solver_profile": [vp, P(f64), P(i64), i32, P(i64), P(i64)],
     "hdb_solver_destroy": [vp],
 }
 _RESTYPE = {"hdb_last_error": C.c_char_p}

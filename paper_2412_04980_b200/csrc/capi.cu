@@ -299,7 +299,20 @@ int hdb_solver_precond(hdb_solver* s, int level, const void* v, void* out) {
     HDB_CUDA(cudaMemsetAsync(E.dscal + kSlotFlag, 0, sizeof(cd), E.st));
     s->s.precond(level, (const cd*)v, (cd*)out);
     check_launch();
+    s->s.flush_counts();
     E.fetch(1);
+  });
+}
+int hdb_solver_profile(hdb_solver* s, double* ms_host, long long* calls_host, int cap, long long* syncs,
+                       long long* launches) {
+  return guarded([&] {
+    const SolveReport& r = s->s.rep;
+    for (int i = 0; i < cap && i < (int)r.prof_ms.size(); ++i) {
+      ms_host[i] = r.prof_ms[i];
+      calls_host[i] = r.prof_calls[i];
+    }
+    *syncs = r.syncs;
+    *launches = r.launches;
   });
 }
 int hdb_solver_destroy(hdb_solver* s) {

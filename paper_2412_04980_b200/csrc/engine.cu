@@ -6,6 +6,7 @@
 //   MadpSolver        madp.py:220-371 (apply_preconditioner 301-327, _solve_cslp 277-299)
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 
@@ -53,12 +54,13 @@ void Engine::free(void* p) {
 }
 
 void Engine::fetch(int count) {
+  syncs++;
   HDB_CUDA(cudaMemcpyAsync(hscal, dscal, sizeof(cd) * count, cudaMemcpyDeviceToHost, st));
   HDB_CUDA(cudaStreamSynchronize(st));
-  if (hscal[kSlotFlag].x != 0.0) {
-    // leave the flag set for inspection; solver entry points clear it
+  // leave the flag set for inspection; solver entry points clear it
+  if (hscal[kSlotFlag].x == 1.0)
     throw Error(E_MGDIV, "multigrid V-cycle residual exceeded the divergence guard (mg.py:135-138)");
-  }
+  if (hscal[kSlotFlag].x == 2.0) throw Error(E_NONFINITE, "non-finite value in a device-resident Krylov solve");
 }
 
 double Engine::fetch_norm(int slot) {
@@ -129,6 +131,40 @@ KWS::~KWS() {
   for (auto p : Z) E.free(p);
   E.free(tmp);
   if (dbasis) { E.free(dbasis); E.free(dy); cudaFreeHost(hbasis); cudaFreeHost(hy); }
+}
+
+// ------------------------------------------------------ small-level solves
+long long small_level_limit() {
+  static long long lim = -1;
+  if (lim < 0) {
+    const char* e = getenv("HDB_SMALL_N");
+    lim = e ? atoll(e) : 70000;
+  }
+  return lim;
+}
+
+void SmallSolve::ensure(const LevelOp* o, int cap_) {
+  if (op == o && cap >= cap_) return;
+  Engine& E = engine();
+  if (basis) E.free(basis);
+  op = o;
+  cap = cap_;
+  basis = E.alloc((long long)(cap + 1) * o->n);
+}
+
+void SmallSolve::run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {
+  Engine& E = engine();
+  launch_small_gmres(op->c, op->g, op->ksq, b, x, basis, op->n, stop.rel_tol, stop.max_iters, its_dev, rel_dev,
+                     E.dscal + kSlotFlag, E.st);
+  E.launches++;
+}
+
+SmallSolve::~SmallSolve() {
+  if (basis && engine_ready()) engine().free(basis);
+}
+
+static bool use_small(long long n, int cap) {
+  return n <= small_level_limit() && cap <= small_gmres_max_cap();
 }
 
 // ----------------------------------------------------------------- FGMRES
@@ -313,6 +349,10 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
     if (Ainv) {
       launch_gemv(Ainv, b, x, ninv, E.st);
       E.launches++;
+    } else if (use_small(ops[i]->n, coarse_stop.max_iters)) {
+      small_coarse.ensure(ops[i], coarse_stop.max_iters);
+      Engine& E2 = engine();
+      small_coarse.run(b, x, coarse_stop, (int*)(E2.dscal + kSlotMisc), (double*)(E2.dscal + kSlotMisc) + 1);
     } else {
       const LevelOp* op = ops[i];
       LinOp A = [op](const cd* in, cd* out) { op->apply(in, out); };
@@ -385,6 +425,11 @@ void MadpSolver::set_levels(int ml_) {
 
 void MadpSolver::setup() {
   Engine& E = engine();
+  if (!dcounts) {
+    dcap = 1 << 16;
+    dcounts = (int*)E.alloc_bytes(sizeof(int) * dcap);
+    drel = (double*)E.alloc_bytes(sizeof(double) * dcap);
+  }
   for (int l = 1; l <= ml; ++l) {
     MadpLevel& L = lv[l];
     if (!L.A) throw Error(E_ARG, "level operator missing");
@@ -400,14 +445,33 @@ MadpSolver::~MadpSolver() {
   for (auto& L : lv) {
     for (cd* p : {L.vhat, L.vtil, L.t, L.rhs, L.r}) E.free(p);
   }
+  E.free(dcounts);
+  E.free(drel);
 }
 
 void MadpSolver::reset_report() {
   rep = SolveReport();
+  dused = 0;
+  pending.clear();
   rep.cycle_iters.assign(ml + 1, {});
   rep.cslp_iters.assign(ml + 1, {});
   rep.matvecs.assign(ml + 1, 0);
+  rep.prof_ms.assign((ml + 1) * PROF_KINDS, 0.0);
+  rep.prof_calls.assign((ml + 1) * PROF_KINDS, 0);
 }
+
+namespace {
+struct ProfScope {
+  SolveReport& r;
+  int slot;
+  std::chrono::steady_clock::time_point t0;
+  ProfScope(SolveReport& r_, int level, int kind) : r(r_), slot(level * PROF_KINDS + kind), t0(std::chrono::steady_clock::now()) {}
+  ~ProfScope() {
+    r.prof_ms[slot] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    r.prof_calls[slot] += 1;
+  }
+};
+}  // namespace
 
 void MadpSolver::A(int l, const cd* u, cd* out) {
   rep.matvecs[l] += 1;  // madp.py:271-273
@@ -416,6 +480,7 @@ void MadpSolver::A(int l, const cd* u, cd* out) {
 
 // madp.py:277-299
 void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
+  ProfScope ps(rep, l, PROF_CSLP);
   MadpLevel& L = lv[l];
   Engine& E = engine();
   if (L.cslp == CSLP_NONE) {
@@ -428,13 +493,36 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     return;
   }
   const LevelOp* M = L.M;
+  if (use_small(M->n, L.cslp_stop.max_iters)) {
+    if (dused >= dcap) flush_counts();
+    L.small_cslp.ensure(M, L.cslp_stop.max_iters);
+    L.small_cslp.run(rhs, out, L.cslp_stop, dcounts + dused, drel + dused);
+    rep.cslp_iters[l].push_back(-1);
+    pending.emplace_back(l, (int)rep.cslp_iters[l].size() - 1);
+    dused++;
+    return;
+  }
   LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
   KReport r = fgmres(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_cslp);
   rep.cslp_iters[l].push_back(r.iterations);
 }
 
+// copy device-resident iteration counts into the report
+void MadpSolver::flush_counts() {
+  Engine& E = engine();
+  if (dused > 0) {
+    std::vector<int> h(dused);
+    HDB_CUDA(cudaMemcpyAsync(h.data(), dcounts, sizeof(int) * dused, cudaMemcpyDeviceToHost, E.st));
+    E.fetch(1);  // sync + flag check
+    for (int k = 0; k < dused; ++k) rep.cslp_iters[pending[k].first][pending[k].second] = h[k];
+  }
+  dused = 0;
+  pending.clear();
+}
+
 // madp.py:301-327  (A-DEF1, lambda = 1)
 void MadpSolver::precond(int l, const cd* v, cd* out) {
+  ProfScope ps(rep, l, PROF_ADEF);
   Engine& E = engine();
   MadpLevel& L = lv[l];
   MadpLevel& N = lv[l + 1];
@@ -445,7 +533,11 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   LinOp Mop;
   if (nxt == ml) Mop = [this, nxt](const cd* in, cd* o) { cslp_apply(nxt, in, o); };
   else Mop = [this, nxt](const cd* in, cd* o) { precond(nxt, in, o); };
-  KReport r = fgmres(N.A->n, Aop, &Mop, N.vhat, N.vtil, N.cycle_stop, N.ws_defl);
+  KReport r;
+  {
+    ProfScope pd(rep, nxt, PROF_DEFL);
+    r = fgmres(N.A->n, Aop, &Mop, N.vhat, N.vtil, N.cycle_stop, N.ws_defl);
+  }
   rep.cycle_iters[nxt].push_back(r.iterations);
   launch_prolong(N.vtil, nullptr, L.t, L.A->g.nx, L.A->g.ny, 0, E.st);
   E.launches++;
@@ -465,6 +557,7 @@ void MadpSolver::solve(const cd* b, cd* x) {
   HDB_CUDA(cudaEventCreate(&e0));
   HDB_CUDA(cudaEventCreate(&e1));
   HDB_CUDA(cudaEventRecord(e0, E.st));
+  const long long s0 = E.syncs, l0 = E.launches;
   const auto t0 = std::chrono::steady_clock::now();
   std::function<void(int, double)> hook = [this, t0](int, double) {
     rep.iter_wall_ms.push_back(
@@ -474,6 +567,7 @@ void MadpSolver::solve(const cd* b, cd* x) {
   LinOp Mop = [this](const cd* in, cd* o) { precond(1, in, o); };
   try {
     rep.outer = fgmres(lv[1].A->n, Aop, &Mop, b, x, outer, lv[1].ws_defl, &hook);
+    flush_counts();
   } catch (...) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -484,6 +578,8 @@ void MadpSolver::solve(const cd* b, cd* x) {
   float ms = 0.f;
   HDB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   rep.wall_ms = ms;
+  rep.syncs = E.syncs - s0;
+  rep.launches = E.launches - l0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 }

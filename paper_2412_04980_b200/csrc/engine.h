@@ -45,6 +45,7 @@ struct Engine {
   cd* hscal = nullptr;   // pinned host mirror
   size_t bytes_alloc = 0;
   long long launches = 0;  // kernels launched through the engine (telemetry)
+  long long syncs = 0;     // host synchronisations (Hessenberg reads etc.)
 
   explicit Engine(int dev);
   ~Engine();
@@ -106,12 +107,26 @@ struct KWS {
 KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
                const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr);
 
+// small-level Krylov solves run device-resident (one cluster launch per solve)
+long long small_level_limit();  // points; env HDB_SMALL_N (0 disables)
+
+struct SmallSolve {  // device-resident GMRES on one level operator
+  const LevelOp* op = nullptr;
+  cd* basis = nullptr;
+  int cap = 0;
+  void ensure(const LevelOp* o, int cap_);
+  // launches; iteration count lands in *its_dev, final relres in *rel_dev
+  void run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev);
+  ~SmallSolve();
+};
+
 struct Multigrid {
   std::vector<const LevelOp*> ops;  // sub-levels, finest first
   std::vector<cd*> X, Y, R, B, O;   // per-level scratch (X,Y,R), rhs (B), output (O)
   cd* Ainv = nullptr;               // coarsest dense inverse (n <= direct limit)
   int ninv = 0;
   KWS coarse_ws;
+  SmallSolve small_coarse;
   Stop coarse_stop{1e-8, 50};
   double omega = 0.8, guard = 10.0;
   int pre = 1, post = 1;
@@ -130,12 +145,19 @@ struct MadpLevel {
   int cslp = CSLP_NONE;
   Stop cslp_stop{0.1, 1}, cycle_stop{1.0, 1};
   KWS ws_defl, ws_cslp;
+  SmallSolve small_cslp;
   cd *vhat = nullptr, *vtil = nullptr;        // this level's input / output as a deflation system
   cd *t = nullptr, *rhs = nullptr, *r = nullptr;  // A-DEF1 temporaries of P_l
 };
 
+// inclusive host wall time per level and role (telemetry for DESIGN.md / profiles/)
+enum { PROF_DEFL = 0, PROF_CSLP = 1, PROF_ADEF = 2, PROF_KINDS = 3 };
+
 struct SolveReport {
   KReport outer;
+  std::vector<double> prof_ms;        // (ml+1) * PROF_KINDS
+  std::vector<long long> prof_calls;  // same layout
+  long long syncs = 0, launches = 0;
   std::vector<std::vector<int>> cycle_iters, cslp_iters;  // index = level
   std::vector<long long> matvecs;
   std::vector<double> iter_wall_ms;
@@ -144,6 +166,11 @@ struct SolveReport {
 
 struct MadpSolver {
   int ml = 0;
+  int* dcounts = nullptr;      // device iteration counts of device-resident solves
+  double* drel = nullptr;
+  int dcap = 0, dused = 0;
+  std::vector<std::pair<int, int>> pending;  // (level, index into cslp_iters[level]) per slot
+  void flush_counts();
   std::vector<MadpLevel> lv;  // index 1..ml
   Stop outer{1e-6, 150};
   SolveReport rep;

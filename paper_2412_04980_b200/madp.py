@@ -271,6 +271,20 @@ class MadpSolver:
         rep = self.report(wall_ms=(time.perf_counter() - t0) * 1e3)
         return out, rep
 
+    def profile(self) -> dict:
+        """Per-level inclusive host time of the last solve (telemetry)."""
+        ml = self.hierarchy.ml
+        n = (ml + 1) * 3
+        ms, calls = (C.c_double * n)(), (C.c_longlong * n)()
+        syncs, launches = C.c_longlong(), C.c_longlong()
+        check(lib().hdb_solver_profile(self.handle, ms, calls, n, C.byref(syncs), C.byref(launches)))
+        roles = ("deflation_fgmres", "cslp", "adef1")
+        out = {"syncs": syncs.value, "launches": launches.value, "levels": {}}
+        for l in range(1, ml + 1):
+            out["levels"][l] = {roles[k]: {"ms": round(ms[l * 3 + k], 3), "calls": calls[l * 3 + k]}
+                                for k in range(3) if calls[l * 3 + k]}
+        return out
+
     def report(self, wall_ms=None) -> ConvergenceReport:
         L = lib()
         h = self.handle
