@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <memory>
 
 #include "engine.h"
@@ -133,39 +134,55 @@ KWS::~KWS() {
   if (dbasis) { E.free(dbasis); E.free(dy); cudaFreeHost(hbasis); cudaFreeHost(hy); }
 }
 
-// ------------------------------------------------------ small-level solves
-long long small_level_limit() {
-  static long long lim = -1;
-  if (lim < 0) {
-    const char* e = getenv("HDB_SMALL_N");
-    lim = e ? atoll(e) : 70000;
+// ------------------------------------------------- device-resident solves
+static long long env_ll(const char* name, long long dflt) {
+  const char* e = getenv(name);
+  return e ? atoll(e) : dflt;
+}
+
+int resident_mode(long long n, int cap) {
+  static long long small = -1, grid = -1;
+  if (small < 0) {
+    small = std::min(env_ll("HDB_SMALL_N", 70000), resident_cluster_points());
+    grid = std::min(env_ll("HDB_GRID_N", 2000000), resident_grid_points());
   }
-  return lim;
+  if (cap > resident_max_cap()) return -1;
+  if (n <= small) return 0;
+  if (n <= grid) return 1;
+  return -1;
 }
 
 void SmallSolve::ensure(const LevelOp* o, int cap_) {
   if (op == o && cap >= cap_) return;
   Engine& E = engine();
-  if (basis) E.free(basis);
+  E.free(basis);
+  E.free(Rg);
+  E.free(gpart);
   op = o;
   cap = cap_;
   basis = E.alloc((long long)(cap + 1) * o->n);
+  Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap);
+  gpart = E.alloc(2LL * resident_grid_ctas());
 }
 
 void SmallSolve::run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {
   Engine& E = engine();
-  launch_small_gmres(op->c, op->g, op->ksq, b, x, basis, op->n, stop.rel_tol, stop.max_iters, its_dev, rel_dev,
-                     E.dscal + kSlotFlag, E.st);
+  const int mode = resident_mode(op->n, stop.max_iters);
+  if (mode < 0 || launch_resident_gmres(mode, op->c, op->g, op->ksq, b, x, basis, Rg, gpart, op->n, stop.rel_tol,
+                                        stop.max_iters, its_dev, rel_dev, E.dscal + kSlotFlag, E.st) != 0)
+    throw Error(E_CUDA, std::string("device-resident GMRES launch failed: ") + cudaGetErrorString(cudaGetLastError()));
   E.launches++;
 }
 
 SmallSolve::~SmallSolve() {
-  if (basis && engine_ready()) engine().free(basis);
+  if (!engine_ready()) return;
+  Engine& E = engine();
+  E.free(basis);
+  E.free(Rg);
+  E.free(gpart);
 }
 
-static bool use_small(long long n, int cap) {
-  return n <= small_level_limit() && cap <= small_gmres_max_cap();
-}
+static bool use_small(long long n, int cap) { return resident_mode(n, cap) >= 0; }
 
 // ----------------------------------------------------------------- FGMRES
 static const double kHappy = 1e-30;  // krylov.py:28

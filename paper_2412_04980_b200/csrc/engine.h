@@ -107,12 +107,17 @@ struct KWS {
 KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
                const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr);
 
-// small-level Krylov solves run device-resident (one cluster launch per solve)
-long long small_level_limit();  // points; env HDB_SMALL_N (0 disables)
+// Krylov solves on levels that fit the resident working set run as ONE
+// device-resident launch (kernels_resident.cu): cluster mode up to
+// HDB_SMALL_N points (default 70k), whole-grid cooperative mode up to
+// HDB_GRID_N points (default 2.0M, capped by shared memory).  0 disables.
+int resident_mode(long long n, int cap);  // -1: launch-driven path
 
 struct SmallSolve {  // device-resident GMRES on one level operator
   const LevelOp* op = nullptr;
   cd* basis = nullptr;
+  cd* Rg = nullptr;
+  cd* gpart = nullptr;
   int cap = 0;
   void ensure(const LevelOp* o, int cap_);
   // launches; iteration count lands in *its_dev, final relres in *rel_dev

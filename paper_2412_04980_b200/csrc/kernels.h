@@ -28,11 +28,14 @@ void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStr
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st);
 void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st);
 
-// device-resident GMRES on one thread-block cluster (kernels_cluster.cu)
-int small_gmres_max_cap();
-int small_gmres_cluster();
-void launch_small_gmres(const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x, cd* basis,
-                        long long n, double tol, int cap, int* its_out, double* relres_out, cd* flag,
-                        cudaStream_t st);
+// device-resident GMRES (kernels_resident.cu).  mode 0: one cluster, 1: whole grid
+// (cooperative).  Returns nonzero when the problem does not fit that mode.
+int resident_max_cap();
+long long resident_cluster_points();
+long long resident_grid_points();
+int resident_grid_ctas();
+int launch_resident_gmres(int mode, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
+                          cd* basis, cd* Rg, cd* gpart, long long n, double tol, int cap, int* its_out,
+                          double* relres_out, cd* flag, cudaStream_t st);
 
 }  // namespace hdb

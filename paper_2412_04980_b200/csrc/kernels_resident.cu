@@ -1,0 +1,427 @@
+// Device-resident GMRES: a whole unrestarted GMRES solve (krylov.py:61-177
+// with apply_M = None) — operator applies, modified Gram-Schmidt, Givens
+// rotations, stopping test, least squares, solution update and the explicit
+// final residual — in ONE launch.  Used for every CSLP-GMRES and MG-coarsest
+// GMRES on levels that fit the resident working set.
+//
+// Why: in the launch-driven engine every MGS coefficient is a kernel launch
+// and every Arnoldi step a host round trip for the Hessenberg column
+// (measured 168 us per GMRES iteration on the 65^2 level of BASELINE config 2,
+// profiles/).  Resident, a step costs one barrier + a deterministic reduction.
+//
+// Two synchronisation policies share the solver body:
+//   ClusterSync  one thread-block cluster (<= 16 CTAs), partials through DSMEM,
+//                barrier.cluster — small levels (<= ~70k points);
+//   GridSync     cooperative launch over all SMs, partials through global
+//                memory, grid barrier — mid-size levels (<= ~2M points).
+// CTA r owns the flat point range [r*N/P, (r+1)*N/P); its slice of the Arnoldi
+// vector w lives in shared memory for the whole solve; basis vectors live in
+// global memory (L2-resident on small levels).  Reductions are deterministic
+// (fixed warp/block tree, then the P CTA partials combined in rank order by
+// every CTA, so all CTAs hold bit-identical scalars).  Stencil and vector
+// arithmetic is the same as the launch path.
+#include <cooperative_groups.h>
+
+#include "kernels.h"
+#include "stencil.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace hdb {
+
+constexpr int kRT = 512;        // threads per CTA
+constexpr int kMaxCap = 400;    // iteration cap supported by the device solver
+
+struct ResidentArgs {
+  OpCoef c;
+  Geom g;
+  const double* ksq;
+  const cd* b;
+  cd* x;
+  cd* basis;          // (cap + 1) vectors of n points
+  cd* Rg;             // packed upper-triangular R (cap*(cap+1)/2) + y (cap), written by rank 0
+  cd* gpart;          // GridSync: 2 * nranks partials
+  long long n;
+  double tol;
+  int cap;
+  int* its_out;
+  double* relres_out;
+  cd* flag;           // .x = 2.0 on a non-finite value (NumericalError)
+};
+
+struct RSmem {
+  cd warp[kRT / 32];
+  cd part[2];
+  cd bcast[2];
+  cd hcol[kMaxCap + 2];
+  cd sn[kMaxCap];
+  double cs[kMaxCap];
+  cd g[kMaxCap + 2];
+  int decision;
+};
+
+template <int R>
+__device__ __forceinline__ cd op_point(const OpCoef& c, const Geom& g, const cd* u, const double* k, int gj, int i) {
+  const long long p = (long long)(gj - g.row0) * g.nx + i;
+  if (pinned(g, c, gj, i)) return u[p];
+  if (R == 1) {
+    return five_point(c.s, c.mc, k[p], u[p], upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
+                      upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
+  }
+  constexpr int N = 2 * R + 1;
+  cd acc = mkc(0.0, 0.0);
+#pragma unroll 1
+  for (int a = 0; a < N; ++a) {
+#pragma unroll
+    for (int bb = 0; bb < N; ++bb) {
+      const int jj = gj + a - R, ii = i + bb - R;
+      const double kp = kpad(k, g, c, jj, ii);
+      const cd m = c.mass[a * N + bb];
+      const cd coef = mkc(__dadd_rn(c.lap[a * N + bb], __dmul_rn(m.x, kp)), __dmul_rn(m.y, kp));
+      acc = c_add(acc, c_mul(coef, upad(u, k, g, c, jj, ii)));
+    }
+  }
+  return acc;
+}
+
+__device__ __forceinline__ cd warp_sum_c(cd v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// block partial -> thread 0 (fixed tree)
+__device__ __forceinline__ cd block_partial(cd v, RSmem& s) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum_c(v);
+  if (lane == 0) s.warp[wid] = v;
+  __syncthreads();
+  cd t = mkc(0.0, 0.0);
+  if (wid == 0) {
+    t = lane < kRT / 32 ? s.warp[lane] : mkc(0.0, 0.0);
+    t = warp_sum_c(t);
+  }
+  return t;  // valid in thread 0
+}
+
+struct ClusterSync {
+  cg::cluster_group cl;
+  __device__ ClusterSync() : cl(cg::this_cluster()) {}
+  __device__ int rank() const { return (int)cl.block_rank(); }
+  __device__ int nranks() const { return (int)cl.num_blocks(); }
+  __device__ void barrier() { cl.sync(); }
+  __device__ cd reduce(cd v, RSmem& s, int& buf, cd*) {
+    const cd t = block_partial(v, s);
+    if (threadIdx.x == 0) s.part[buf] = t;
+    cl.sync();
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x < 32) {
+      cd q = mkc(0.0, 0.0);
+      if (lane < nranks()) q = *cl.map_shared_rank(&s.part[buf], lane);
+      q = warp_sum_c(q);
+      if (lane == 0) s.bcast[buf] = q;
+    }
+    __syncthreads();
+    const cd r = s.bcast[buf];
+    buf ^= 1;
+    return r;
+  }
+};
+
+struct GridSync {
+  cg::grid_group gr;
+  __device__ GridSync() : gr(cg::this_grid()) {}
+  __device__ int rank() const { return (int)blockIdx.x; }
+  __device__ int nranks() const { return (int)gridDim.x; }
+  __device__ void barrier() { gr.sync(); }
+  __device__ cd reduce(cd v, RSmem& s, int& buf, cd* gpart) {
+    const cd t = block_partial(v, s);
+    const int P = nranks();
+    if (threadIdx.x == 0) __stcg(&gpart[buf * P + blockIdx.x], t);
+    gr.sync();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      cd q = mkc(0.0, 0.0);
+      for (int r = lane; r < P; r += 32) {
+        const cd z = __ldcg(&gpart[buf * P + r]);
+        q.x += z.x;
+        q.y += z.y;
+      }
+      q = warp_sum_c(q);
+      if (lane == 0) s.bcast[buf] = q;
+    }
+    __syncthreads();
+    const cd r = s.bcast[buf];
+    buf ^= 1;
+    return r;
+  }
+};
+
+__device__ __forceinline__ double cabs_(cd z) { return hypot(z.x, z.y); }
+__device__ __forceinline__ cd cmul_(cd a, cd b) { return mkc(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ cd cdiv_(cd a, cd b) {
+  if (b.y == 0.0) return mkc(a.x / b.x, a.y / b.x);
+  const double d = b.x * b.x + b.y * b.y;
+  return mkc((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+
+template <class Sync, int R>
+__global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RSmem& s = *reinterpret_cast<RSmem*>(smem_raw);
+  cd* ws = reinterpret_cast<cd*>(smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);  // this CTA's slice of w
+  Sync sy;
+  const int P = sy.nranks(), rank = sy.rank();
+  const long long n = A.n;
+  const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
+  const int cnt = (int)(p1 - p0);
+  const int t = threadIdx.x;
+  const int nx = A.g.nx;
+  int buf = 0;
+  auto V = [&](int i) { return A.basis + (long long)i * n; };
+  cd* Rg = A.Rg;
+  cd* yg = A.Rg + (long long)A.cap * (A.cap + 1) / 2;
+
+  cd acc = mkc(0.0, 0.0);
+  for (int q = t; q < cnt; q += kRT) { const cd v = A.b[p0 + q]; acc = c_conjmul_acc(acc, v, v); }
+  const double bnorm = sqrt(fmax(sy.reduce(acc, s, buf, A.gpart).x, 0.0));
+  if (bnorm == 0.0) {  // krylov.py:96-97
+    for (int q = t; q < cnt; q += kRT) A.x[p0 + q] = mkc(0.0, 0.0);
+    if (rank == 0 && t == 0) { *A.its_out = 0; *A.relres_out = 0.0; }
+    return;
+  }
+  if (!isfinite(bnorm)) {
+    if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = 0; }
+    return;
+  }
+  const double beta = bnorm;  // r0 = b (zero initial guess); rel = 1 never triggers the early exit
+  {
+    const double inv = 1.0 / beta;
+    cd* v0 = V(0);
+    for (int q = t; q < cnt; q += kRT) {
+      const cd v = A.b[p0 + q];
+      v0[p0 + q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+    }
+  }
+  if (t == 0) s.g[0] = mkc(beta, 0.0);
+  int its = 0;
+  for (int j = 0; j < A.cap; ++j) {
+    sy.barrier();  // V_j complete everywhere
+    const cd* vj = V(j);
+    for (int q = t; q < cnt; q += kRT) {
+      const long long p = p0 + q;
+      ws[q] = op_point<R>(A.c, A.g, vj, A.ksq, (int)(p / nx) + A.g.row0, (int)(p % nx));
+    }
+    // modified Gram-Schmidt (krylov.py:121-124): h_i = <V_i, w>; w -= h_i V_i
+    for (int i = 0; i <= j; ++i) {
+      const cd* vi = V(i) + p0;
+      cd a = mkc(0.0, 0.0);
+      for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
+      const cd h = sy.reduce(a, s, buf, A.gpart);
+      if (t == 0) s.hcol[i] = h;
+      for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
+    }
+    cd a = mkc(0.0, 0.0);
+    for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+    const double hn = sqrt(fmax(sy.reduce(a, s, buf, A.gpart).x, 0.0));
+    if (t == 0) {
+      // rotations (krylov.py:126-151), identical in every CTA
+      cd* col = s.hcol;
+      col[j + 1] = mkc(hn, 0.0);
+      bool finite = true;
+      for (int i = 0; i <= j + 1; ++i) finite &= isfinite(col[i].x) && isfinite(col[i].y);
+      for (int i = 0; i < j; ++i) {
+        const cd sc = cmul_(s.sn[i], col[i + 1]);
+        const cd tt = mkc(s.cs[i] * col[i].x + sc.x, s.cs[i] * col[i].y + sc.y);
+        const cd nb = cmul_(mkc(-s.sn[i].x, s.sn[i].y), col[i]);
+        col[i + 1] = mkc(nb.x + s.cs[i] * col[i + 1].x, nb.y + s.cs[i] * col[i + 1].y);
+        col[i] = tt;
+      }
+      const cd h1 = col[j], h2 = col[j + 1];
+      double c;
+      cd sn;
+      const double a1 = cabs_(h1), a2 = cabs_(h2);
+      if (a2 == 0.0) { c = 1.0; sn = mkc(0.0, 0.0); }
+      else if (a1 == 0.0) { c = 0.0; sn = mkc(1.0, 0.0); }
+      else {
+        const double tt = hypot(a1, a2);
+        c = a1 / tt;
+        const cd q = cmul_(mkc(h1.x / a1, h1.y / a1), mkc(h2.x, -h2.y));
+        sn = mkc(q.x / tt, q.y / tt);
+      }
+      s.cs[j] = c;
+      s.sn[j] = sn;
+      const cd sh = cmul_(sn, h2);
+      col[j] = mkc(c * h1.x + sh.x, c * h1.y + sh.y);
+      if (rank == 0) {
+        cd* Rc = Rg + (long long)j * (j + 1) / 2;
+        for (int i = 0; i <= j; ++i) Rc[i] = col[i];
+      }
+      const cd gj = s.g[j];
+      s.g[j + 1] = cmul_(mkc(-sn.x, sn.y), gj);
+      s.g[j] = mkc(c * gj.x, c * gj.y);
+      const double rel = cabs_(s.g[j + 1]) / bnorm;
+      s.decision = !finite ? 2 : ((hn < 1e-30 || rel <= A.tol) ? 1 : 0);
+    }
+    __syncthreads();
+    its = j + 1;
+    const int dec = s.decision;
+    if (dec == 2) {
+      if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = its; }
+      return;
+    }
+    if (dec == 1) break;
+    const double inv = 1.0 / hn;
+    cd* vn = V(j + 1) + p0;
+    for (int q = t; q < cnt; q += kRT) {
+      const cd v = ws[q];
+      vn[q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+    }
+  }
+  // least squares (krylov.py:161-168) on rank 0, y broadcast through global memory
+  if (rank == 0 && t == 0) {
+    for (int i = its - 1; i >= 0; --i) {
+      cd accy = s.g[i];
+      for (int k = i + 1; k < its; ++k) {
+        const cd pr = cmul_(Rg[(long long)k * (k + 1) / 2 + i], yg[k]);
+        accy = mkc(accy.x - pr.x, accy.y - pr.y);
+      }
+      yg[i] = cdiv_(accy, Rg[(long long)i * (i + 1) / 2 + i]);
+    }
+  }
+  sy.barrier();
+  for (int q = t; q < cnt; q += kRT) {
+    cd xx = mkc(0.0, 0.0);
+    for (int i = 0; i < its; ++i) xx = c_add(xx, c_mul_np(__ldcg(&yg[i]), V(i)[p0 + q]));
+    A.x[p0 + q] = xx;
+  }
+  sy.barrier();  // x complete everywhere
+  // explicit true residual (krylov.py:174)
+  cd f = mkc(0.0, 0.0);
+  for (int q = t; q < cnt; q += kRT) {
+    const long long p = p0 + q;
+    const cd d = c_sub(A.b[p], op_point<R>(A.c, A.g, A.x, A.ksq, (int)(p / nx) + A.g.row0, (int)(p % nx)));
+    f = c_conjmul_acc(f, d, d);
+  }
+  const double fin = sqrt(fmax(sy.reduce(f, s, buf, A.gpart).x, 0.0)) / bnorm;
+  if (rank == 0 && t == 0) {
+    *A.its_out = its;
+    *A.relres_out = fin;
+    if (!isfinite(fin)) A.flag->x = 2.0;
+  }
+}
+
+// ------------------------------------------------------------------ launch
+static size_t smem_for(long long chunk) { return ((sizeof(RSmem) + 15) / 16) * 16 + (size_t)chunk * sizeof(cd); }
+
+static int g_cluster = 0;
+static int g_grid = 0;
+static size_t g_smem_optin = 0;
+
+static void init_limits() {
+  if (g_smem_optin) return;
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  g_smem_optin = (size_t)v;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  g_grid = v;
+}
+
+template <class K>
+static void set_attrs(K kern, size_t sm, bool cluster) {
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (cluster) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
+
+template <int R>
+static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
+  auto kern = k_resident_gmres<ClusterSync, R>;
+  if (g_cluster == 0) {
+    const size_t sm0 = smem_for(8192);
+    set_attrs(kern, sm0, true);
+    for (int c : {16, 8, 4}) {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(c); cfg.blockDim = dim3(kRT); cfg.dynamicSmemBytes = sm0; cfg.attrs = at; cfg.numAttrs = 1;
+      int num = 0;
+      if (cudaOccupancyMaxActiveClusters(&num, kern, &cfg) == cudaSuccess && num > 0) { g_cluster = c; break; }
+      cudaGetLastError();
+    }
+    if (g_cluster == 0) g_cluster = -1;
+  }
+  if (g_cluster < 0) return false;
+  const long long chunk = (a.n + g_cluster - 1) / g_cluster;
+  const size_t sm = smem_for(chunk);
+  if (sm > g_smem_optin) return false;
+  set_attrs(kern, sm, true);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = g_cluster; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(g_cluster);
+  cfg.blockDim = dim3(kRT);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+}
+
+template <int R>
+static bool launch_grid(ResidentArgs a, cudaStream_t st) {
+  auto kern = k_resident_gmres<GridSync, R>;
+  const long long chunk = (a.n + g_grid - 1) / g_grid;
+  const size_t sm = smem_for(chunk);
+  if (sm > g_smem_optin) return false;
+  set_attrs(kern, sm, false);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRT, sm) != cudaSuccess || per_sm < 1) {
+    cudaGetLastError();
+    return false;
+  }
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((void*)kern, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess;
+}
+
+int resident_max_cap() { return kMaxCap; }
+
+long long resident_cluster_points() {
+  init_limits();
+  const size_t room = g_smem_optin > smem_for(0) ? g_smem_optin - smem_for(0) : 0;
+  return (long long)(room / sizeof(cd)) * 16;
+}
+long long resident_grid_points() {
+  init_limits();
+  const size_t room = g_smem_optin > smem_for(0) ? g_smem_optin - smem_for(0) : 0;
+  return (long long)(room / sizeof(cd)) * g_grid;
+}
+
+// returns 0 on success, 1 if the problem does not fit a resident launch
+int launch_resident_gmres(int mode, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
+                          cd* basis, cd* Rg, cd* gpart, long long n, double tol, int cap, int* its_out,
+                          double* relres_out, cd* flag, cudaStream_t st) {
+  init_limits();
+  ResidentArgs a;
+  a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
+  a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag;
+  bool ok;
+  if (mode == 0) {
+    ok = c.radius == 1 ? launch_cluster<1>(a, st) : c.radius == 2 ? launch_cluster<2>(a, st) : launch_cluster<3>(a, st);
+  } else {
+    ok = c.radius == 1 ? launch_grid<1>(a, st) : c.radius == 2 ? launch_grid<2>(a, st) : launch_grid<3>(a, st);
+  }
+  return ok ? 0 : 1;
+}
+
+int resident_grid_ctas() {
+  init_limits();
+  return g_grid;
+}
+
+}  // namespace hdb

@@ -143,6 +143,8 @@ SOLVES = {
     "c1s": (lambda: mp1_problem(k=50.0, n=129, ml=2, boundary="sommerfeld"), 150, True),
     "wedge20": (lambda: wedge_problem(f=20.0, nx=145, ml=4), 150, True),
     "c1_cap20": (lambda: mp1_problem(k=50.0, n=129, ml=2, boundary="dirichlet"), 20, True),
+    # config-2 analogue (k=100, 1025^2, ml=6): solution stored every 8th point
+    "c2a": (lambda: mp1_problem(k=100.0, n=1025, ml=6, boundary="sommerfeld"), 150, 8),
 }
 
 
@@ -171,8 +173,12 @@ def solves(names):
                    floor_hist_abs=np.abs(h0[:n] - h1[:n]).max(),
                    floor_sol_rel=np.linalg.norm(x - xp) / np.linalg.norm(x),
                    floor_its=repp.outer_iterations)
-        if save_x:
+        if save_x is True:
             rec["solution"] = x
+        elif save_x:
+            rec["solution_stride"] = np.array(save_x)
+            rec["solution_sub"] = x[::save_x, ::save_x]
+        rec["floor_hist"] = h1
         np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **rec)
         print(name, rep.outer_iterations, rep.final_relres, rec["floor_hist_abs"], rec["floor_sol_rel"])
 
