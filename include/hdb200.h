@@ -95,6 +95,12 @@ int hdb_fgmres(long long n, hdb_linop_fn A, void* A_user, hdb_linop_fn M, void* 
                int* iterations, double* final_relres, int* converged,
                double* history_host, int history_cap);
 
+/* GMRES on one level operator, no preconditioner (the CSLP solve of
+ * madp.py:290-291): mode -1 launch-driven engine, 0 device-resident on one
+ * thread-block cluster, 1 device-resident cooperative grid, 2 automatic      */
+int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_iters, int mode,
+                 int* iterations, double* final_relres);
+
 /* ---- MADP solver: replaces MadpSolver (madp.py:220-371) ------------------- */
 int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max);
 /* cslp: 0 none, 1 mg, 2 gmres (madp.py:55-58); level 1 ignores the cycle rule */

@@ -8,7 +8,12 @@
 
 using namespace hdb;
 
-struct hdb_op { LevelOp op; };
+struct hdb_op {
+  LevelOp op;
+  SmallSolve resident;  // workspaces reused across hdb_op_gmres calls
+  KWS ws;
+  int* dres = nullptr;  // its (int) + relres (double)
+};
 struct hdb_mg { Multigrid mg; };
 struct hdb_solver { MadpSolver s; };
 
@@ -98,7 +103,7 @@ int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int*
 int hdb_op_destroy(hdb_op* op) {
   return guarded([&] {
     if (!op) return;
-    if (engine_ready()) { engine().sync(); engine().free(op->op.ksq); }
+    if (engine_ready()) { engine().sync(); engine().free(op->op.ksq); engine().free(op->dres); }
     delete op;
   });
 }
@@ -205,6 +210,39 @@ int hdb_fgmres(long long n, hdb_linop_fn A, void* Au, hdb_linop_fn M, void* Mu, 
     *final_relres = r.final_relres;
     *converged = r.converged ? 1 : 0;
     for (int i = 0; i < hist_cap && i < (int)r.history.size(); ++i) hist[i] = r.history[i];
+  });
+}
+
+int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_iters, int mode, int* iterations,
+                 double* final_relres) {
+  return guarded([&] {
+    if (max_iters < 1) throw Error(E_ARG, "max_iters must be >= 1");
+    Engine& E = engine();
+    HDB_CUDA(cudaMemsetAsync(E.dscal + kSlotFlag, 0, sizeof(cd), E.st));
+    const LevelOp* L = &op->op;
+    int m = mode == 2 ? resident_mode(L->n, max_iters) : mode;
+    if (m >= 0) {
+      SmallSolve& ss = op->resident;
+      ss.ensure(L, max_iters);
+      if (!op->dres) op->dres = (int*)E.alloc_bytes(16);
+      int* dits = op->dres;
+      double* drel = (double*)(op->dres + 2);
+      if (launch_resident_gmres(m, L->c, L->g, L->ksq, (const cd*)b, (cd*)x, ss.basis, ss.Rg, ss.gpart, L->n,
+                                rel_tol, max_iters, dits, drel, E.dscal + kSlotFlag, E.st) != 0)
+        throw Error(E_ARG, "problem does not fit the requested device-resident mode");
+      int h_its = 0;
+      double h_rel = 0.0;
+      HDB_CUDA(cudaMemcpyAsync(&h_its, dits, sizeof(int), cudaMemcpyDeviceToHost, E.st));
+      HDB_CUDA(cudaMemcpyAsync(&h_rel, drel, sizeof(double), cudaMemcpyDeviceToHost, E.st));
+      E.fetch(1);
+      *iterations = h_its;
+      *final_relres = h_rel;
+      return;
+    }
+    LinOp Aop = [L](const cd* in, cd* o) { L->apply(in, o); };
+    KReport r = fgmres(L->n, Aop, nullptr, (const cd*)b, (cd*)x, Stop{rel_tol, max_iters}, op->ws);
+    *iterations = r.iterations;
+    *final_relres = r.final_relres;
   });
 }
 

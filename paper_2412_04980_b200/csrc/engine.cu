@@ -144,7 +144,7 @@ int resident_mode(long long n, int cap) {
   static long long small = -1, grid = -1;
   if (small < 0) {
     small = std::min(env_ll("HDB_SMALL_N", 70000), resident_cluster_points());
-    grid = std::min(env_ll("HDB_GRID_N", 2000000), resident_grid_points());
+    grid = std::min(env_ll("HDB_GRID_N", 0), resident_grid_points());
   }
   if (cap > resident_max_cap()) return -1;
   if (n <= small) return 0;
@@ -182,7 +182,7 @@ SmallSolve::~SmallSolve() {
   E.free(gpart);
 }
 
-static bool use_small(long long n, int cap) { return resident_mode(n, cap) >= 0; }
+bool use_small(long long n, int cap) { return resident_mode(n, cap) >= 0; }
 
 // ----------------------------------------------------------------- FGMRES
 static const double kHappy = 1e-30;  // krylov.py:28

@@ -50,6 +50,8 @@ struct ResidentArgs {
 };
 
 struct RSmem {
+  uint64_t mbar[2];
+  cd gather[2][16];
   cd warp[kRT / 32];
   cd part[2];
   cd bcast[2];
@@ -107,27 +109,79 @@ __device__ __forceinline__ cd block_partial(cd v, RSmem& s) {
   return t;  // valid in thread 0
 }
 
+// --- cluster reductions: push all-gather through DSMEM ----------------------
+// Every CTA's thread 0 writes its block partial with st.async into slot
+// [its rank] of every CTA's partial array and completes that CTA's mbarrier
+// (16 bytes of transaction each); every thread then waits on its local
+// mbarrier and sums the C slots in rank order.  No cluster barrier, no global
+// fence: a step costs one DSMEM latency.  Buffers alternate; a buffer's
+// mbarrier is re-armed right after its phase completes, which always precedes
+// the next pushes into it (those need this CTA's partial of the step between).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.b32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  }
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void push_c16(uint32_t raddr, cd v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(raddr), "d"(v.x), "d"(v.y), "r"(rbar) : "memory");
+}
+
+constexpr int kMaxCluster = 16;
+
 struct ClusterSync {
   cg::cluster_group cl;
-  __device__ ClusterSync() : cl(cg::this_cluster()) {}
+  uint32_t par[2];
+  __device__ ClusterSync() : cl(cg::this_cluster()) { par[0] = par[1] = 0; }
   __device__ int rank() const { return (int)cl.block_rank(); }
   __device__ int nranks() const { return (int)cl.num_blocks(); }
   __device__ void barrier() { cl.sync(); }
+  __device__ void init(RSmem& s) {
+    if (threadIdx.x == 0) {
+      mbar_init(&s.mbar[0], 1);
+      mbar_init(&s.mbar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_arm(&s.mbar[0], 16u * nranks());
+      mbar_arm(&s.mbar[1], 16u * nranks());
+    }
+    cl.sync();  // every CTA's barriers exist and are armed before any push
+  }
   __device__ cd reduce(cd v, RSmem& s, int& buf, cd*) {
     const cd t = block_partial(v, s);
-    if (threadIdx.x == 0) s.part[buf] = t;
-    cl.sync();
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x < 32) {
-      cd q = mkc(0.0, 0.0);
-      if (lane < nranks()) q = *cl.map_shared_rank(&s.part[buf], lane);
-      q = warp_sum_c(q);
-      if (lane == 0) s.bcast[buf] = q;
+    const int C = nranks();
+    const int b = buf;
+    if (threadIdx.x == 0) {
+      const uint32_t la = smem_addr(&s.gather[b][rank()]);
+      const uint32_t lb = smem_addr(&s.mbar[b]);
+      for (int r = 0; r < C; ++r) push_c16(mapa(la, r), t, mapa(lb, r));
     }
-    __syncthreads();
-    const cd r = s.bcast[buf];
+    mbar_wait(&s.mbar[b], par[b]);
+    par[b] ^= 1u;
+    cd q = mkc(0.0, 0.0);
+    for (int r = 0; r < C; ++r) {
+      const cd z = s.gather[b][r];
+      q.x += z.x;
+      q.y += z.y;
+    }
+    if (threadIdx.x == 0) mbar_arm(&s.mbar[b], 16u * C);  // next use of this buffer
     buf ^= 1;
-    return r;
+    return q;
   }
 };
 
@@ -137,6 +191,7 @@ struct GridSync {
   __device__ int rank() const { return (int)blockIdx.x; }
   __device__ int nranks() const { return (int)gridDim.x; }
   __device__ void barrier() { gr.sync(); }
+  __device__ void init(RSmem&) {}
   __device__ cd reduce(cd v, RSmem& s, int& buf, cd* gpart) {
     const cd t = block_partial(v, s);
     const int P = nranks();
@@ -174,6 +229,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   RSmem& s = *reinterpret_cast<RSmem*>(smem_raw);
   cd* ws = reinterpret_cast<cd*>(smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);  // this CTA's slice of w
   Sync sy;
+  sy.init(s);
   const int P = sy.nranks(), rank = sy.rank();
   const long long n = A.n;
   const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
@@ -191,10 +247,12 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   if (bnorm == 0.0) {  // krylov.py:96-97
     for (int q = t; q < cnt; q += kRT) A.x[p0 + q] = mkc(0.0, 0.0);
     if (rank == 0 && t == 0) { *A.its_out = 0; *A.relres_out = 0.0; }
+    sy.barrier();
     return;
   }
   if (!isfinite(bnorm)) {
     if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = 0; }
+    sy.barrier();
     return;
   }
   const double beta = bnorm;  // r0 = b (zero initial guess); rel = 1 never triggers the early exit
@@ -271,6 +329,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     const int dec = s.decision;
     if (dec == 2) {
       if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = its; }
+      sy.barrier();
       return;
     }
     if (dec == 1) break;
@@ -312,6 +371,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     *A.relres_out = fin;
     if (!isfinite(fin)) A.flag->x = 2.0;
   }
+  sy.barrier();  // no CTA leaves while a peer may still address its shared memory
 }
 
 // ------------------------------------------------------------------ launch
