@@ -101,6 +101,10 @@ int hdb_fgmres(long long n, hdb_linop_fn A, void* A_user, hdb_linop_fn M, void* 
 int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_iters, int mode,
                  int* iterations, double* final_relres);
 
+/* telemetry: enable=1 zeroes and arms per-phase cycle counters of the
+ * device-resident solver; enable=0 disarms and copies the 8 counters out     */
+int hdb_resident_profile(int enable, long long* host_out8);
+
 /* ---- MADP solver: replaces MadpSolver (madp.py:220-371) ------------------- */
 int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max);
 /* cslp: 0 none, 1 mg, 2 gmres (madp.py:55-58); level 1 ignores the cycle rule */

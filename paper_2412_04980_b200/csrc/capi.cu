@@ -227,7 +227,7 @@ int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_ite
       if (!op->dres) op->dres = (int*)E.alloc_bytes(16);
       int* dits = op->dres;
       double* drel = (double*)(op->dres + 2);
-      if (launch_resident_gmres(m, L->c, L->g, L->ksq, (const cd*)b, (cd*)x, ss.basis, ss.Rg, ss.gpart, L->n,
+      if (launch_resident_gmres(m, resident_ortho(), L->c, L->g, L->ksq, (const cd*)b, (cd*)x, ss.basis, ss.Rg, ss.gpart, L->n,
                                 rel_tol, max_iters, dits, drel, E.dscal + kSlotFlag, E.st) != 0)
         throw Error(E_ARG, "problem does not fit the requested device-resident mode");
       int h_its = 0;
@@ -243,6 +243,25 @@ int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_ite
     KReport r = fgmres(L->n, Aop, nullptr, (const cd*)b, (cd*)x, Stop{rel_tol, max_iters}, op->ws);
     *iterations = r.iterations;
     *final_relres = r.final_relres;
+  });
+}
+
+// telemetry: per-phase cycle counters of device-resident solves (CTA 0, thread 0)
+static long long* g_phase = nullptr;
+int hdb_resident_profile(int enable, long long* host_out8) {
+  return guarded([&] {
+    Engine& E = engine();
+    if (enable) {
+      if (!g_phase) g_phase = (long long*)E.alloc_bytes(8 * sizeof(long long));
+      HDB_CUDA(cudaMemsetAsync(g_phase, 0, 8 * sizeof(long long), E.st));
+      resident_set_profile(g_phase);
+    } else {
+      if (host_out8 && g_phase) {
+        HDB_CUDA(cudaMemcpyAsync(host_out8, g_phase, 8 * sizeof(long long), cudaMemcpyDeviceToHost, E.st));
+        E.sync();
+      }
+      resident_set_profile(nullptr);
+    }
   });
 }
 

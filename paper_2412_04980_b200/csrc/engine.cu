@@ -140,11 +140,20 @@ static long long env_ll(const char* name, long long dflt) {
   return e ? atoll(e) : dflt;
 }
 
+int resident_ortho() {
+  static int o = -1;
+  if (o < 0) {
+    const char* e = getenv("HDB_ORTHO");
+    o = (e && std::string(e) == "mgs") ? 0 : 1;
+  }
+  return o;
+}
+
 int resident_mode(long long n, int cap) {
   static long long small = -1, grid = -1;
   if (small < 0) {
-    small = std::min(env_ll("HDB_SMALL_N", 70000), resident_cluster_points());
-    grid = std::min(env_ll("HDB_GRID_N", 0), resident_grid_points());
+    small = std::min(env_ll("HDB_SMALL_N", 12000), resident_cluster_points());
+    grid = std::min(env_ll("HDB_GRID_N", 2000000), resident_grid_points());
   }
   if (cap > resident_max_cap()) return -1;
   if (n <= small) return 0;
@@ -162,16 +171,21 @@ void SmallSolve::ensure(const LevelOp* o, int cap_) {
   cap = cap_;
   basis = E.alloc((long long)(cap + 1) * o->n);
   Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap);
-  gpart = E.alloc(2LL * resident_grid_ctas());
+  gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1));
 }
 
-void SmallSolve::run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {
+bool SmallSolve::try_run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {
   Engine& E = engine();
   const int mode = resident_mode(op->n, stop.max_iters);
-  if (mode < 0 || launch_resident_gmres(mode, op->c, op->g, op->ksq, b, x, basis, Rg, gpart, op->n, stop.rel_tol,
-                                        stop.max_iters, its_dev, rel_dev, E.dscal + kSlotFlag, E.st) != 0)
-    throw Error(E_CUDA, std::string("device-resident GMRES launch failed: ") + cudaGetErrorString(cudaGetLastError()));
+  if (mode < 0) return false;
+  if (launch_resident_gmres(mode, resident_ortho(), op->c, op->g, op->ksq, b, x, basis, Rg, gpart, op->n,
+                            stop.rel_tol, stop.max_iters, its_dev, rel_dev, E.dscal + kSlotFlag, E.st) != 0) {
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) throw Error(E_CUDA, std::string("device-resident GMRES launch: ") + cudaGetErrorString(err));
+    return false;  // does not fit the resident working set: caller uses the launch path
+  }
   E.launches++;
+  return true;
 }
 
 SmallSolve::~SmallSolve() {
@@ -182,7 +196,7 @@ SmallSolve::~SmallSolve() {
   E.free(gpart);
 }
 
-bool use_small(long long n, int cap) { return resident_mode(n, cap) >= 0; }
+
 
 // ----------------------------------------------------------------- FGMRES
 static const double kHappy = 1e-30;  // krylov.py:28
@@ -366,14 +380,18 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
     if (Ainv) {
       launch_gemv(Ainv, b, x, ninv, E.st);
       E.launches++;
-    } else if (use_small(ops[i]->n, coarse_stop.max_iters)) {
-      small_coarse.ensure(ops[i], coarse_stop.max_iters);
-      Engine& E2 = engine();
-      small_coarse.run(b, x, coarse_stop, (int*)(E2.dscal + kSlotMisc), (double*)(E2.dscal + kSlotMisc) + 1);
     } else {
       const LevelOp* op = ops[i];
-      LinOp A = [op](const cd* in, cd* out) { op->apply(in, out); };
-      fgmres(op->n, A, nullptr, b, x, coarse_stop, coarse_ws);
+      Engine& E2 = engine();
+      bool done = false;
+      if (resident_mode(op->n, coarse_stop.max_iters) >= 0) {
+        small_coarse.ensure(op, coarse_stop.max_iters);
+        done = small_coarse.try_run(b, x, coarse_stop, (int*)(E2.dscal + kSlotMisc), (double*)(E2.dscal + kSlotMisc) + 1);
+      }
+      if (!done) {
+        LinOp A = [op](const cd* in, cd* out) { op->apply(in, out); };
+        fgmres(op->n, A, nullptr, b, x, coarse_stop, coarse_ws);
+      }
     }
     return;
   }
@@ -510,14 +528,15 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     return;
   }
   const LevelOp* M = L.M;
-  if (use_small(M->n, L.cslp_stop.max_iters)) {
+  if (resident_mode(M->n, L.cslp_stop.max_iters) >= 0) {
     if (dused >= dcap) flush_counts();
     L.small_cslp.ensure(M, L.cslp_stop.max_iters);
-    L.small_cslp.run(rhs, out, L.cslp_stop, dcounts + dused, drel + dused);
-    rep.cslp_iters[l].push_back(-1);
-    pending.emplace_back(l, (int)rep.cslp_iters[l].size() - 1);
-    dused++;
-    return;
+    if (L.small_cslp.try_run(rhs, out, L.cslp_stop, dcounts + dused, drel + dused)) {
+      rep.cslp_iters[l].push_back(-1);
+      pending.emplace_back(l, (int)rep.cslp_iters[l].size() - 1);
+      dused++;
+      return;
+    }
   }
   LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
   KReport r = fgmres(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_cslp);

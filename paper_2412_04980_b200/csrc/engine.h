@@ -109,9 +109,11 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
 
 // Krylov solves on levels that fit the resident working set run as ONE
 // device-resident launch (kernels_resident.cu): cluster mode up to
-// HDB_SMALL_N points (default 70k), whole-grid cooperative mode up to
-// HDB_GRID_N points (default 2.0M, capped by shared memory).  0 disables.
+// HDB_SMALL_N points (default 12k), whole-grid cooperative mode up to
+// HDB_GRID_N points (default 2M) when the stencil windows fit shared memory.
+// 0 disables a mode.
 int resident_mode(long long n, int cap);  // -1: launch-driven path
+int resident_ortho();  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
 
 struct SmallSolve {  // device-resident GMRES on one level operator
   const LevelOp* op = nullptr;
@@ -120,8 +122,9 @@ struct SmallSolve {  // device-resident GMRES on one level operator
   cd* gpart = nullptr;
   int cap = 0;
   void ensure(const LevelOp* o, int cap_);
-  // launches; iteration count lands in *its_dev, final relres in *rel_dev
-  void run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev);
+  // launches if the problem fits a resident mode (false: use the launch path);
+  // iteration count lands in *its_dev, final relres in *rel_dev
+  bool try_run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev);
   ~SmallSolve();
 };
 

@@ -22,6 +22,8 @@
 // arithmetic is the same as the launch path.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include "kernels.h"
 #include "stencil.cuh"
 
@@ -47,11 +49,29 @@ struct ResidentArgs {
   int* its_out;
   double* relres_out;
   cd* flag;           // .x = 2.0 on a non-finite value (NumericalError)
+  long long* prof;    // optional: per-phase cycles of CTA 0 thread 0 (telemetry), may be null
+  int tiled;          // stencil windows staged in shared memory
+  int tile_elems;     // window elements (max over CTAs)
 };
+
+// phase clock (CTA 0, thread 0) — only when A.prof != nullptr
+#define PHASE(k)                                                   \
+  do {                                                             \
+    if (A.prof && rank == 0 && t == 0) {                           \
+      const long long now_ = clock64();                            \
+      A.prof[k] += now_ - tprev_;                                  \
+      tprev_ = now_;                                               \
+    }                                                              \
+  } while (0)
+
+constexpr int kVecCap = 130;  // max vector all-gather length (CGS2: cap + 1)
+
+typedef cd GatherBuf[2][16][kVecCap];  // [buffer][source rank][element] (cluster mode only)
 
 struct RSmem {
   uint64_t mbar[2];
-  cd gather[2][16];
+  cd pv[kVecCap];             // this CTA's block partial vector
+  cd hv[kVecCap];             // reduced vector (CGS2 coefficients)
   cd warp[kRT / 32];
   cd part[2];
   cd bcast[2];
@@ -81,6 +101,71 @@ __device__ __forceinline__ cd op_point(const OpCoef& c, const Geom& g, const cd*
       const cd m = c.mass[a * N + bb];
       const cd coef = mkc(__dadd_rn(c.lap[a * N + bb], __dmul_rn(m.x, kp)), __dmul_rn(m.y, kp));
       acc = c_add(acc, c_mul(coef, upad(u, k, g, c, jj, ii)));
+    }
+  }
+  return acc;
+}
+
+// Shared-memory stencil window of this CTA's rows: rows [rlo-R, rhi+R] x columns
+// [-R, nx+R) of the ghost-closed field (upad) and of k^2 (kpad).  Taps then read
+// shared memory only; the window is loaded with all loads in flight.
+struct Tile {
+  int rlo, rows, cols;  // first own global row, window rows / cols
+};
+
+template <int R>
+__device__ __forceinline__ Tile make_tile(const Geom& g, long long p0, long long p1) {
+  Tile T;
+  T.rlo = (int)(p0 / g.nx) + g.row0;
+  const int rhi = (int)((p1 - 1) / g.nx) + g.row0;
+  T.rows = rhi - T.rlo + 1 + 2 * R;
+  T.cols = g.nx + 2 * R;
+  return T;
+}
+
+template <int R>
+__device__ __forceinline__ void load_u_tile(cd* ut, const Tile& T, const cd* u, const double* k, const Geom& g,
+                                            const OpCoef& c) {
+  const int n = T.rows * T.cols;
+#pragma unroll 4
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int tr = e / T.cols, tc = e - tr * T.cols;
+    ut[e] = upad(u, k, g, c, T.rlo - R + tr, tc - R);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void load_k_tile(double* kt, const Tile& T, const double* k, const Geom& g,
+                                            const OpCoef& c) {
+  const int n = T.rows * T.cols;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int tr = e / T.cols, tc = e - tr * T.cols;
+    kt[e] = kpad(k, g, c, T.rlo - R + tr, tc - R);
+  }
+}
+
+// (A u) at global (gj, i) from the windows (same arithmetic as the launch kernels)
+template <int R>
+__device__ __forceinline__ cd op_point_tile(const OpCoef& c, const Geom& g, const Tile& T, const cd* ut,
+                                            const double* kt, int gj, int i) {
+  const int tr = gj - T.rlo + R, tc = i + R;
+  const cd* uc = ut + tr * T.cols + tc;
+  if (pinned(g, c, gj, i)) return *uc;
+  if (R == 1) {
+    return five_point(c.s, c.mc, kt[tr * T.cols + tc], *uc, uc[-1], uc[1], uc[-T.cols], uc[T.cols]);
+  }
+  constexpr int N = 2 * R + 1;
+  const cd* u0 = uc - R * T.cols - R;
+  const double* k0 = kt + (tr - R) * T.cols + tc - R;
+  cd acc = mkc(0.0, 0.0);
+#pragma unroll
+  for (int a = 0; a < N; ++a) {
+#pragma unroll
+    for (int bb = 0; bb < N; ++bb) {
+      const double kp = k0[a * T.cols + bb];
+      const cd m = c.mass[a * N + bb];
+      const cd coef = mkc(__dadd_rn(c.lap[a * N + bb], __dmul_rn(m.x, kp)), __dmul_rn(m.y, kp));
+      acc = c_add(acc, c_mul(coef, u0[a * T.cols + bb]));
     }
   }
   return acc;
@@ -146,62 +231,92 @@ __device__ __forceinline__ void push_c16(uint32_t raddr, cd v, uint32_t rbar) {
 constexpr int kMaxCluster = 16;
 
 struct ClusterSync {
+  static constexpr bool kGather = true;
   cg::cluster_group cl;
   uint32_t par[2];
+  GatherBuf* gb = nullptr;  // in dynamic shared memory after RSmem
   __device__ ClusterSync() : cl(cg::this_cluster()) { par[0] = par[1] = 0; }
   __device__ int rank() const { return (int)cl.block_rank(); }
   __device__ int nranks() const { return (int)cl.num_blocks(); }
   __device__ void barrier() { cl.sync(); }
-  __device__ void init(RSmem& s) {
+  __device__ void init(RSmem& s, void* gather_mem) {
+    gb = reinterpret_cast<GatherBuf*>(gather_mem);
     if (threadIdx.x == 0) {
       mbar_init(&s.mbar[0], 1);
       mbar_init(&s.mbar[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_arm(&s.mbar[0], 16u * nranks());
-      mbar_arm(&s.mbar[1], 16u * nranks());
     }
-    cl.sync();  // every CTA's barriers exist and are armed before any push
+    cl.sync();  // every CTA's barriers exist before any push
   }
-  __device__ cd reduce(cd v, RSmem& s, int& buf, cd*) {
-    const cd t = block_partial(v, s);
-    const int C = nranks();
-    const int b = buf;
-    if (threadIdx.x == 0) {
-      const uint32_t la = smem_addr(&s.gather[b][rank()]);
-      const uint32_t lb = smem_addr(&s.mbar[b]);
-      for (int r = 0; r < C; ++r) push_c16(mapa(la, r), t, mapa(lb, r));
+  // all-gather + ordered sum of the block partial vector s.pv[0..m) (written and
+  // __syncthreads-visible); result in out[0..m) (smem), visible to all threads
+  // on return.  Arming happens here: pushes that arrive earlier only drive the
+  // transaction count negative while the local arrival is still pending.
+  __device__ void gather_sum(RSmem& s, int m, cd* out, int& buf) {
+    const int C = nranks(), me = rank(), b = buf;
+    if (threadIdx.x == 0) mbar_arm(&s.mbar[b], 16u * (uint32_t)(C * m));
+    for (int e = threadIdx.x; e < m * C; e += blockDim.x) {
+      const int r = e / m, i = e % m;  // destination rank, element
+      push_c16(mapa(smem_addr(&(*gb)[b][me][i]), r), s.pv[i], mapa(smem_addr(&s.mbar[b]), r));
     }
     mbar_wait(&s.mbar[b], par[b]);
     par[b] ^= 1u;
-    cd q = mkc(0.0, 0.0);
-    for (int r = 0; r < C; ++r) {
-      const cd z = s.gather[b][r];
-      q.x += z.x;
-      q.y += z.y;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      cd q = mkc(0.0, 0.0);
+      for (int r = 0; r < C; ++r) {
+        q.x += (*gb)[b][r][i].x;
+        q.y += (*gb)[b][r][i].y;
+      }
+      out[i] = q;
     }
-    if (threadIdx.x == 0) mbar_arm(&s.mbar[b], 16u * C);  // next use of this buffer
+    __syncthreads();
     buf ^= 1;
-    return q;
   }
+  __device__ cd reduce(cd v, RSmem& s, int& buf, cd*) {
+    const cd t = block_partial(v, s);
+    if (threadIdx.x == 0) s.pv[0] = t;
+    __syncthreads();
+    gather_sum(s, 1, s.bcast, buf);
+    return s.bcast[0];
+  }
+  __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd*) { gather_sum(s, m, out, buf); }
 };
 
 struct GridSync {
+  static constexpr bool kGather = false;
   cg::grid_group gr;
   __device__ GridSync() : gr(cg::this_grid()) {}
   __device__ int rank() const { return (int)blockIdx.x; }
   __device__ int nranks() const { return (int)gridDim.x; }
   __device__ void barrier() { gr.sync(); }
-  __device__ void init(RSmem&) {}
+  __device__ void init(RSmem&, void*) {}
+  // s.pv[0..m) -> out[0..m), fixed rank order
+  __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd* gpart) {
+    const int P = nranks();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) __stcg(&gpart[((long long)buf * P + blockIdx.x) * kVecCap + i], s.pv[i]);
+    gr.sync();
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      cd q = mkc(0.0, 0.0);
+      for (int r = 0; r < P; ++r) {
+        const cd z = __ldcg(&gpart[((long long)buf * P + r) * kVecCap + i]);
+        q.x += z.x;
+        q.y += z.y;
+      }
+      out[i] = q;
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
   __device__ cd reduce(cd v, RSmem& s, int& buf, cd* gpart) {
     const cd t = block_partial(v, s);
     const int P = nranks();
-    if (threadIdx.x == 0) __stcg(&gpart[buf * P + blockIdx.x], t);
+    if (threadIdx.x == 0) __stcg(&gpart[((long long)buf * P + blockIdx.x) * kVecCap], t);
     gr.sync();
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
       cd q = mkc(0.0, 0.0);
       for (int r = lane; r < P; r += 32) {
-        const cd z = __ldcg(&gpart[buf * P + r]);
+        const cd z = __ldcg(&gpart[((long long)buf * P + r) * kVecCap]);
         q.x += z.x;
         q.y += z.y;
       }
@@ -223,17 +338,56 @@ __device__ __forceinline__ cd cdiv_(cd a, cd b) {
   return mkc((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
 }
 
-template <class Sync, int R>
+// CGS pass: out = V[0..m)^H w (warp per basis vector over this CTA's points),
+// then w -= V out.  Returns with out[] reduced cluster/grid-wide in s.hv.
+template <class Sync>
+__device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n, long long p0, int cnt, int m,
+                         int& buf, cd* gpart) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = wid; i < m; i += kRT / 32) {
+    const cd* vi = basis + (long long)i * n + p0;
+    cd a = mkc(0.0, 0.0);
+#pragma unroll 8
+    for (int q = lane; q < cnt; q += 32) a = c_conjmul_acc(a, vi[q], ws[q]);
+    a = warp_sum_c(a);
+    if (lane == 0) s.pv[i] = a;
+  }
+  __syncthreads();
+  sy.reduce_vec(s, m, s.hv, buf, gpart);
+  for (int q = threadIdx.x; q < cnt; q += kRT) {
+    cd w = ws[q];
+    const cd* vq = basis + p0 + q;
+    int i = 0;
+    for (; i + 8 <= m; i += 8) {  // 8 loads in flight, then the dependent updates in order
+      cd v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i + u) * n];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w = c_sub(w, c_mul_np(s.hv[i + u], v[u]));
+    }
+    for (; i < m; ++i) w = c_sub(w, c_mul_np(s.hv[i], vq[(long long)i * n]));
+    ws[q] = w;
+  }
+  __syncthreads();
+}
+
+template <class Sync, int R, int ORTHO>
 __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RSmem& s = *reinterpret_cast<RSmem*>(smem_raw);
-  cd* ws = reinterpret_cast<cd*>(smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);  // this CTA's slice of w
+  constexpr size_t kHead = ((sizeof(RSmem) + 15) / 16) * 16 + (Sync::kGather ? sizeof(GatherBuf) : 0);
   Sync sy;
-  sy.init(s);
+  sy.init(s, smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);
   const int P = sy.nranks(), rank = sy.rank();
   const long long n = A.n;
   const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
   const int cnt = (int)(p1 - p0);
+  const long long chunk_max = (n + P - 1) / P;
+  cd* ws = reinterpret_cast<cd*>(smem_raw + kHead);  // this CTA's slice of w
+  const Tile T = make_tile<R>(A.g, p0, p1);
+  cd* ut = A.tiled ? ws + chunk_max : nullptr;                 // stencil window of the current vector
+  double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
+  if (A.tiled && cnt > 0) load_k_tile<R>(kt, T, A.ksq, A.g, A.c);
   const int t = threadIdx.x;
   const int nx = A.g.nx;
   int buf = 0;
@@ -266,25 +420,51 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   }
   if (t == 0) s.g[0] = mkc(beta, 0.0);
   int its = 0;
+  long long tprev_ = clock64();
   for (int j = 0; j < A.cap; ++j) {
     sy.barrier();  // V_j complete everywhere
+    PHASE(0);
     const cd* vj = V(j);
-    for (int q = t; q < cnt; q += kRT) {
-      const long long p = p0 + q;
-      ws[q] = op_point<R>(A.c, A.g, vj, A.ksq, (int)(p / nx) + A.g.row0, (int)(p % nx));
+    if (A.tiled) {
+      if (cnt > 0) load_u_tile<R>(ut, T, vj, A.ksq, A.g, A.c);
+      __syncthreads();
+      for (int q = t; q < cnt; q += kRT) {
+        const long long p = p0 + q;
+        ws[q] = op_point_tile<R>(A.c, A.g, T, ut, kt, (int)(p / nx) + A.g.row0, (int)(p % nx));
+      }
+    } else {
+      for (int q = t; q < cnt; q += kRT) {
+        const long long p = p0 + q;
+        ws[q] = op_point<R>(A.c, A.g, vj, A.ksq, (int)(p / nx) + A.g.row0, (int)(p % nx));
+      }
     }
-    // modified Gram-Schmidt (krylov.py:121-124): h_i = <V_i, w>; w -= h_i V_i
-    for (int i = 0; i <= j; ++i) {
-      const cd* vi = V(i) + p0;
-      cd a = mkc(0.0, 0.0);
-      for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
-      const cd h = sy.reduce(a, s, buf, A.gpart);
-      if (t == 0) s.hcol[i] = h;
-      for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
+    PHASE(1);
+    if (ORTHO == 0) {
+      // modified Gram-Schmidt (krylov.py:121-124): h_i = <V_i, w>; w -= h_i V_i
+      for (int i = 0; i <= j; ++i) {
+        const cd* vi = V(i) + p0;
+        cd a = mkc(0.0, 0.0);
+        for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
+        const cd h = sy.reduce(a, s, buf, A.gpart);
+        if (t == 0) s.hcol[i] = h;
+        for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
+      }
+    } else {
+      // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
+      // Hessenberg column in exact arithmetic, two reductions instead of j+1
+      __syncthreads();
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
+      for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
+      __syncthreads();
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
+      for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
+      __syncthreads();
     }
+    PHASE(2);
     cd a = mkc(0.0, 0.0);
     for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
     const double hn = sqrt(fmax(sy.reduce(a, s, buf, A.gpart).x, 0.0));
+    PHASE(3);
     if (t == 0) {
       // rotations (krylov.py:126-151), identical in every CTA
       cd* col = s.hcol;
@@ -325,6 +505,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       s.decision = !finite ? 2 : ((hn < 1e-30 || rel <= A.tol) ? 1 : 0);
     }
     __syncthreads();
+    PHASE(4);
     its = j + 1;
     const int dec = s.decision;
     if (dec == 2) {
@@ -339,6 +520,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       const cd v = ws[q];
       vn[q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
     }
+    PHASE(5);
   }
   // least squares (krylov.py:161-168) on rank 0, y broadcast through global memory
   if (rank == 0 && t == 0) {
@@ -352,17 +534,37 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     }
   }
   sy.barrier();
+  const bool ysm = its <= kVecCap;
+  if (ysm)
+    for (int i = t; i < its; i += kRT) s.hv[i] = __ldcg(&yg[i]);
+  __syncthreads();
+  const cd* yc = ysm ? s.hv : yg;
   for (int q = t; q < cnt; q += kRT) {
     cd xx = mkc(0.0, 0.0);
-    for (int i = 0; i < its; ++i) xx = c_add(xx, c_mul_np(__ldcg(&yg[i]), V(i)[p0 + q]));
+    const cd* vq = A.basis + p0 + q;
+    int i = 0;
+    for (; i + 8 <= its; i += 8) {
+      cd v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i + u) * n];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xx = c_add(xx, c_mul_np(yc[i + u], v[u]));
+    }
+    for (; i < its; ++i) xx = c_add(xx, c_mul_np(yc[i], vq[(long long)i * n]));
     A.x[p0 + q] = xx;
   }
   sy.barrier();  // x complete everywhere
   // explicit true residual (krylov.py:174)
   cd f = mkc(0.0, 0.0);
+  if (A.tiled) {
+    if (cnt > 0) load_u_tile<R>(ut, T, A.x, A.ksq, A.g, A.c);
+    __syncthreads();
+  }
   for (int q = t; q < cnt; q += kRT) {
     const long long p = p0 + q;
-    const cd d = c_sub(A.b[p], op_point<R>(A.c, A.g, A.x, A.ksq, (int)(p / nx) + A.g.row0, (int)(p % nx)));
+    const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
+    const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
+    const cd d = c_sub(A.b[p], ax);
     f = c_conjmul_acc(f, d, d);
   }
   const double fin = sqrt(fmax(sy.reduce(f, s, buf, A.gpart).x, 0.0)) / bnorm;
@@ -375,9 +577,31 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
 }
 
 // ------------------------------------------------------------------ launch
-static size_t smem_for(long long chunk) { return ((sizeof(RSmem) + 15) / 16) * 16 + (size_t)chunk * sizeof(cd); }
+static size_t smem_head(bool cluster) {
+  return ((sizeof(RSmem) + 15) / 16) * 16 + (cluster ? sizeof(GatherBuf) : 0);
+}
+static size_t smem_for(long long chunk, bool cluster) { return smem_head(cluster) + (size_t)chunk * sizeof(cd); }
+
+// largest stencil window over the P CTAs (rows x (nx + 2R))
+static int tile_elems_for(long long n, int nx, int P, int R) {
+  long long best = 0;
+  for (int r = 0; r < P; ++r) {
+    const long long p0 = n * r / P, p1 = n * (r + 1) / P;
+    if (p1 <= p0) continue;
+    const long long rows = (p1 - 1) / nx - p0 / nx + 1 + 2 * R;
+    best = std::max(best, rows * (nx + 2 * R));
+  }
+  return (int)best;
+}
+
+static size_t smem_tiled(long long chunk, int tile, bool cluster) {
+  return smem_for(chunk, cluster) + (size_t)tile * (sizeof(cd) + sizeof(double));
+}
 
 static int g_cluster = 0;
+static long long* g_prof = nullptr;  // set by resident_set_profile (telemetry)
+
+void resident_set_profile(long long* dev_counters) { g_prof = dev_counters; }
 static int g_grid = 0;
 static size_t g_smem_optin = 0;
 
@@ -397,11 +621,11 @@ static void set_attrs(K kern, size_t sm, bool cluster) {
   if (cluster) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
-template <int R>
+template <int R, int O>
 static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
-  auto kern = k_resident_gmres<ClusterSync, R>;
+  auto kern = k_resident_gmres<ClusterSync, R, O>;
   if (g_cluster == 0) {
-    const size_t sm0 = smem_for(8192);
+    const size_t sm0 = smem_for(4096, true);
     set_attrs(kern, sm0, true);
     for (int c : {16, 8, 4}) {
       cudaLaunchConfig_t cfg = {};
@@ -417,8 +641,11 @@ static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
   }
   if (g_cluster < 0) return false;
   const long long chunk = (a.n + g_cluster - 1) / g_cluster;
-  const size_t sm = smem_for(chunk);
-  if (sm > g_smem_optin) return false;
+  ResidentArgs b = a;
+  b.tile_elems = tile_elems_for(a.n, a.g.nx, g_cluster, R);
+  size_t sm = smem_tiled(chunk, b.tile_elems, true);
+  b.tiled = sm <= g_smem_optin;
+  if (!b.tiled) return false;  // untiled resident solves lose to the launch path
   set_attrs(kern, sm, true);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -430,15 +657,17 @@ static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
   cfg.stream = st;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, kern, b) == cudaSuccess;
 }
 
-template <int R>
+template <int R, int O>
 static bool launch_grid(ResidentArgs a, cudaStream_t st) {
-  auto kern = k_resident_gmres<GridSync, R>;
+  auto kern = k_resident_gmres<GridSync, R, O>;
   const long long chunk = (a.n + g_grid - 1) / g_grid;
-  const size_t sm = smem_for(chunk);
-  if (sm > g_smem_optin) return false;
+  a.tile_elems = tile_elems_for(a.n, a.g.nx, g_grid, R);
+  size_t sm = smem_tiled(chunk, a.tile_elems, false);
+  a.tiled = sm <= g_smem_optin;
+  if (!a.tiled) return false;  // untiled resident solves lose to the launch path
   set_attrs(kern, sm, false);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRT, sm) != cudaSuccess || per_sm < 1) {
@@ -450,32 +679,37 @@ static bool launch_grid(ResidentArgs a, cudaStream_t st) {
 }
 
 int resident_max_cap() { return kMaxCap; }
+int resident_vec_cap() { return kVecCap - 1; }
 
 long long resident_cluster_points() {
   init_limits();
-  const size_t room = g_smem_optin > smem_for(0) ? g_smem_optin - smem_for(0) : 0;
+  const size_t room = g_smem_optin > smem_for(0, true) ? g_smem_optin - smem_for(0, true) : 0;
   return (long long)(room / sizeof(cd)) * 16;
 }
 long long resident_grid_points() {
   init_limits();
-  const size_t room = g_smem_optin > smem_for(0) ? g_smem_optin - smem_for(0) : 0;
+  const size_t room = g_smem_optin > smem_for(0, false) ? g_smem_optin - smem_for(0, false) : 0;
   return (long long)(room / sizeof(cd)) * g_grid;
 }
 
 // returns 0 on success, 1 if the problem does not fit a resident launch
-int launch_resident_gmres(int mode, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
+template <int O>
+static bool launch_any(int mode, const ResidentArgs& a, int radius, cudaStream_t st) {
+  if (mode == 0)
+    return radius == 1 ? launch_cluster<1, O>(a, st) : radius == 2 ? launch_cluster<2, O>(a, st)
+                                                                    : launch_cluster<3, O>(a, st);
+  return radius == 1 ? launch_grid<1, O>(a, st) : radius == 2 ? launch_grid<2, O>(a, st) : launch_grid<3, O>(a, st);
+}
+
+int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
                           cd* basis, cd* Rg, cd* gpart, long long n, double tol, int cap, int* its_out,
                           double* relres_out, cd* flag, cudaStream_t st) {
   init_limits();
-  ResidentArgs a;
+  ResidentArgs a{};
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
-  a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag;
-  bool ok;
-  if (mode == 0) {
-    ok = c.radius == 1 ? launch_cluster<1>(a, st) : c.radius == 2 ? launch_cluster<2>(a, st) : launch_cluster<3>(a, st);
-  } else {
-    ok = c.radius == 1 ? launch_grid<1>(a, st) : c.radius == 2 ? launch_grid<2>(a, st) : launch_grid<3>(a, st);
-  }
+  a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
+  if (ortho == 1 && cap + 1 > kVecCap) ortho = 0;
+  const bool ok = ortho ? launch_any<1>(mode, a, c.radius, st) : launch_any<0>(mode, a, c.radius, st);
   return ok ? 0 : 1;
 }
 

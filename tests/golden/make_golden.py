@@ -6,6 +6,10 @@ GPU box, where the reference does not exist.
 
     python tests/golden/make_golden.py            # unit-level fixtures (seconds)
     python tests/golden/make_golden.py --solves   # + full-solve records (minutes)
+
+solve_c2.npz (BASELINE configs[1], 27 min on 4 threads) is produced by
+    python tests/golden/run_reference_solve.py c2 /tmp/c2.npz --workers 4 --save-solution
+and reduced to history + every 32nd solution point by tests/golden/reduce_c2.py.
 """
 import json
 import os
