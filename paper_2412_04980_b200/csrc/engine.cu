@@ -128,6 +128,8 @@ cd* KWS::z(int i) {
 KWS::~KWS() {
   if (!engine_ready()) return;
   Engine& E = engine();
+  E.free(dV);
+  E.free(gpart);
   for (auto p : V) E.free(p);
   for (auto p : Z) E.free(p);
   E.free(tmp);
@@ -147,6 +149,12 @@ int resident_ortho() {
     o = (e && std::string(e) == "mgs") ? 0 : 1;
   }
   return o;
+}
+
+long long coop_mgs_min() {
+  static long long v = -1;
+  if (v < 0) v = env_ll("HDB_COOP_MGS_N", 150000);
+  return v > 0 ? v : (1LL << 62);
 }
 
 int resident_mode(long long n, int cap) {
@@ -264,12 +272,33 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     }
     cd* w = ws.v(j + 1);
     A(z, w);
-    // MGS chain (krylov.py:121-124), one fused launch per coefficient
-    launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st);
-    for (int i = 0; i < j; ++i)
-      launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
-    launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
-    E.launches += j + 2;
+    // MGS chain (krylov.py:121-124): one cooperative launch on large levels,
+    // else one fused launch per coefficient
+    bool coop = false;
+    if (n >= coop_mgs_min()) {
+      if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1));
+      if (ws.dV_cap < j + 1) {
+        E.free(ws.dV);
+        ws.dV_cap = std::max(2 * (j + 1), 64);
+        ws.dV = (cd**)E.alloc_bytes(sizeof(cd*) * ws.dV_cap);
+        ws.dV_n = 0;
+      }
+      while (ws.dV_n < j + 1) {  // append V pointers (their addresses never change)
+        cd* p = ws.v(ws.dV_n);
+        HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, &ws.V[ws.dV_n], sizeof(cd*), cudaMemcpyHostToDevice, E.st));
+        (void)p;
+        ws.dV_n++;
+      }
+      coop = launch_mgs_grid(w, (const cd* const*)ws.dV, j, n, ws.gpart, E.dscal + kSlotH, E.st) == 0;
+      if (coop) E.launches++;
+    }
+    if (!coop) {
+      launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st);
+      for (int i = 0; i < j; ++i)
+        launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
+      launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
+      E.launches += j + 2;
+    }
     E.fetch(kSlotH + j + 2);
     std::vector<cplx> col(j + 2);
     for (int i = 0; i <= j; ++i) col[i] = cplx(E.hscal[kSlotH + i].x, E.hscal[kSlotH + i].y);
@@ -310,8 +339,10 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
       conv = true;
       break;
     }
-    launch_scale(w, w, 1.0 / hn, n, E.st);  // V_{j+1} = w / hnext
-    E.launches++;
+    if (!coop) {  // the cooperative MGS already wrote V_{j+1} = w / hnext
+      launch_scale(w, w, 1.0 / hn, n, E.st);
+      E.launches++;
+    }
   }
   // least squares R y = g (krylov.py:161-168), solution update (169-172)
   const int m = its;

@@ -91,6 +91,9 @@ using LinOp = std::function<void(const cd* in, cd* out)>;
 struct KWS {
   long long n = 0;
   std::vector<cd*> V, Z;
+  cd** dV = nullptr;       // device table of V pointers (cooperative MGS)
+  int dV_cap = 0, dV_n = 0;
+  cd* gpart = nullptr;     // grid-reduction partials
   cd* tmp = nullptr;
   cd** dbasis = nullptr;  // device pointer table for the solution update
   cd* dy = nullptr;
@@ -113,7 +116,8 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
 // HDB_GRID_N points (default 2M) when the stencil windows fit shared memory.
 // 0 disables a mode.
 int resident_mode(long long n, int cap);  // -1: launch-driven path
-int resident_ortho();  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
+int resident_ortho();
+long long coop_mgs_min();  // levels >= this many points use the cooperative MGS step (HDB_COOP_MGS_N)  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
 
 struct SmallSolve {  // device-resident GMRES on one level operator
   const LevelOp* op = nullptr;

@@ -35,7 +35,9 @@ long long resident_cluster_points();
 long long resident_grid_points();
 int resident_grid_ctas();
 int resident_vec_cap();
-void resident_set_profile(long long* dev_counters);  // 8 per-phase cycle counters or null
+void resident_set_profile(long long* dev_counters);
+// one Arnoldi step's MGS chain in a cooperative launch (large levels); 1 = does not fit
+int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st);  // 8 per-phase cycle counters or null
 // ortho 0: modified Gram-Schmidt (reference order), 1: CGS2 (caps <= resident_vec_cap())
 int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
                           cd* basis, cd* Rg, cd* gpart, long long n, double tol, int cap, int* its_out,

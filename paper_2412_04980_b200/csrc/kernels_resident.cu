@@ -64,12 +64,15 @@ struct ResidentArgs {
     }                                                              \
   } while (0)
 
-constexpr int kVecCap = 130;  // max vector all-gather length (CGS2: cap + 1)
+constexpr int kVecCap = 402;     // CGS2 coefficient vectors (cap + 1), grid mode
+constexpr int kGatherCap = 130;  // cluster all-gather vector length (DSMEM buffers)
 
-typedef cd GatherBuf[2][16][kVecCap];  // [buffer][source rank][element] (cluster mode only)
+typedef cd GatherBuf[2][16][kGatherCap];  // [buffer][source rank][element] (cluster mode only)
 
 struct RSmem {
   uint64_t mbar[2];
+  cd coef[49];    // per-tap coefficients when this CTA's k^2 window is uniform
+  int uniform;
   cd pv[kVecCap];             // this CTA's block partial vector
   cd hv[kVecCap];             // reduced vector (CGS2 coefficients)
   cd warp[kRT / 32];
@@ -147,7 +150,7 @@ __device__ __forceinline__ void load_k_tile(double* kt, const Tile& T, const dou
 // (A u) at global (gj, i) from the windows (same arithmetic as the launch kernels)
 template <int R>
 __device__ __forceinline__ cd op_point_tile(const OpCoef& c, const Geom& g, const Tile& T, const cd* ut,
-                                            const double* kt, int gj, int i) {
+                                            const double* kt, const cd* ucoef, int gj, int i) {
   const int tr = gj - T.rlo + R, tc = i + R;
   const cd* uc = ut + tr * T.cols + tc;
   if (pinned(g, c, gj, i)) return *uc;
@@ -158,6 +161,14 @@ __device__ __forceinline__ cd op_point_tile(const OpCoef& c, const Geom& g, cons
   const cd* u0 = uc - R * T.cols - R;
   const double* k0 = kt + (tr - R) * T.cols + tc - R;
   cd acc = mkc(0.0, 0.0);
+  if (ucoef) {  // uniform k^2 window: same rounded coefficients, formed once
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+#pragma unroll
+      for (int bb = 0; bb < N; ++bb) acc = c_add(acc, c_mul(ucoef[a * N + bb], u0[a * T.cols + bb]));
+    }
+    return acc;
+  }
 #pragma unroll
   for (int a = 0; a < N; ++a) {
 #pragma unroll
@@ -232,6 +243,7 @@ constexpr int kMaxCluster = 16;
 
 struct ClusterSync {
   static constexpr bool kGather = true;
+  static constexpr int kVecMax = kGatherCap;
   cg::cluster_group cl;
   uint32_t par[2];
   GatherBuf* gb = nullptr;  // in dynamic shared memory after RSmem
@@ -284,6 +296,7 @@ struct ClusterSync {
 
 struct GridSync {
   static constexpr bool kGather = false;
+  static constexpr int kVecMax = kVecCap;
   cg::grid_group gr;
   __device__ GridSync() : gr(cg::this_grid()) {}
   __device__ int rank() const { return (int)blockIdx.x; }
@@ -388,6 +401,25 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   cd* ut = A.tiled ? ws + chunk_max : nullptr;                 // stencil window of the current vector
   double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
   if (A.tiled && cnt > 0) load_k_tile<R>(kt, T, A.ksq, A.g, A.c);
+  const cd* ucoef = nullptr;
+  if (A.tiled && R > 1) {
+    if (threadIdx.x == 0) s.uniform = cnt > 0;
+    __syncthreads();
+    const int ne = T.rows * T.cols;
+    const double k00 = cnt > 0 ? kt[0] : 0.0;
+    for (int e = threadIdx.x; e < ne; e += kRT)
+      if (kt[e] != k00) s.uniform = 0;
+    __syncthreads();
+    if (s.uniform) {
+      constexpr int NN = (2 * R + 1) * (2 * R + 1);
+      if (threadIdx.x < NN) {
+        const cd m = A.c.mass[threadIdx.x];
+        s.coef[threadIdx.x] = mkc(__dadd_rn(A.c.lap[threadIdx.x], __dmul_rn(m.x, k00)), __dmul_rn(m.y, k00));
+      }
+      ucoef = s.coef;
+    }
+    __syncthreads();
+  }
   const int t = threadIdx.x;
   const int nx = A.g.nx;
   int buf = 0;
@@ -430,7 +462,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       __syncthreads();
       for (int q = t; q < cnt; q += kRT) {
         const long long p = p0 + q;
-        ws[q] = op_point_tile<R>(A.c, A.g, T, ut, kt, (int)(p / nx) + A.g.row0, (int)(p % nx));
+        ws[q] = op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, (int)(p / nx) + A.g.row0, (int)(p % nx));
       }
     } else {
       for (int q = t; q < cnt; q += kRT) {
@@ -563,7 +595,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   for (int q = t; q < cnt; q += kRT) {
     const long long p = p0 + q;
     const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
-    const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
+    const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
     const cd d = c_sub(A.b[p], ax);
     f = c_conjmul_acc(f, d, d);
   }
@@ -679,7 +711,7 @@ static bool launch_grid(ResidentArgs a, cudaStream_t st) {
 }
 
 int resident_max_cap() { return kMaxCap; }
-int resident_vec_cap() { return kVecCap - 1; }
+int resident_vec_cap() { return kVecCap - 1; }  // gpart stride - 1
 
 long long resident_cluster_points() {
   init_limits();
@@ -708,7 +740,7 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
   ResidentArgs a{};
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
   a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
-  if (ortho == 1 && cap + 1 > kVecCap) ortho = 0;
+  if (ortho == 1 && cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
   const bool ok = ortho ? launch_any<1>(mode, a, c.radius, st) : launch_any<0>(mode, a, c.radius, st);
   return ok ? 0 : 1;
 }
@@ -716,6 +748,83 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
 int resident_grid_ctas() {
   init_limits();
   return g_grid;
+}
+
+}  // namespace hdb
+
+namespace hdb {
+
+// ---------------------------------------------------------------------------
+// One Arnoldi step's modified Gram-Schmidt for large levels (the launch-driven
+// engine's MGS chain in ONE cooperative launch): w (= A z, global) is held in
+// shared memory across the chain; each step reads V_i once (the thread keeps
+// its V_i values in registers between the dot and the update) and does one
+// deterministic grid reduction.  Writes h_i to hout[i], ||w||^2 to hout[j+1].x
+// and, as the launch path does after the host's stopping test, V_{j+1} =
+// w * (1/||w||) into w's buffer (harmless when the step converges).
+// Same arithmetic as k_mgs (krylov.py:121-124).
+constexpr int kMgsPPT = 16;  // points per thread held in registers
+
+__global__ void __launch_bounds__(kRT) k_mgs_grid(cd* w, const cd* const* V, int j, long long n, cd* gpart,
+                                                  cd* hout) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  RSmem& s = *reinterpret_cast<RSmem*>(smem_raw);
+  cd* ws = reinterpret_cast<cd*>(smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);
+  GridSync sy;
+  const int P = gridDim.x, rank = blockIdx.x, t = threadIdx.x;
+  const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
+  const int cnt = (int)(p1 - p0);
+  int buf = 0;
+  for (int q = t; q < cnt; q += kRT) ws[q] = w[p0 + q];
+  for (int i = 0; i <= j; ++i) {
+    const cd* vi = V[i] + p0;
+    cd vr[kMgsPPT];
+    cd a = mkc(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < kMgsPPT; ++k) {
+      const int q = t + k * kRT;
+      vr[k] = q < cnt ? vi[q] : mkc(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < kMgsPPT; ++k) {
+      const int q = t + k * kRT;
+      if (q < cnt) a = c_conjmul_acc(a, vr[k], ws[q]);
+    }
+    for (int q = t + kMgsPPT * kRT; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
+    const cd h = sy.reduce(a, s, buf, gpart);
+    if (rank == 0 && t == 0) hout[i] = h;
+#pragma unroll
+    for (int k = 0; k < kMgsPPT; ++k) {
+      const int q = t + k * kRT;
+      if (q < cnt) ws[q] = c_sub(ws[q], c_mul_np(h, vr[k]));
+    }
+    for (int q = t + kMgsPPT * kRT; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
+  }
+  cd a = mkc(0.0, 0.0);
+  for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+  const cd nn = sy.reduce(a, s, buf, gpart);
+  if (rank == 0 && t == 0) hout[j + 1] = nn;
+  const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
+  const double inv = 1.0 / hn;
+  for (int q = t; q < cnt; q += kRT) {
+    const cd v = ws[q];
+    w[p0 + q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+  }
+}
+
+// returns 0 when launched, 1 when the level does not fit (caller: launch chain)
+int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st) {
+  init_limits();
+  const long long chunk = (n + g_grid - 1) / g_grid;
+  const size_t sm = smem_for(chunk, false);
+  if (sm > g_smem_optin || chunk > (long long)kMgsPPT * kRT * 2) return 1;
+  static size_t configured = 0;
+  if (sm > configured) {
+    cudaFuncSetAttribute(k_mgs_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    configured = sm;
+  }
+  void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout};
+  return cudaLaunchCooperativeKernel((void*)k_mgs_grid, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
 }
 
 }  // namespace hdb
