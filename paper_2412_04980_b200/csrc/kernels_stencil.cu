@@ -52,6 +52,119 @@ __global__ void __launch_bounds__(256) k_r1(const cd* __restrict__ u, const cd* 
 }
 
 // ------------------------------------------------------------------------
+// radius 1, column-strip form (the hot fine-level kernel).  A warp owns 32
+// consecutive columns; each thread walks RB rows keeping rows j-1, j, j+1 of
+// its column in registers (one new row load per output row); W/E come from
+// lane shuffles (edge lanes load their outer neighbour).  Blocks that touch a
+// physical boundary or a slab edge take the per-point closure path.  Same
+// arithmetic as k_r1 (bit-identical).
+constexpr int SX = 32, SY = 4, RB = 16;  // block 32x4 threads, 16 rows per thread
+
+template <int MODE>
+__global__ void __launch_bounds__(SX * SY) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                 const double* __restrict__ k, cd* __restrict__ out, Geom g,
+                                                 OpCoef c, double omega) {
+  const int i = blockIdx.x * SX + threadIdx.x;
+  const int jbeg = (blockIdx.y * SY + threadIdx.y) * RB;  // local row
+  const int gi0 = blockIdx.x * SX, gj0 = g.row0 + blockIdx.y * SY * RB;
+  const int gj1 = gj0 + SY * RB;  // exclusive
+  const bool interior = gi0 >= 1 && gi0 + SX <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
+                        blockIdx.y * SY * RB + SY * RB <= g.ny;
+  if (!interior) {
+    // generic per-point path (boundaries, ragged edges)
+    if (i >= g.nx) return;
+    for (int r = 0; r < RB; ++r) {
+      const int j = jbeg + r;
+      if (j >= g.ny) return;
+      const int gj = j + g.row0;
+      const long long p = (long long)j * g.nx + i;
+      if (MODE == 3) {
+        const cd bb = b[p];
+        if (pinned(g, c, gj, i)) { out[p] = c_scale(omega, bb); continue; }
+        out[p] = c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), bb);
+        continue;
+      }
+      const cd uc = u[p];
+      if (pinned(g, c, gj, i)) {
+        if (MODE == 0) out[p] = uc;
+        else if (MODE == 1) out[p] = c_sub(b[p], uc);
+        else out[p] = c_add(uc, c_scale(omega, c_sub(b[p], uc)));
+        continue;
+      }
+      const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
+                               upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
+      if (MODE == 0) { out[p] = Au; continue; }
+      const cd r1 = c_sub(b[p], Au);
+      if (MODE == 1) { out[p] = r1; continue; }
+      out[p] = c_add(uc, c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), r1));
+    }
+    return;
+  }
+  // interior fast path: no closure, no pinning; every (i, j) and its neighbours exist
+  const int lane = threadIdx.x;
+  const long long nx = g.nx;
+  const cd* up = u + (long long)jbeg * nx + i;
+  if (MODE == 3) {
+    const double* kp = k + (long long)jbeg * nx + i;
+    const cd* bp = b + (long long)jbeg * nx + i;
+    cd* op = out + (long long)jbeg * nx + i;
+#pragma unroll 4
+    for (int r = 0; r < RB; ++r) {
+      const double kc = kp[r * nx];
+      // interior diagonal: 4s + mc k (no Sommerfeld terms), Smith reciprocal
+      const double dr = __dadd_rn(4.0 * c.s, __dmul_rn(c.mc.x, kc)), di = __dmul_rn(c.mc.y, kc);
+      cd d;
+      if (fabs(dr) >= fabs(di)) {
+        const double rat = __ddiv_rn(di, dr), scl = __ddiv_rn(1.0, __dadd_rn(dr, __dmul_rn(di, rat)));
+        d = mkc(scl, __dmul_rn(-rat, scl));
+      } else {
+        const double rat = __ddiv_rn(dr, di), scl = __ddiv_rn(1.0, __dadd_rn(di, __dmul_rn(dr, rat)));
+        d = mkc(__dmul_rn(rat, scl), -scl);
+      }
+      op[r * nx] = c_mul(c_scale(omega, d), bp[r * nx]);
+    }
+    return;
+  }
+  cd s_ = up[-nx], c_ = up[0];
+#pragma unroll 2
+  for (int r = 0; r < RB; ++r) {
+    const long long o = (long long)r * nx;
+    const cd n_ = up[o + nx];
+    cd w_, e_;
+    w_.x = __shfl_up_sync(0xffffffffu, c_.x, 1);
+    w_.y = __shfl_up_sync(0xffffffffu, c_.y, 1);
+    e_.x = __shfl_down_sync(0xffffffffu, c_.x, 1);
+    e_.y = __shfl_down_sync(0xffffffffu, c_.y, 1);
+    if (lane == 0) w_ = up[o - 1];
+    if (lane == SX - 1) e_ = up[o + 1];
+    const long long pp = (long long)(jbeg + r) * nx + i;
+    const cd Au = five_point(c.s, c.mc, k[pp], c_, w_, e_, s_, n_);
+    if (MODE == 0) {
+      out[pp] = Au;
+    } else {
+      const cd r1 = c_sub(b[pp], Au);
+      if (MODE == 1) {
+        out[pp] = r1;
+      } else {
+        const double kc = k[pp];
+        const double dr = __dadd_rn(4.0 * c.s, __dmul_rn(c.mc.x, kc)), di = __dmul_rn(c.mc.y, kc);
+        cd d;
+        if (fabs(dr) >= fabs(di)) {
+          const double rat = __ddiv_rn(di, dr), scl = __ddiv_rn(1.0, __dadd_rn(dr, __dmul_rn(di, rat)));
+          d = mkc(scl, __dmul_rn(-rat, scl));
+        } else {
+          const double rat = __ddiv_rn(dr, di), scl = __ddiv_rn(1.0, __dadd_rn(di, __dmul_rn(dr, rat)));
+          d = mkc(__dmul_rn(rat, scl), -scl);
+        }
+        out[pp] = c_add(c_, c_mul(c_scale(omega, d), r1));
+      }
+    }
+    s_ = c_;
+    c_ = n_;
+  }
+}
+
+// ------------------------------------------------------------------------
 // radius 2/3: shared-memory tile of the ghost-closed u and k^2 windows, then
 // the reference's row-major tap order (_kernels.py:44-50):
 //   acc += (lap[o] + mass[o]*kpad) * upad
@@ -100,10 +213,18 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
 
 // ------------------------------------------------------------------------
 static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny + 7) / 8); }
+static inline dim3 grid_r1s(const Geom& g) { return dim3((g.nx + SX - 1) / SX, (g.ny + SY * RB - 1) / (SY * RB)); }
+static inline bool use_strip(const Geom& g) { return g.nx >= 64 && g.ny >= SY * RB; }
 
 void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
                   int mode, cudaStream_t st) {
   if (c.radius == 1) {
+    if (use_strip(g)) {
+      const dim3 blk(SX, SY), grd = grid_r1s(g);
+      if (mode == 0) k_r1s<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+      else k_r1s<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+      return;
+    }
     const dim3 blk(32, 8), grd = grid_r1(g);
     if (mode == 0) k_r1<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
     else k_r1<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
@@ -121,6 +242,12 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
 
 void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out,
                    double omega, bool from_zero, cudaStream_t st) {
+  if (use_strip(g)) {
+    const dim3 blk(SX, SY), grd = grid_r1s(g);
+    if (from_zero) k_r1s<3><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+    else k_r1s<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+    return;
+  }
   const dim3 blk(32, 8), grd = grid_r1(g);
   if (from_zero) k_r1<3><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
   else k_r1<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
