@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_r1(const cd* __restrict__ u, const cd* 
 constexpr int SX = 32, SY = 4, RB = 16;  // block 32x4 threads, 16 rows per thread
 
 template <int MODE>
-__global__ void __launch_bounds__(SX * SY) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
+__global__ void __launch_bounds__(SX * SY, 8) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
                                                  const double* __restrict__ k, cd* __restrict__ out, Geom g,
                                                  OpCoef c, double omega) {
   const int i = blockIdx.x * SX + threadIdx.x;
