@@ -53,6 +53,14 @@ int hdb_set_stream(void* stream);
 int hdb_sync(void);
 /* kernels launched through the library so far, device bytes allocated */
 int hdb_stats(long long* launches, long long* bytes_alloc);
+/* ranks: one process per GPU over NCCL (id from hdb_comm_unique_id on rank 0,
+ * broadcast by the caller), or host threads of one process, each with its own
+ * engine (hdb_thread_engine_begin) — used to test the slab path on one GPU    */
+int hdb_comm_unique_id(char* out128);
+int hdb_comm_init_nccl(const char* id128, int nranks, int rank);
+int hdb_comm_init_threads(long long group, int nranks, int rank);
+int hdb_thread_engine_begin(int device);
+int hdb_thread_engine_end(void);
 
 /* ---- level operators: replaces LevelOperator (operators.py:96-208) -------- */
 /* lap: (2r+1)^2 float coefficients = lap_coef (operators.py:111);
@@ -61,6 +69,13 @@ int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int*
                   const double* lap, const double* mass_re, const double* mass_im,
                   const double* ksq_host);
 int hdb_op_destroy(hdb_op* op);
+/* row slab [row0, row0+ny_local) of a level with ny_global rows (row-slab
+ * decomposition); `halo` rows (>= radius, >= 2) are carried by
+ * this level's vectors; slab_row0/slab_ny: every rank's slab                  */
+int hdb_op_create_slab(hdb_op** out, int nx, int ny_global, int radius, double h, const int* bc4,
+                       const double* lap, const double* mass_re, const double* mass_im,
+                       const double* ksq_full_host, int row0, int ny_local, int halo, int nranks,
+                       const int* slab_row0, const int* slab_ny);
 /* LevelOperator.apply (operators.py:130-147): out = A u, Dirichlet rows pinned */
 int hdb_op_apply(hdb_op* op, const void* u, void* out);
 /* out = b - A u  (MG residual mg.py:116, A-DEF1 v - A t madp.py:325-326) */

@@ -21,7 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          f"-I{os.path.join(os.path.dirname(PKG), 'include')}"]
 SOURCES = ["kernels_stencil.cu", "kernels_transfer.cu", "kernels_blas.cu", "kernels_resident.cu", "engine.cu",
-           "capi.cu"]
+           "comm.cu", "capi.cu"]
 
 
 def _stale(force: bool) -> bool:
@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = OUT + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", tmp, *objs]
+    cmd = [NVCC, *ARCH, "-shared", "--cudart", "static", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -32,6 +32,13 @@ SIGNATURES = {
     "hdb_stats": [P(i64), P(i64)],
     "hdb_op_create": [P(vp), i32, i32, i32, f64, P(i32), P(f64), P(f64), P(f64), P(f64)],
     "hdb_op_destroy": [vp],
+    "hdb_op_create_slab": [P(vp), i32, i32, i32, f64, P(i32), P(f64), P(f64), P(f64), P(f64), i32, i32, i32, i32,
+                           P(i32), P(i32)],
+    "hdb_comm_unique_id": [C.c_char_p],
+    "hdb_comm_init_nccl": [C.c_char_p, i32, i32],
+    "hdb_comm_init_threads": [i64, i32, i32],
+    "hdb_thread_engine_begin": [i32],
+    "hdb_thread_engine_end": [],
     "hdb_op_apply": [vp, vp, vp],
     "hdb_op_residual": [vp, vp, vp, vp],
     "hdb_op_jacobi": [vp, vp, vp, vp, f64],

@@ -1,5 +1,6 @@
 // extern "C" boundary (declared in include/hdb200.h).  Every entry point
 // catches engine exceptions and turns them into a status + message.
+#include <algorithm>
 #include <cstring>
 #include <string>
 
@@ -100,10 +101,74 @@ int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int*
   });
 }
 
+// a row slab [row0, row0+ny_local) of a level with ny_global rows; `halo` rows of
+// k^2 are copied around it (from the full host array), vectors of this level
+// carry `halo` halo rows; slab_row0/slab_ny list every rank's slab.
+int hdb_op_create_slab(hdb_op** out, int nx, int ny_global, int radius, double h, const int* bc4, const double* lap,
+                       const double* mass_re, const double* mass_im, const double* ksq_full_host, int row0,
+                       int ny_local, int halo, int nranks, const int* slab_row0, const int* slab_ny) {
+  return guarded([&] {
+    if (halo < radius || halo < 2) throw Error(E_ARG, "halo must cover the stencil radius and the transfer (2)");
+    if (ny_local < halo) throw Error(E_ARG, "slab thinner than its halo");
+    hdb_op* o = nullptr;
+    // build the coefficients through the full-grid path on a dummy k^2, then replace geometry
+    const int st = hdb_op_create(&o, nx, std::max(ny_local, 2), radius, h, bc4, lap, mass_re, mass_im, ksq_full_host);
+    if (st != HDB_OK) throw Error(st, g_err);
+    Engine& E = engine();
+    LevelOp& L = o->op;
+    E.free(L.ksq);
+    L.g.nx = nx; L.g.ny = ny_local; L.g.row0 = row0; L.g.nyg = ny_global;
+    L.n = (long long)nx * ny_local;
+    L.H = halo;
+    L.sharded = nranks > 1;
+    L.slab_row0.assign(slab_row0, slab_row0 + nranks);
+    L.slab_ny.assign(slab_ny, slab_ny + nranks);
+    const long long hel = (long long)halo * nx;
+    double* base = (double*)E.alloc_bytes(sizeof(double) * (L.n + 2 * hel));
+    HDB_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (L.n + 2 * hel), E.st));
+    L.ksq = base + hel;
+    const int r_lo = std::max(0, row0 - halo), r_hi = std::min(ny_global, row0 + ny_local + halo);
+    HDB_CUDA(cudaMemcpyAsync(L.ksq + (long long)(r_lo - row0) * nx, ksq_full_host + (long long)r_lo * nx,
+                             sizeof(double) * (size_t)(r_hi - r_lo) * nx, cudaMemcpyHostToDevice, E.st));
+    HDB_CUDA(cudaStreamSynchronize(E.st));
+    *out = o;
+  });
+}
+
+int hdb_comm_unique_id(char* out128) {
+  return guarded([&] { nccl_unique_id(out128); });
+}
+int hdb_comm_init_nccl(const char* id128, int nranks, int rank) {
+  return guarded([&] {
+    Engine& E = engine();
+    delete E.comm;
+    E.comm = nullptr;
+    if (nranks > 1) E.comm = make_nccl_comm(id128, nranks, rank);
+  });
+}
+int hdb_comm_init_threads(long long group, int nranks, int rank) {
+  return guarded([&] {
+    Engine& E = engine();
+    delete E.comm;
+    E.comm = nullptr;
+    if (nranks > 1) E.comm = make_thread_comm(group, nranks, rank);
+  });
+}
+int hdb_thread_engine_begin(int device) {
+  return guarded([&] { thread_engine_begin(device); });
+}
+int hdb_thread_engine_end(void) {
+  return guarded([&] { thread_engine_end(); });
+}
+
 int hdb_op_destroy(hdb_op* op) {
   return guarded([&] {
     if (!op) return;
-    if (engine_ready()) { engine().sync(); engine().free(op->op.ksq); engine().free(op->dres); }
+    if (engine_ready()) {
+      engine().sync();
+      engine().free(op->op.ksq - op->op.halo_elems());
+      engine().free(op->dres);
+    }
     delete op;
   });
 }
@@ -126,14 +191,15 @@ int hdb_restrict(const void* fine, int nfy, int nfx, void* coarse, int zero_mask
   return guarded([&] {
     if ((nfx - 1) % 2 || (nfy - 1) % 2 || nfx < 3 || nfy < 3)
       throw Error(E_ARG, "cannot coarsen: n-1 must be even (transfers.py:53-56)");
-    launch_restrict((const cd*)fine, (cd*)coarse, nfx, nfy, zero_mask, engine().st);
+    launch_restrict((const cd*)fine, (cd*)coarse, full_tgeom(nfx, nfy), zero_mask, engine().st);
     check_launch();
   });
 }
 int hdb_prolong(const void* coarse, int nfy, int nfx, const void* base, void* fine) {
   return guarded([&] {
     if ((nfx - 1) % 2 || (nfy - 1) % 2) throw Error(E_ARG, "fine shape does not refine the coarse grid");
-    launch_prolong((const cd*)coarse, (const cd*)base, (cd*)fine, nfx, nfy, base != nullptr, engine().st);
+    launch_prolong((const cd*)coarse, (const cd*)base, (cd*)fine, full_tgeom(nfx, nfy), base != nullptr,
+                   engine().st);
     check_launch();
   });
 }

@@ -34,6 +34,7 @@ Engine::Engine(int dev) : device(dev) {
 Engine::~Engine() {
   cudaStreamSynchronize(st);
   if (own_st) st = own_st;
+  delete comm;
   cudaFree(red.partials);
   cudaFree(red.ticket);
   cudaFree(dscal);
@@ -69,9 +70,22 @@ double Engine::fetch_norm(int slot) {
   return std::sqrt(v > 0.0 ? v : 0.0);
 }
 
+static thread_local Engine* t_engine = nullptr;
+
 Engine& engine() {
+  if (t_engine) return *t_engine;
   if (!g_engine) throw Error(E_ARG, "hdb_init() has not been called");
   return *g_engine;
+}
+
+void thread_engine_begin(int device) {
+  if (t_engine) return;
+  t_engine = new Engine(device);
+}
+
+void thread_engine_end() {
+  delete t_engine;
+  t_engine = nullptr;
 }
 
 void engine_init(int device) {
@@ -80,22 +94,92 @@ void engine_init(int device) {
   g_engine.reset(new Engine(device));
 }
 
-bool engine_ready() { return (bool)g_engine; }
+bool engine_ready() { return t_engine || (bool)g_engine; }
 
 // --------------------------------------------------------------- level op
+void LevelOp::exchange(const cd* u, int rows) const {
+  if (!sharded) return;
+  Engine& E = engine();
+  if (!E.comm) throw Error(E_ARG, "sharded level without a communicator");
+  if (rows > H) throw Error(E_ARG, "halo exchange wider than the allocated halo");
+  cd* v = const_cast<cd*>(u);
+  const long long nx = g.nx;
+  const size_t bytes = sizeof(cd) * (size_t)rows * nx;
+  E.comm->exchange(v, v - rows * nx, bytes, v + (long long)(g.ny - rows) * nx, v + (long long)g.ny * nx, bytes, E.st);
+}
+
+void LevelOp::reduce(cd* slot) const {
+  if (!sharded) return;
+  Engine& E = engine();
+  E.comm->allreduce((double*)slot, 2, E.st);
+}
+
 void LevelOp::apply(const cd* u, cd* out) const {
   Engine& E = engine();
+  exchange(u, c.radius);
   launch_apply(c, g, u, nullptr, ksq, out, 0, E.st);
   E.launches++;
 }
 void LevelOp::residual(const cd* b, const cd* u, cd* out) const {
   Engine& E = engine();
+  exchange(u, c.radius);
   launch_apply(c, g, u, b, ksq, out, 1, E.st);
   E.launches++;
 }
 void LevelOp::jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const {
   Engine& E = engine();
+  if (!from_zero) exchange(x, 1);
   launch_jacobi(c, g, x, b, ksq, out, omega, from_zero, E.st);
+  E.launches++;
+}
+
+// ----------------------------------------------------------- level transfers
+TGeom level_tgeom(const LevelOp& f, const LevelOp& c) {
+  TGeom t;
+  t.nfx = f.g.nx; t.f_row0 = f.g.row0; t.f_ny = f.g.ny; t.nfy_g = f.g.nyg;
+  t.ncx = c.g.nx; t.c_row0 = c.g.row0; t.c_ny = c.g.ny; t.ncy_g = c.g.nyg;
+  return t;
+}
+
+// coarse slab of this rank under a fine slab (nested partition)
+static void coarse_slab_of(const LevelOp& f, int rank, int ncy_g, int& row0, int& ny) {
+  const int P = (int)f.slab_row0.size();
+  row0 = f.slab_row0[rank] / 2;
+  const int end = rank == P - 1 ? ncy_g : f.slab_row0[rank + 1] / 2;
+  ny = end - row0;
+}
+
+void restrict_levels(const LevelOp& f, const LevelOp& c, const cd* fine, cd* out, cd* slab, int zero_mask) {
+  Engine& E = engine();
+  f.exchange(fine, 2);
+  if (f.sharded && !c.sharded) {
+    // restrict this rank's part of the coarse grid, then gather the replicated vector
+    TGeom t = level_tgeom(f, c);
+    const int P = E.comm->size;
+    int r0, rn;
+    coarse_slab_of(f, E.comm->rank, c.g.nyg, r0, rn);
+    t.c_row0 = r0;
+    t.c_ny = rn;
+    launch_restrict(fine, slab, t, zero_mask, E.st);
+    E.launches++;
+    std::vector<size_t> off(P), bytes(P);
+    for (int r = 0; r < P; ++r) {
+      int a, n;
+      coarse_slab_of(f, r, c.g.nyg, a, n);
+      off[r] = sizeof(cd) * (size_t)a * c.g.nx;
+      bytes[r] = sizeof(cd) * (size_t)n * c.g.nx;
+    }
+    E.comm->allgatherv(slab, out, off, bytes, E.st);
+    return;
+  }
+  launch_restrict(fine, out, level_tgeom(f, c), zero_mask, E.st);
+  E.launches++;
+}
+
+void prolong_levels(const LevelOp& c, const LevelOp& f, const cd* coarse, const cd* base, cd* fine) {
+  Engine& E = engine();
+  c.exchange(coarse, 1);
+  launch_prolong(coarse, base, fine, level_tgeom(f, c), base != nullptr, E.st);
   E.launches++;
 }
 
@@ -104,7 +188,7 @@ void KWS::ensure(long long n_, int cap_, bool flexible) {
   Engine& E = engine();
   if (n_ != n && n != 0) throw Error(E_ARG, "Krylov workspace reused with a different vector length");
   n = n_;
-  if (!tmp) tmp = E.alloc(n);
+  if (!tmp) tmp = E.alloc_h(n, halo);
   if (cap_ + 1 > cap) {
     if (dbasis) { E.free(dbasis); E.free(dy); cudaFreeHost(hbasis); cudaFreeHost(hy); }
     cap = cap_ + 1;
@@ -117,11 +201,11 @@ void KWS::ensure(long long n_, int cap_, bool flexible) {
 }
 
 cd* KWS::v(int i) {
-  while ((int)V.size() <= i) V.push_back(engine().alloc(n));
+  while ((int)V.size() <= i) V.push_back(engine().alloc_h(n, halo));
   return V[i];
 }
 cd* KWS::z(int i) {
-  while ((int)Z.size() <= i) Z.push_back(engine().alloc(n));
+  while ((int)Z.size() <= i) Z.push_back(engine().alloc_h(n, halo));
   return Z[i];
 }
 
@@ -130,9 +214,9 @@ KWS::~KWS() {
   Engine& E = engine();
   E.free(dV);
   E.free(gpart);
-  for (auto p : V) E.free(p);
-  for (auto p : Z) E.free(p);
-  E.free(tmp);
+  for (auto p : V) E.free_h(p, halo);
+  for (auto p : Z) E.free_h(p, halo);
+  E.free_h(tmp, halo);
   if (dbasis) { E.free(dbasis); E.free(dy); cudaFreeHost(hbasis); cudaFreeHost(hy); }
 }
 
@@ -210,7 +294,11 @@ SmallSolve::~SmallSolve() {
 static const double kHappy = 1e-30;  // krylov.py:28
 
 KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
-               const std::function<void(int, double)>* hook, const cd* x0) {
+               const std::function<void(int, double)>* hook, const cd* x0, const LevelOp* dist) {
+  const bool shard = dist && dist->sharded;
+  auto red = [&](cd* slot) {
+    if (shard) dist->reduce(slot);
+  };
   Engine& E = engine();
   if (stop.max_iters < 1) throw Error(E_ARG, "max_iters must be >= 1");
   if (stop.max_iters + kSlotH + 2 >= kSlotMgPost) throw Error(E_ARG, "Krylov iteration cap too large");
@@ -219,6 +307,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
 
   launch_dot(b, b, n, E.red, E.dscal + kSlotH, E.st);
   E.launches++;
+  red(E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   const double bnorm = E.fetch_norm(kSlotH);
   auto copy_x0 = [&] {
@@ -233,6 +322,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     launch_add(b, ws.tmp, ws.tmp, n, 1, E.st);
     launch_dot(ws.tmp, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
     E.launches += 2;
+    red(E.dscal + kSlotH);
     r0 = ws.tmp;
   }
   if (bnorm == 0.0) {  // krylov.py:96-97
@@ -275,7 +365,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     // MGS chain (krylov.py:121-124): one cooperative launch on large levels,
     // else one fused launch per coefficient
     bool coop = false;
-    if (n >= coop_mgs_min()) {
+    if (!shard && n >= coop_mgs_min()) {
       if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1));
       if (ws.dV_cap < j + 1) {
         E.free(ws.dV);
@@ -294,9 +384,13 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     }
     if (!coop) {
       launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st);
-      for (int i = 0; i < j; ++i)
+      red(E.dscal + kSlotH);
+      for (int i = 0; i < j; ++i) {
         launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
+        red(E.dscal + kSlotH + i + 1);
+      }
       launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
+      red(E.dscal + kSlotH + j + 1);
       E.launches += j + 2;
     }
     E.fetch(kSlotH + j + 2);
@@ -364,6 +458,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   A(x, ws.tmp);
   launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
   E.launches++;
+  red(E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   const double fin = E.fetch_norm(kSlotH) / bnorm;
   if (!std::isfinite(fin)) throw Error(E_NONFINITE, "non-finite solution");
@@ -384,20 +479,27 @@ static int dirichlet_mask(const OpCoef& c) {
 void Multigrid::setup() {
   Engine& E = engine();
   const int L = (int)ops.size();
-  X.assign(L, nullptr); Y.assign(L, nullptr); R.assign(L, nullptr); B.assign(L, nullptr); O.assign(L, nullptr);
+  for (auto v : {&X, &Y, &R, &B, &O, &S}) v->assign(L, nullptr);
   for (int i = 0; i < L; ++i) {
-    const long long n = ops[i]->n;
-    if (i < L - 1) { X[i] = E.alloc(n); Y[i] = E.alloc(n); R[i] = E.alloc(n); }
-    if (i > 0) { B[i] = E.alloc(n); O[i] = E.alloc(n); }
+    const long long n = ops[i]->n, h = ops[i]->halo_elems();
+    if (i < L - 1) { X[i] = E.alloc_h(n, h); Y[i] = E.alloc_h(n, h); R[i] = E.alloc_h(n, h); }
+    if (i > 0) {
+      B[i] = E.alloc_h(n, h);
+      O[i] = E.alloc_h(n, h);
+      if (ops[i - 1]->sharded && !ops[i]->sharded) S[i] = E.alloc(n);  // local part before the gather
+    }
   }
-  R[0] = R[0] ? R[0] : E.alloc(ops[0]->n);
+  if (!R[0]) R[0] = E.alloc_h(ops[0]->n, ops[0]->halo_elems());
 }
 
 Multigrid::~Multigrid() {
   if (!engine_ready()) return;
   Engine& E = engine();
-  for (auto v : {&X, &Y, &R, &B, &O})
-    for (auto p : *v) E.free(p);
+  for (size_t i = 0; i < ops.size() && i < X.size(); ++i) {
+    const long long h = ops[i]->halo_elems();
+    for (auto v : {&X, &Y, &R, &B, &O}) E.free_h((*v)[i], h);
+    E.free(S[i]);
+  }
   E.free(Ainv);
 }
 
@@ -417,11 +519,12 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
       bool done = false;
       if (resident_mode(op->n, coarse_stop.max_iters) >= 0) {
         small_coarse.ensure(op, coarse_stop.max_iters);
-        done = small_coarse.try_run(b, x, coarse_stop, (int*)(E2.dscal + kSlotMisc), (double*)(E2.dscal + kSlotMisc) + 1);
+        done = !op->sharded && small_coarse.try_run(b, x, coarse_stop, (int*)(E2.dscal + kSlotMisc), (double*)(E2.dscal + kSlotMisc) + 1);
       }
       if (!done) {
         LinOp A = [op](const cd* in, cd* out) { op->apply(in, out); };
-        fgmres(op->n, A, nullptr, b, x, coarse_stop, coarse_ws);
+        coarse_ws.halo = op->halo_elems();
+        fgmres(op->n, A, nullptr, b, x, coarse_stop, coarse_ws, nullptr, nullptr, op);
       }
     }
     return;
@@ -442,12 +545,10 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
   // coarse-grid correction
   op->residual(b, cur, R[i]);
   const LevelOp* co = ops[i + 1];
-  launch_restrict(R[i], B[i + 1], op->g.nx, op->g.ny, dirichlet_mask(co->c), E.st);
-  E.launches++;
+  restrict_levels(*op, *co, R[i], B[i + 1], S[i + 1], dirichlet_mask(co->c));
   cycle(i + 1, B[i + 1], O[i + 1], nullptr);
   cd* dst = (post == 0) ? x : oth;
-  launch_prolong(O[i + 1], cur, dst, op->g.nx, op->g.ny, 1, E.st);
-  E.launches++;
+  prolong_levels(*co, *op, O[i + 1], cur, dst);
   if (post == 0) return;
   std::swap(cur, dst);  // cur = corrected iterate, dst = free buffer
   for (int s = 0; s < post; ++s) {
@@ -467,12 +568,15 @@ void Multigrid::vcycle(const cd* b, cd* x, const cd* x0) {
     op->residual(b, x0, R[0]);
     launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgR0, E.st);
     E.launches++;
+    op->reduce(E.dscal + kSlotMgR0);
   }
   cycle(0, b, x, x0);
   // divergence guard (mg.py:133-138), evaluated on device; raised at the next host sync
   op->residual(b, x, R[0]);
   launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgPost, E.st);
   launch_dot(b, b, op->n, E.red, E.dscal + kSlotMgB, E.st);
+  op->reduce(E.dscal + kSlotMgPost);
+  op->reduce(E.dscal + kSlotMgB);
   launch_guard(E.dscal + kSlotMgPost, E.dscal + kSlotMgB, x0 ? E.dscal + kSlotMgR0 : nullptr, guard,
                E.dscal + kSlotFlag, E.st);
   E.launches += 3;
@@ -499,9 +603,16 @@ void MadpSolver::setup() {
   for (int l = 1; l <= ml; ++l) {
     MadpLevel& L = lv[l];
     if (!L.A) throw Error(E_ARG, "level operator missing");
-    const long long n = L.A->n;
-    if (l >= 2 && !L.vhat) { L.vhat = E.alloc(n); L.vtil = E.alloc(n); }
-    if (l < ml && !L.t) { L.t = E.alloc(n); L.rhs = E.alloc(n); L.r = E.alloc(n); }
+    const long long n = L.A->n, h = L.A->halo_elems();
+    L.ws_defl.halo = h;
+    L.ws_cslp.halo = h;
+    if (l >= 2 && !L.vhat) {
+      L.vhat = E.alloc_h(n, h);
+      L.vtil = E.alloc_h(n, h);
+      if (lv[l - 1].A->sharded && !L.A->sharded) L.slab = E.alloc(n);
+    }
+    if (l < ml && !L.t) { L.t = E.alloc_h(n, h); L.rhs = E.alloc_h(n, h); L.r = E.alloc_h(n, h); }
+    if (l == 1 && L.A->sharded && !L.xh) { L.bh = E.alloc_h(n, h); L.xh = E.alloc_h(n, h); }
   }
 }
 
@@ -509,7 +620,9 @@ MadpSolver::~MadpSolver() {
   if (!engine_ready()) return;
   Engine& E = engine();
   for (auto& L : lv) {
-    for (cd* p : {L.vhat, L.vtil, L.t, L.rhs, L.r}) E.free(p);
+    const long long h = L.A ? L.A->halo_elems() : 0;
+    for (cd* p : {L.vhat, L.vtil, L.t, L.rhs, L.r, L.bh, L.xh}) E.free_h(p, h);
+    E.free(L.slab);
   }
   E.free(dcounts);
   E.free(drel);
@@ -559,7 +672,7 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     return;
   }
   const LevelOp* M = L.M;
-  if (resident_mode(M->n, L.cslp_stop.max_iters) >= 0) {
+  if (!M->sharded && resident_mode(M->n, L.cslp_stop.max_iters) >= 0) {
     if (dused >= dcap) flush_counts();
     L.small_cslp.ensure(M, L.cslp_stop.max_iters);
     if (L.small_cslp.try_run(rhs, out, L.cslp_stop, dcounts + dused, drel + dused)) {
@@ -570,7 +683,7 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     }
   }
   LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
-  KReport r = fgmres(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_cslp);
+  KReport r = fgmres(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_cslp, nullptr, nullptr, M);
   rep.cslp_iters[l].push_back(r.iterations);
 }
 
@@ -593,8 +706,7 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   Engine& E = engine();
   MadpLevel& L = lv[l];
   MadpLevel& N = lv[l + 1];
-  launch_restrict(v, N.vhat, L.A->g.nx, L.A->g.ny, 0, E.st);
-  E.launches++;
+  restrict_levels(*L.A, *N.A, v, N.vhat, N.slab, 0);
   const int nxt = l + 1;
   LinOp Aop = [this, nxt](const cd* in, cd* o) { A(nxt, in, o); };
   LinOp Mop;
@@ -603,11 +715,10 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   KReport r;
   {
     ProfScope pd(rep, nxt, PROF_DEFL);
-    r = fgmres(N.A->n, Aop, &Mop, N.vhat, N.vtil, N.cycle_stop, N.ws_defl);
+    r = fgmres(N.A->n, Aop, &Mop, N.vhat, N.vtil, N.cycle_stop, N.ws_defl, nullptr, nullptr, N.A);
   }
   rep.cycle_iters[nxt].push_back(r.iterations);
-  launch_prolong(N.vtil, nullptr, L.t, L.A->g.nx, L.A->g.ny, 0, E.st);
-  E.launches++;
+  prolong_levels(*N.A, *L.A, N.vtil, nullptr, L.t);
   rep.matvecs[l] += 1;
   L.A->residual(v, L.t, L.rhs);  // v - A t
   cslp_apply(l, L.rhs, L.r);
@@ -633,7 +744,15 @@ void MadpSolver::solve(const cd* b, cd* x) {
   LinOp Aop = [this](const cd* in, cd* o) { A(1, in, o); };
   LinOp Mop = [this](const cd* in, cd* o) { precond(1, in, o); };
   try {
-    rep.outer = fgmres(lv[1].A->n, Aop, &Mop, b, x, outer, lv[1].ws_defl, &hook);
+    const LevelOp* A1 = lv[1].A;
+    const long long n1 = A1->n;
+    if (A1->sharded) {  // stencil inputs need halo rows: solve through halo'd copies
+      HDB_CUDA(cudaMemcpyAsync(lv[1].bh, b, sizeof(cd) * n1, cudaMemcpyDeviceToDevice, E.st));
+      rep.outer = fgmres(n1, Aop, &Mop, lv[1].bh, lv[1].xh, outer, lv[1].ws_defl, &hook, nullptr, A1);
+      HDB_CUDA(cudaMemcpyAsync(x, lv[1].xh, sizeof(cd) * n1, cudaMemcpyDeviceToDevice, E.st));
+    } else {
+      rep.outer = fgmres(n1, Aop, &Mop, b, x, outer, lv[1].ws_defl, &hook);
+    }
     flush_counts();
   } catch (...) {
     cudaEventDestroy(e0);

@@ -1,5 +1,6 @@
 // Host-side engine: device buffers, level operators, Krylov driver (FGMRES with
-// host Givens), CSLP multigrid V-cycle and the recursive A-DEF1 (MADP) solver.
+// host Givens), CSLP multigrid V-cycle and the recursive A-DEF1 (MADP) solver,
+// single GPU or row slabs over several ranks (Comm).
 #pragma once
 #include <complex>
 #include <functional>
@@ -7,6 +8,7 @@
 #include <string>
 #include <vector>
 
+#include "comm.h"
 #include "kernels.h"
 
 namespace hdb {
@@ -29,12 +31,12 @@ using cplx = std::complex<double>;
 
 // device scalar block layout (Engine::dscal)
 constexpr int kScal = 1024;
-constexpr int kSlotFlag = 0;        // .x = 1.0 once an MG divergence guard fired
+constexpr int kSlotFlag = 0;        // .x = 1.0 MG divergence guard fired, 2.0 non-finite (device solve)
 constexpr int kSlotH = 1;           // Hessenberg column h_0.. at kSlotH + i
+constexpr int kSlotMgR0 = 1019;
 constexpr int kSlotMgPost = 1020;
 constexpr int kSlotMgB = 1021;
 constexpr int kSlotMisc = 1022;
-constexpr int kSlotMgR0 = 1019;
 
 struct Engine {
   int device = 0;
@@ -46,21 +48,29 @@ struct Engine {
   size_t bytes_alloc = 0;
   long long launches = 0;  // kernels launched through the engine (telemetry)
   long long syncs = 0;     // host synchronisations (Hessenberg reads etc.)
+  Comm* comm = nullptr;    // row-slab communicator of this rank (owned), null on one rank
 
   explicit Engine(int dev);
   ~Engine();
   cd* alloc(long long n);              // complex vector
   void* alloc_bytes(size_t b);
   void free(void* p);
+  // vector with `halo` elements before and after (slab halo rows); returns the interior pointer
+  cd* alloc_h(long long n, long long halo) { return alloc(n + 2 * halo) + halo; }
+  void free_h(cd* p, long long halo) {
+    if (p) free(p - halo);
+  }
   void sync() { HDB_CUDA(cudaStreamSynchronize(st)); }
-  // read slots [0, count) to host (one copy + sync) and raise on a fired MG guard
+  // read slots [0, count) to host (one copy + sync) and raise on a fired device flag
   void fetch(int count);
   double fetch_norm(int slot);  // sqrt(max(re,0)) of a slot, after fetch
 };
 
-Engine& engine();            // process-wide engine of the selected device
+Engine& engine();            // the calling thread's engine, else the process-wide one
 void engine_init(int device);
 bool engine_ready();
+void thread_engine_begin(int device);  // give the calling thread its own engine (rank threads)
+void thread_engine_end();
 
 struct Stop {
   double rel_tol;
@@ -74,15 +84,22 @@ struct KReport {
   bool converged = false;
 };
 
-// one level operator (A or CSLP M) on device
+// one level operator (A or CSLP M) on device; a slab of rows when sharded
 struct LevelOp {
   OpCoef c;
   Geom g;
-  double* ksq = nullptr;  // device, ny*nx
-  long long n = 0;
+  double* ksq = nullptr;  // device, (ny + 2H) * nx, interior pointer
+  long long n = 0;        // local points
+  int H = 0;              // halo rows allocated around this level's vectors
+  bool sharded = false;
+  std::vector<int> slab_row0, slab_ny;  // every rank's slab (sharded levels)
+  long long halo_elems() const { return (long long)H * g.nx; }
+  void exchange(const cd* u, int rows) const;  // fill `rows` halo rows of u from the neighbours
   void apply(const cd* u, cd* out) const;                 // out = A u
   void residual(const cd* b, const cd* u, cd* out) const;  // out = b - A u
   void jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const;
+  // reductions over this level's distribution (all-reduce when sharded)
+  void reduce(cd* dev_slot) const;
 };
 
 using LinOp = std::function<void(const cd* in, cd* out)>;
@@ -90,14 +107,15 @@ using LinOp = std::function<void(const cd* in, cd* out)>;
 // Krylov workspace: basis vectors grow on demand and are kept across calls
 struct KWS {
   long long n = 0;
+  long long halo = 0;      // halo elements around every basis vector (sharded levels)
   std::vector<cd*> V, Z;
   cd** dV = nullptr;       // device table of V pointers (cooperative MGS)
   int dV_cap = 0, dV_n = 0;
   cd* gpart = nullptr;     // grid-reduction partials
   cd* tmp = nullptr;
-  cd** dbasis = nullptr;  // device pointer table for the solution update
+  cd** dbasis = nullptr;   // device pointer table for the solution update
   cd* dy = nullptr;
-  cd** hbasis = nullptr;  // pinned staging
+  cd** hbasis = nullptr;   // pinned staging
   cd* hy = nullptr;
   int cap = 0;
   void ensure(long long n_, int cap_, bool flexible);
@@ -106,9 +124,11 @@ struct KWS {
   ~KWS();
 };
 
-// right-preconditioned unrestarted FGMRES (krylov.py:61-177); M == nullptr -> GMRES
+// right-preconditioned unrestarted FGMRES (krylov.py:61-177); M == nullptr -> GMRES.
+// `dist` (may be null) distributes the vectors: its reductions all-reduce.
 KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
-               const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr);
+               const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr,
+               const LevelOp* dist = nullptr);
 
 // Krylov solves on levels that fit the resident working set run as ONE
 // device-resident launch (kernels_resident.cu): cluster mode up to
@@ -116,8 +136,8 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
 // HDB_GRID_N points (default 2M) when the stencil windows fit shared memory.
 // 0 disables a mode.
 int resident_mode(long long n, int cap);  // -1: launch-driven path
-int resident_ortho();
-long long coop_mgs_min();  // levels >= this many points use the cooperative MGS step (HDB_COOP_MGS_N)  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
+int resident_ortho();  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
+long long coop_mgs_min();  // levels >= this many points use the cooperative MGS step (HDB_COOP_MGS_N)
 
 struct SmallSolve {  // device-resident GMRES on one level operator
   const LevelOp* op = nullptr;
@@ -132,9 +152,17 @@ struct SmallSolve {  // device-resident GMRES on one level operator
   ~SmallSolve();
 };
 
+// slab-to-slab / slab-to-replicated transfer between two levels
+TGeom level_tgeom(const LevelOp& fine, const LevelOp& coarse);
+// restrict fine (level op f) into coarse buffer `out` of level op c; gathers into
+// the full vector when c is replicated and f sharded (`slab` = local scratch)
+void restrict_levels(const LevelOp& f, const LevelOp& c, const cd* fine, cd* out, cd* slab, int zero_mask);
+// prolong coarse (level op c) into fine (level op f), base != null: fine = base + Z coarse
+void prolong_levels(const LevelOp& c, const LevelOp& f, const cd* coarse, const cd* base, cd* fine);
+
 struct Multigrid {
   std::vector<const LevelOp*> ops;  // sub-levels, finest first
-  std::vector<cd*> X, Y, R, B, O;   // per-level scratch (X,Y,R), rhs (B), output (O)
+  std::vector<cd*> X, Y, R, B, O, S;  // per-level scratch (X,Y,R), rhs (B), output (O), gather slab (S)
   cd* Ainv = nullptr;               // coarsest dense inverse (n <= direct limit)
   int ninv = 0;
   KWS coarse_ws;
@@ -158,8 +186,10 @@ struct MadpLevel {
   Stop cslp_stop{0.1, 1}, cycle_stop{1.0, 1};
   KWS ws_defl, ws_cslp;
   SmallSolve small_cslp;
-  cd *vhat = nullptr, *vtil = nullptr;        // this level's input / output as a deflation system
+  cd *vhat = nullptr, *vtil = nullptr;            // this level's input / output as a deflation system
   cd *t = nullptr, *rhs = nullptr, *r = nullptr;  // A-DEF1 temporaries of P_l
+  cd* slab = nullptr;                             // restriction slab before a gather (replicated level)
+  cd *bh = nullptr, *xh = nullptr;                // level-1 halo'd copies of b and x (sharded solves)
 };
 
 // inclusive host wall time per level and role (telemetry for DESIGN.md / profiles/)

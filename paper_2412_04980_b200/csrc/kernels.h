@@ -16,8 +16,14 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
                   cudaStream_t st);
 void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out, double omega,
                    bool from_zero, cudaStream_t st);
-void launch_restrict(const cd* fine, cd* coarse, int nfx, int nfy, int zero_mask, cudaStream_t st);
-void launch_prolong(const cd* coarse, const cd* base, cd* fine, int nfx, int nfy, int accumulate, cudaStream_t st);
+// transfer geometry: fine rows [f_row0, f_row0+f_ny) of nfy_g, coarse rows [c_row0, c_row0+c_ny) of ncy_g
+struct TGeom {
+  int nfx, f_row0, f_ny, nfy_g;
+  int ncx, c_row0, c_ny, ncy_g;
+};
+TGeom full_tgeom(int nfx, int nfy);
+void launch_restrict(const cd* fine, cd* coarse, const TGeom& t, int zero_mask, cudaStream_t st);
+void launch_prolong(const cd* coarse, const cd* base, cd* fine, const TGeom& t, int accumulate, cudaStream_t st);
 
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st);
 void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st);

@@ -166,11 +166,26 @@ def _model_bytes_per_point(radius):
 class MadpSolver:
     """Outer FGMRES with the recursive multilevel A-DEF1 preconditioner (GPU)."""
 
-    def __init__(self, hierarchy, config: SolverConfig, workers: int = 1):
+    def __init__(self, hierarchy, config: SolverConfig, workers: int = 1, dist=None):
+        """dist: optional distributed.DistContext — row-slab solve over dist.size ranks
+        (each rank passes the full rhs and gets its own slab of the solution)."""
         if config.ml != hierarchy.ml:
             raise ConfigError(f"config has {config.ml} levels but the hierarchy has {hierarchy.ml}")
         self.hierarchy, self.config = hierarchy, config
         self.workers = max(1, int(workers))
+        self.dist = dist
+        self.plan = None
+        spec = lambda depth: None  # noqa: E731
+        if dist is not None and dist.size > 1:
+            from .distributed import slab_plan
+            ny = hierarchy.level(1).ny
+            # every grid depth a level or a multigrid sub-level can reach
+            max_depth = 1
+            while (ny - 1) % 2 ** max_depth == 0 and (ny - 1) // 2 ** max_depth + 1 >= 3:
+                max_depth += 1
+            self.plan = slab_plan(ny, dist.size, max_depth, dist.min_rows)
+            spec = lambda depth: self.plan.spec(depth, dist.rank)  # noqa: E731
+        self._spec = spec
         self.A: dict[int, LevelOperator] = {}
         self.M: dict[int, LevelOperator] = {}
         self.mg: dict[int, CslpMultigrid] = {}
@@ -178,13 +193,14 @@ class MadpSolver:
             pol = config.policy(l)
             if pol.cslp_method == CSLP_BICGSTAB:
                 raise ConfigError("cslp_method='bicgstab' is not implemented by the GPU solver (DESIGN.md §Scope)")
-            self.A[l] = helmholtz_operator(hierarchy, l)
+            self.A[l] = helmholtz_operator(hierarchy, l, slab=spec(l - 1))
             if pol.cslp_method == CSLP_GMRES:
-                self.M[l] = cslp_operator(hierarchy, l, pol.cslp_shift, config.beta1)
+                self.M[l] = cslp_operator(hierarchy, l, pol.cslp_shift, config.beta1, slab=spec(l - 1))
             elif pol.cslp_method == CSLP_MG:
                 lv = hierarchy.level(l)
                 self.mg[l] = CslpMultigrid(lv.nx, lv.ny, lv.h, hierarchy.ksq_at(l), hierarchy.boundary,
-                                           beta2=pol.cslp_shift, beta1=config.beta1, config=config.mg_config)
+                                           beta2=pol.cslp_shift, beta1=config.beta1, config=config.mg_config,
+                                           slabs=(lambda s, l=l: spec(l - 1 + s)))
         self._h = None
 
     # -- device solver -------------------------------------------------------
@@ -258,6 +274,12 @@ class MadpSolver:
             from .errors import ShapeError
             raise ShapeError(f"rhs shape {tuple(b2d.shape)} != {shape}")
         t0 = time.perf_counter()
+        sl = self._spec(0)
+        if sl is not None:  # distributed: this rank's slab in, this rank's slab out (host buffers)
+            hb = np.ascontiguousarray(np.asarray(b2d)[sl.row0:sl.row0 + sl.ny], dtype=np.complex128)
+            hx = np.empty_like(hb)
+            check(lib().hdb_solver_solve(self.handle, hb.ctypes.data, hx.ctypes.data, 1))
+            return hx, self.report(wall_ms=(time.perf_counter() - t0) * 1e3)
         if dev.is_device(b2d):
             db = b2d.to(dev.torch_mod().complex128).contiguous()
             x = dev.empty(shape)

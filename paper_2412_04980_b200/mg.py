@@ -96,14 +96,18 @@ def assemble_radius1_dense(op: LevelOperator, max_points: int = 4096) -> np.ndar
 class CslpMultigrid:
     """V-cycle for ``-Laplace - (beta1 + i beta2) I(k^2)`` on one grid (GPU)."""
 
-    def __init__(self, nx, ny, h, ksq, boundary, beta2, beta1=1.0, config: MgConfig = MgConfig()):
+    def __init__(self, nx, ny, h, ksq, boundary, beta2, beta1=1.0, config: MgConfig = MgConfig(),
+                 slabs=None):
+        """slabs: optional callable sub-level index -> distributed.SlabSpec or None
+        (row-slab decomposition of the sub-hierarchy; None everywhere = one rank)."""
         self.config = config
         shift = complex(beta1, beta2)
         self.levels: list[_SubLevel] = []
         cx, cy, ch = int(nx), int(ny), float(h)
         kk = np.ascontiguousarray(ksq, dtype=np.float64)
         while True:
-            self.levels.append(_SubLevel(op=radius1_operator(cx, cy, ch, kk, boundary, shift)))
+            sl = slabs(len(self.levels)) if slabs is not None else None
+            self.levels.append(_SubLevel(op=radius1_operator(cx, cy, ch, kk, boundary, shift, slab=sl)))
             if not ((cx - 1) % 2 == 0 and (cy - 1) % 2 == 0 and min(cx, cy) > 5
                     and len(self.levels) < config.mg_levels):
                 break

@@ -33,7 +33,7 @@ class LevelOperator:
     """Matrix-free ``-Laplace - shift * I(k^2)`` on one grid level (GPU)."""
 
     def __init__(self, level, nx, ny, h, ksq, boundary, laplace: StencilKernel, mass: StencilKernel,
-                 shift=1.0, level_scale=1.0):
+                 shift=1.0, level_scale=1.0, slab=None):
         if laplace.radius != mass.radius:
             raise ShapeError("laplace and mass kernels must share a radius")
         self.level = level
@@ -48,6 +48,7 @@ class LevelOperator:
         # float conversion, once (operators.py:111-113)
         self.lap_coef = laplace.as_float() / self.h ** 2
         self.mass_coef = (-self.shift / level_scale) * mass.as_float().astype(np.complex128)
+        self.slab = slab  # distributed.SlabSpec of this rank, None = whole grid
         self._handle = None
 
     # -- device handle ------------------------------------------------------
@@ -61,8 +62,16 @@ class LevelOperator:
             mre = np.ascontiguousarray(self.mass_coef.real)
             mim = np.ascontiguousarray(self.mass_coef.imag)
             f = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
-            check(L.hdb_op_create(C.byref(h), self.nx, self.ny, self.radius, self.h, bc, f(lap), f(mre), f(mim),
-                                  f(self.ksq)))
+            if self.slab is None:
+                check(L.hdb_op_create(C.byref(h), self.nx, self.ny, self.radius, self.h, bc, f(lap), f(mre), f(mim),
+                                      f(self.ksq)))
+            else:
+                sl = self.slab
+                P = len(sl.table_row0)
+                r0s = (C.c_int * P)(*sl.table_row0)
+                nys = (C.c_int * P)(*sl.table_ny)
+                check(L.hdb_op_create_slab(C.byref(h), self.nx, self.ny, self.radius, self.h, bc, f(lap), f(mre),
+                                           f(mim), f(self.ksq), sl.row0, sl.ny, sl.halo, P, r0s, nys))
             self._handle = h
         return self._handle
 
@@ -185,24 +194,24 @@ class LevelOperator:
         return A
 
 
-def _level_operator(hierarchy, level, shift):
+def _level_operator(hierarchy, level, shift, slab=None):
     lv = hierarchy.level(level)
     lap, mass = level_kernels(level)
     return LevelOperator(level, lv.nx, lv.ny, lv.h, hierarchy.ksq_at(level), hierarchy.boundary, lap, mass,
-                         shift=shift, level_scale=mass_level_scale(level))
+                         shift=shift, level_scale=mass_level_scale(level), slab=slab)
 
 
-def helmholtz_operator(hierarchy, level: int) -> LevelOperator:
-    return _level_operator(hierarchy, level, 1.0)
+def helmholtz_operator(hierarchy, level: int, slab=None) -> LevelOperator:
+    return _level_operator(hierarchy, level, 1.0, slab)
 
 
-def cslp_operator(hierarchy, level: int, beta2: float, beta1: float = 1.0) -> LevelOperator:
-    return _level_operator(hierarchy, level, complex(beta1, beta2))
+def cslp_operator(hierarchy, level: int, beta2: float, beta1: float = 1.0, slab=None) -> LevelOperator:
+    return _level_operator(hierarchy, level, complex(beta1, beta2), slab)
 
 
-def radius1_operator(nx, ny, h, ksq, boundary, shift) -> LevelOperator:
+def radius1_operator(nx, ny, h, ksq, boundary, shift, slab=None) -> LevelOperator:
     lap, mass = level_kernels(1)
-    return LevelOperator(0, nx, ny, h, ksq, boundary, lap, mass, shift=shift, level_scale=1.0)
+    return LevelOperator(0, nx, ny, h, ksq, boundary, lap, mass, shift=shift, level_scale=1.0, slab=slab)
 
 
 def apply_helmholtz(op: LevelOperator, hierarchy, u: ComplexField) -> ComplexField:

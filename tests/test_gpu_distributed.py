@@ -1,0 +1,84 @@
+"""Row-slab (multi-rank) solve on one GPU: ranks are host threads with their own
+engine and stream, exchanging halos / all-reducing dots through the in-process
+transport (the NCCL transport only swaps the byte movement).  Every rank's slab
+of the solution must equal the single-rank solve to rounding, with the same
+iteration counts."""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+hdb = pytest.importorskip("paper_2412_04980_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _solve_ranks(build, P, min_rows):
+    from paper_2412_04980_b200.distributed import DistContext
+    group = DistContext.new_group()
+    out = [None] * P
+    errs = []
+
+    def worker(r):
+        try:
+            ctx = DistContext.threads(r, P, group)
+            ctx.min_rows = min_rows
+            prob = build()
+            s = hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy), dist=ctx)
+            x, rep = s.solve(prob.rhs)
+            sl = s._spec(0)
+            out[r] = (sl.row0 if sl else 0, np.array(x), rep, s.plan.depths)
+            s.close()
+            ctx.close()
+        except BaseException as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(r,)) for r in range(P)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("P,min_rows", [(2, 16), (4, 8)])
+def test_slab_solve_matches_single_rank(P, min_rows):
+    build = lambda: hdb.mp1_problem(k=50.0, n=129, ml=3, boundary="sommerfeld")  # noqa: E731
+    prob = build()
+    with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
+        u, ref = s.solve(prob.rhs)
+    xref = u.grid_view(prob.hierarchy)
+    res = _solve_ranks(build, P, min_rows)
+    assert res[0][3] >= 2, "expected at least two sharded grid depths"
+    x = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])], axis=0)
+    assert x.shape == xref.shape
+    for _, _, rep, _ in res:
+        assert rep.outer_iterations == ref.outer_iterations
+        assert rep.cycle_iters == ref.cycle_iters
+        assert np.abs(np.array(rep.residual_history) - np.array(ref.residual_history)).max() <= 1e-10
+    assert np.linalg.norm(x - xref) <= 1e-9 * np.linalg.norm(xref)
+
+
+def test_slab_solve_heterogeneous_dirichlet_mix():
+    def build():
+        vel = hdb.VelocityModel(kind="wedge", layers=[(-400.0, -200.0, 2000.0), (-800.0, -600.0, 1500.0),
+                                                      (0.0, 0.0, 3000.0)])
+        hier = hdb.build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=600.0 / 144, ml=4, velocity=vel, f=20.0,
+                                   boundary=("sommerfeld", "sommerfeld", "dirichlet", "sommerfeld"))
+        return hdb.grid.Problem("wedge-mixed", hier, hdb.point_source_rhs(hier, (300.0, -300.0)))
+    prob = build()
+    with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
+        u, ref = s.solve(prob.rhs)
+    xref = u.grid_view(prob.hierarchy)
+    res = _solve_ranks(build, 2, 16)
+    x = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])], axis=0)
+    assert all(r[2].outer_iterations == ref.outer_iterations for r in res)
+    assert np.linalg.norm(x - xref) <= 1e-9 * np.linalg.norm(xref)
