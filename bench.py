@@ -20,8 +20,10 @@ Printed JSON (rank 0, one line):
                  with it) on a bounded sample of the same workload, scaled
   gpu_launches   kernels launched by libhdb200 inside the timed region
 Fine-level vectors are 268 MB (> 126 MB L2), so no explicit L2 flush is needed.
-N > 1: every rank solves its own copy (replicas; slab sharding is the next step,
-DESIGN.md §Multi-GPU) and the max device time over ranks is reported.
+N > 1 (torchrun): the same problem in row slabs over the ranks (NCCL halo
+exchange and dot all-reduce, coarse levels replicated; strong scaling), max
+device time over ranks.  --config c5 is the weak-scaling sweep (8192^2 points
+per GPU, k^3 h^2 = 0.5).
 """
 from __future__ import annotations
 
@@ -50,7 +52,17 @@ CONFIGS = {
             lambda hdb: hdb.mp1_problem(k=50.0, n=129, ml=2, boundary="sommerfeld")),
     "c3_40": ("BASELINE configs[2] @40 Hz: wedge 600x1000 m, h=0.5 m, 1201x2001, ml=5, MADP",
               lambda hdb: hdb.wedge_problem(f=40.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS)),
+    "c5": ("BASELINE configs[4] weak scaling: 8193 x (8192 P + 1) per P GPUs, h=1/8192, k^3 h^2 = 0.5, ml=7",
+           lambda hdb, P=1: c5_problem(hdb, P)),
 }
+
+
+def c5_problem(hdb, P):
+    """[0,1] x [0,P], h = 1/8192, k = (0.5 / h^2)^(1/3), Sommerfeld, centre source."""
+    h = 1.0 / 8192
+    k = (0.5 / h ** 2) ** (1.0 / 3.0)
+    hier = hdb.build_hierarchy(((0.0, 1.0), (0.0, float(P))), h=h, ml=7, k=k, boundary="sommerfeld")
+    return hdb.grid.Problem("c5", hier, hdb.point_source_rhs(hier, (0.5, P / 2.0)))
 
 
 def _peaks():
@@ -237,7 +249,7 @@ def run_reference(args):
     val = float(np.mean(steps))
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": val * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "scaling": "weak" if (args.config == "c5" or ws == 1) else "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
             "config": {"workload": CONFIGS[args.config][0]},
             "cpu_baseline": {"value": val, "unit": "s", "cores": 1, "kind": "port", "sample": cb["sample"]},
             "e2e": {"value": val, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -271,12 +283,19 @@ def main():
     from paper_2412_04980_b200 import _lib
     L = _lib.lib()
 
-    prob = CONFIGS[args.config][1](hdb)
+    prob = CONFIGS[args.config][1](hdb, ws) if args.config == "c5" else CONFIGS[args.config][1](hdb)
     hier = prob.hierarchy
     cfg = hdb.preset("MADP", hier)
-    solver = hdb.MadpSolver(hier, cfg)
-    shape = hier.level(1).shape
+    dist_ctx = None
+    if ws > 1:  # row slabs over the ranks: NCCL halos / dots, replicated coarse levels
+        from paper_2412_04980_b200.distributed import DistContext
+        dist_ctx = DistContext.nccl(rank, ws)
+    solver = hdb.MadpSolver(hier, cfg, dist=dist_ctx)
     b_host = prob.rhs.grid_view(hier)
+    sl = solver._spec(0)
+    if sl is not None:
+        b_host = np.ascontiguousarray(b_host[sl.row0:sl.row0 + sl.ny])
+    shape = b_host.shape
     b_dev = torch.from_numpy(b_host.copy()).cuda()
     x_dev = torch.empty_like(b_dev)
     # pinned host buffers for the end-to-end leg
@@ -304,16 +323,19 @@ def main():
 
     # end-to-end through the public API (numpy in pinned memory -> numpy out)
     e2e = []
+    b_api = prob.rhs.grid_view(hier) if sl is not None else b_pin_np  # distributed API takes the full rhs
     for k in range(max(1, args.steps)):
         torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
         t0 = time.perf_counter()
-        u, rep_e = solver.solve(b_pin_np)
+        u, rep_e = solver.solve(b_api)
         e2e.append(time.perf_counter() - t0)
     e2e_t = _allmax(float(np.mean(e2e)), ws)
 
-    kern = kernel_roofline(hdb, hier) if rank == 0 else {}
+    kern = kernel_roofline(hdb, hier) if (rank == 0 and args.config != "c5") else {}
     peak, peak_src = _peaks()
-    dom = kern.get("stencil5_apply")
+    dom = kern.get("stencil5_apply") or {"gbs": float("nan"), "bytes": 0, "ms": float("nan")}
     out_line = None
     if rank == 0:
         cpu = None
@@ -325,16 +347,19 @@ def main():
         out_line = {
             "metric": METRIC, "value": t_step, "unit": "s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-            "config": {"workload": CONFIGS[args.config][0], "grid": f"{shape[1]}x{shape[0]}",
-                       "levels": hier.ml, "parallelism": "replicas" if ws > 1 else "single",
+            "scaling": "weak" if (args.config == "c5" or ws == 1) else "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+            "config": {"workload": CONFIGS[args.config][0],
+                       "grid": f"{hier.level(1).nx}x{hier.level(1).ny}",
+                       "levels": hier.ml,
+                       "parallelism": (f"row slabs x{ws} ({solver.plan.depths} sharded grid depths, "
+                                       f"coarser replicated)") if ws > 1 else "single",
                        "l2_flush": "inputs larger than L2 (268 MB per fine-level vector)"},
             "outer_iters": rep.outer_iterations, "converged": rep.converged,
             "final_relres": rep.final_relres,
             "cycle_iters_max": {str(l): rep.cycle_max(l) for l in range(2, hier.ml + 1)},
             "cslp_iters_max": {str(l): rep.cslp_max(l) for l in range(1, hier.ml + 1)},
-            "e2e": {"value": e2e_t, "unit": "s", "h2d_bytes_per_step": int(b_host.nbytes),
-                    "d2h_bytes_per_step": int(b_host.nbytes)},
+            "e2e": {"value": e2e_t, "unit": "s", "h2d_bytes_per_step": int(b_host.nbytes) * ws,
+                    "d2h_bytes_per_step": int(b_host.nbytes) * ws},
             "roofline": {"bound": "hbm", "kernel": "stencil5_apply (K1, fine level)",
                          "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
                          "traffic": None, "peak_source": peak_src,
@@ -348,6 +373,8 @@ def main():
         }
         print(json.dumps(out_line), flush=True)
     solver.close()
+    if dist_ctx is not None:
+        dist_ctx.close()
     if ws > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()

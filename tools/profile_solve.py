@@ -9,6 +9,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import paper_2412_04980_b200 as hdb  # noqa: E402
 
@@ -21,6 +22,7 @@ CASES = {
     "c3_10": lambda: hdb.wedge_problem(f=10.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS),
     "c3_20": lambda: hdb.wedge_problem(f=20.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS),
     "c3_40": lambda: hdb.wedge_problem(f=40.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS),
+    "c5": lambda: __import__("bench").c5_problem(hdb, 1),
 }
 
 
