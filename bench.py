@@ -205,10 +205,35 @@ def kernel_roofline(hdb, hier, reps=20):
     return {k: {"bytes": bts, "ms": tt * 1e3, "gbs": bts / tt / 1e9} for k, (bts, tt) in res.items()}
 
 
-def cpu_baseline(config, outer_its, max_outer=1):
+def _work_units(cycle_iters_l2, n_outer):
+    """Cost model of one MADP outer iteration: 1 + its level-2 deflation cycles
+    (every level-2 FGMRES iteration runs the whole coarse recursion once)."""
+    c = list(cycle_iters_l2)[:n_outer] + [0] * max(0, n_outer - len(cycle_iters_l2))
+    return [1 + x for x in c]
+
+
+def reference_counts(config):
+    """Outer iterations and level-2 cycle counts of the REFERENCE's own run of this
+    config (committed fixtures; the oracle reproduces the reference bit for bit)."""
+    name = {"c2": "solve_c2.npz", "c2a": "solve_c2a.npz", "c1s": "solve_c1s.npz"}.get(config)
+    if name is None:
+        return None
+    path = os.path.join(ROOT, "tests", "golden", name)
+    if not os.path.exists(path):
+        return None
+    import ast
+    g = np.load(path, allow_pickle=False)
+    txt = str(g["cycle_iters"])
+    cyc = json.loads(txt) if txt.startswith("{\"") else ast.literal_eval(txt)
+    cyc = {int(k): v for k, v in cyc.items()}
+    return int(g["outer_iterations"]), cyc.get(2, [])
+
+
+def cpu_baseline(config, outer_its, cycle_l2=None, max_outer=1):
     """Oracle (bit-exact restatement of the reference) on a bounded sample: the
-    first `max_outer` outer iteration(s) of the same solve, scaled linearly to
-    the GPU's outer-iteration count."""
+    first `max_outer` outer iteration(s) of the same solve, scaled to the whole
+    solve by the work model 1 + (level-2 cycles) per outer iteration, with the
+    counts of the reference's own run where committed (else the GPU's)."""
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_oracle")
     import oracle
     if config == "c2":
@@ -228,11 +253,21 @@ def cpu_baseline(config, outer_its, max_outer=1):
     t0 = time.perf_counter()
     _, rep = s.solve(b, max_outer=max_outer)
     dt = time.perf_counter() - t0
-    per_it = dt / max(1, rep.iterations)
-    return {"value": per_it * outer_its, "unit": "s", "cores": 1, "kind": "port",
+    ref = reference_counts(config)
+    src = "reference run"
+    if ref is not None:
+        outer_its, cycle_l2 = ref
+    else:
+        src = "GPU run"
+        cycle_l2 = cycle_l2 or []
+    w = _work_units(cycle_l2, outer_its)
+    sampled = sum(_work_units(s.cycle_iters.get(2, []), rep.iterations))
+    scale = sum(w) / max(1, sampled)
+    return {"value": dt * scale, "unit": "s", "cores": 1, "kind": "port",
             "sample": f"oracle (bit-exact CPU restatement of helmdef, numba loops, 1 thread) on the first "
-                      f"{rep.iterations} outer iteration(s) of the same solve: {dt:.2f} s, scaled x{outer_its} "
-                      f"outer iterations"}
+                      f"{rep.iterations} outer iteration(s) of the same solve: {dt:.2f} s for {sampled} work units; "
+                      f"scaled x{scale:.1f} to the {outer_its}-iteration solve ({sum(w)} units = outer iterations + "
+                      f"level-2 cycles, counts of the {src})"}
 
 
 def run_reference(args):
@@ -341,7 +376,7 @@ def main():
         cpu = None
         if not args.no_cpu and ws == 1:
             try:
-                cpu = cpu_baseline(args.config, rep.outer_iterations)
+                cpu = cpu_baseline(args.config, rep.outer_iterations, rep.cycle_iters.get(2, []))
             except Exception as err:  # noqa: BLE001
                 cpu = {"value": None, "unit": "s", "cores": 1, "kind": "port", "sample": f"failed: {err}"}
         out_line = {
@@ -389,7 +424,7 @@ def C_launches(L):
 
 # outer-iteration counts used to scale the reference arm's bounded sample
 # (GPU solve counts, equal to the oracle's where the oracle was run to the end)
-REF_OUTER_ITS = {"c2": 20, "c2a": 17, "c1s": 12, "c3_40": 19}
+REF_OUTER_ITS = {"c2": 29, "c2a": 17, "c1s": 12, "c3_40": 19}
 
 if __name__ == "__main__":
     main()
