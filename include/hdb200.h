@@ -15,7 +15,8 @@
  *   - pointers are DEVICE pointers unless the argument name ends in _host.
  *   - every function returns a status: 0 ok, 1 bad argument (ShapeError /
  *     LevelError / ConfigError), 2 CUDA failure (HelmdefError), 3 non-finite
- *     value (NumericalError), 4 multigrid divergence (MgDivergence);
+ *     value (NumericalError), 4 multigrid divergence (MgDivergence), 5 Bi-CGSTAB
+ *     breakdown (BreakdownError; x holds the best iterate);
  *     hdb_last_error() returns the message of the last failure (thread-local).
  *   - all work is ordered on one library stream per process (hdb_stream);
  *     functions that return host scalars synchronise it.
@@ -32,6 +33,7 @@ extern "C" {
 #define HDB_E_CUDA 2
 #define HDB_E_NONFINITE 3
 #define HDB_E_MGDIV 4
+#define HDB_E_BREAKDOWN 5
 
 typedef struct hdb_op hdb_op;        /* one level operator  -Lap - shift*I(k^2)   */
 typedef struct hdb_mg hdb_mg;        /* CSLP multigrid (mg.py:51)                  */
@@ -110,6 +112,13 @@ int hdb_fgmres(long long n, hdb_linop_fn A, void* A_user, hdb_linop_fn M, void* 
                int* iterations, double* final_relres, int* converged,
                double* history_host, int history_cap);
 
+/* Bi-CGSTAB (krylov.py:185-276); HDB_E_BREAKDOWN leaves the best iterate in x
+ * and its counts in the outputs                                              */
+int hdb_bicgstab(long long n, hdb_linop_fn A, void* A_user, hdb_linop_fn M, void* M_user,
+                 const void* b, const void* x0, void* x, double rel_tol, int max_iters,
+                 int* iterations, double* final_relres, int* converged,
+                 double* history_host, int history_cap, int* history_len);
+
 /* GMRES on one level operator, no preconditioner (the CSLP solve of
  * madp.py:290-291): mode -1 launch-driven engine, 0 device-resident on one
  * thread-block cluster, 1 device-resident cooperative grid, 2 automatic      */
@@ -122,7 +131,7 @@ int hdb_resident_profile(int enable, long long* host_out8);
 
 /* ---- MADP solver: replaces MadpSolver (madp.py:220-371) ------------------- */
 int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max);
-/* cslp: 0 none, 1 mg, 2 gmres (madp.py:55-58); level 1 ignores the cycle rule */
+/* cslp: 0 none, 1 mg, 2 gmres, 3 bicgstab (madp.py:55-58); level 1 ignores the cycle rule */
 int hdb_solver_set_level(hdb_solver* s, int level, hdb_op* A, hdb_op* M, hdb_mg* mg, int cslp,
                          double cslp_tol, int cslp_max, double cycle_tol, int cycle_max);
 /* MadpSolver.solve (madp.py:329-371); host_buffers != 0: b, x are host pointers

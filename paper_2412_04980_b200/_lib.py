@@ -51,6 +51,8 @@ SIGNATURES = {
     "hdb_fgmres": [i64, LINOP_FN, vp, LINOP_FN, vp, vp, vp, vp, f64, i32, ITER_FN, vp,
                    P(i32), P(f64), P(i32), P(f64), i32],
     "hdb_op_gmres": [vp, vp, vp, f64, i32, i32, P(i32), P(f64)],
+    "hdb_bicgstab": [i64, LINOP_FN, vp, LINOP_FN, vp, vp, vp, vp, f64, i32, P(i32), P(f64), P(i32), P(f64), i32,
+                     P(i32)],
     "hdb_resident_profile": [i32, P(i64)],
     "hdb_solver_create": [P(vp), i32, f64, i32],
     "hdb_solver_set_level": [vp, i32, vp, vp, vp, i32, f64, i32, f64, i32],
@@ -117,6 +119,7 @@ def lib():
 
 
 _STATUS = {1: ShapeError, 2: DeviceError, 3: NumericalError, 4: MgDivergence}
+# 5 (Bi-CGSTAB breakdown) is raised by krylov.bicgstab itself (it carries the iterate)
 
 
 def check_raw(L, status: int):

@@ -331,6 +331,32 @@ int hdb_resident_profile(int enable, long long* host_out8) {
   });
 }
 
+int hdb_bicgstab(long long n, hdb_linop_fn A, void* Au, hdb_linop_fn M, void* Mu, const void* b, const void* x0,
+                 void* x, double rel_tol, int max_iters, int* iterations, double* final_relres, int* converged,
+                 double* hist, int hist_cap, int* hist_len) {
+  return guarded([&] {
+    if (max_iters < 1) throw Error(E_ARG, "max_iters must be >= 1");
+    LinOp Aop = [A, Au](const cd* in, cd* out) {
+      if (A(Au, in, out) != 0) throw Error(E_ARG, "operator callback failed");
+    };
+    LinOp Mop = [M, Mu](const cd* in, cd* out) {
+      if (M(Mu, in, out) != 0) throw Error(E_ARG, "preconditioner callback failed");
+    };
+    BWS ws;
+    bool brk = false;
+    std::string why;
+    KReport r = bicgstab(n, Aop, M ? &Mop : nullptr, (const cd*)b, (cd*)x, Stop{rel_tol, max_iters}, ws,
+                         (const cd*)x0, nullptr, &brk, &why);
+    engine().sync();
+    *iterations = r.iterations;
+    *final_relres = r.final_relres;
+    *converged = r.converged ? 1 : 0;
+    *hist_len = (int)r.history.size();
+    for (int i = 0; i < hist_cap && i < (int)r.history.size(); ++i) hist[i] = r.history[i];
+    if (brk) throw Error(E_BREAKDOWN, why);
+  });
+}
+
 int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max) {
   return guarded([&] {
     if (ml < 2) throw Error(E_ARG, "hierarchy needs at least two levels");
@@ -350,7 +376,7 @@ int hdb_solver_set_level(hdb_solver* s, int level, hdb_op* A, hdb_op* M, hdb_mg*
     L.mg = mg ? &mg->mg : nullptr;
     L.cslp = cslp;
     if (cslp == CSLP_MG && !mg) throw Error(E_ARG, "cslp=mg needs a multigrid");
-    if (cslp == CSLP_GMRES && !M) throw Error(E_ARG, "cslp=gmres needs a CSLP operator");
+    if ((cslp == CSLP_GMRES || cslp == CSLP_BICGSTAB) && !M) throw Error(E_ARG, "cslp=gmres/bicgstab needs a CSLP operator");
     L.cslp_stop = Stop{cslp_tol, cslp_max};
     L.cycle_stop = Stop{cycle_tol, cycle_max};
   });

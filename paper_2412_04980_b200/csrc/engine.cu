@@ -468,6 +468,122 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   return rep;
 }
 
+// --------------------------------------------------------------- Bi-CGSTAB
+void BWS::ensure(long long n_) {
+  if (n == n_ && r) return;
+  Engine& E = engine();
+  if (r) throw Error(E_ARG, "Bi-CGSTAB workspace reused with a different vector length");
+  n = n_;
+  for (cd** q : {&r, &rhat, &p, &v, &s, &t, &ph, &sh, &tmp}) *q = E.alloc_h(n, halo);
+}
+BWS::~BWS() {
+  if (!engine_ready() || !r) return;
+  Engine& E = engine();
+  for (cd* q : {r, rhat, p, v, s, t, ph, sh, tmp}) E.free_h(q, halo);
+}
+
+KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, BWS& ws,
+                 const cd* x0, const LevelOp* dist, bool* breakdown, std::string* why) {
+  Engine& E = engine();
+  ws.ensure(n);
+  *breakdown = false;
+  const bool shard = dist && dist->sharded;
+  auto dotv = [&](const cd* u, const cd* w) {  // conj-dot to the host (one sync)
+    launch_dot(u, w, n, E.red, E.dscal + kSlotH, E.st);
+    E.launches++;
+    if (shard) dist->reduce(E.dscal + kSlotH);
+    E.fetch(kSlotH + 1);
+    return cplx(E.hscal[kSlotH].x, E.hscal[kSlotH].y);
+  };
+  auto nrm = [&](const cd* u) { return std::sqrt(std::max(dotv(u, u).real(), 0.0)); };
+  const size_t bytes = sizeof(cd) * n;
+  KReport rep;
+  const double bnorm = nrm(b);
+  if (x0) {
+    HDB_CUDA(cudaMemcpyAsync(x, x0, bytes, cudaMemcpyDeviceToDevice, E.st));
+    A(x0, ws.tmp);
+    launch_add(b, ws.tmp, ws.r, n, 1, E.st);
+  } else {
+    HDB_CUDA(cudaMemsetAsync(x, 0, bytes, E.st));
+    HDB_CUDA(cudaMemcpyAsync(ws.r, b, bytes, cudaMemcpyDeviceToDevice, E.st));
+  }
+  if (bnorm == 0.0) {  // krylov.py:203-204
+    rep.history = {0.0};
+    rep.converged = true;
+    return rep;
+  }
+  double rel = nrm(ws.r) / bnorm;
+  rep.history.push_back(rel);
+  if (rel <= stop.rel_tol && stop.rel_tol < 1.0) {
+    rep.final_relres = rel;
+    rep.converged = true;
+    return rep;
+  }
+  HDB_CUDA(cudaMemcpyAsync(ws.rhat, ws.r, bytes, cudaMemcpyDeviceToDevice, E.st));
+  HDB_CUDA(cudaMemsetAsync(ws.v, 0, bytes, E.st));
+  HDB_CUDA(cudaMemsetAsync(ws.p, 0, bytes, E.st));
+  cplx rho(1.0, 0.0), alpha(1.0, 0.0), omega(1.0, 0.0);
+  const double eps = 1e-30;  // krylov.py:28
+  int its = 0;
+  bool conv = false;
+  auto brk = [&](const char* m) {
+    *breakdown = true;
+    *why = m;
+    rep.iterations = its;
+    rep.final_relres = rep.history.back();
+    rep.converged = false;
+  };
+  for (int it = 1; it <= stop.max_iters; ++it) {
+    const cplx rho_new = dotv(ws.rhat, ws.r);
+    if (std::abs(rho_new) < eps * bnorm * bnorm) { brk("rho vanished in Bi-CGSTAB"); return rep; }
+    const cplx beta = (rho_new / rho) * (alpha / omega);
+    launch_bicg_p(ws.r, ws.p, ws.v, mkc(beta.real(), beta.imag()), mkc(omega.real(), omega.imag()), n, E.st);
+    const cd* phat = ws.p;
+    if (M) { (*M)(ws.p, ws.ph); phat = ws.ph; }
+    A(phat, ws.v);
+    const cplx denom = dotv(ws.rhat, ws.v);
+    if (std::abs(denom) < eps * bnorm * bnorm) { brk("alpha denominator vanished in Bi-CGSTAB"); return rep; }
+    alpha = rho_new / denom;
+    launch_axpy(ws.r, mkc(alpha.real(), alpha.imag()), ws.v, ws.s, n, 1, E.st);  // s = r - alpha v
+    launch_axpy(x, mkc(alpha.real(), alpha.imag()), phat, x, n, 0, E.st);        // x = x + alpha phat
+    E.launches += 3;
+    its = it;
+    const double srel = nrm(ws.s) / bnorm;
+    if (srel <= stop.rel_tol) {
+      rep.history.push_back(srel);
+      conv = true;
+      break;
+    }
+    const cd* shat = ws.s;
+    if (M) { (*M)(ws.s, ws.sh); shat = ws.sh; }
+    A(shat, ws.t);
+    const cplx tt = dotv(ws.t, ws.t);
+    if (std::abs(tt) < eps) { brk("omega denominator vanished in Bi-CGSTAB"); return rep; }
+    omega = dotv(ws.t, ws.s) / tt;
+    if (std::abs(omega) < eps) { brk("omega vanished in Bi-CGSTAB"); return rep; }
+    launch_axpy(x, mkc(omega.real(), omega.imag()), shat, x, n, 0, E.st);     // x = x + omega shat
+    launch_axpy(ws.s, mkc(omega.real(), omega.imag()), ws.t, ws.r, n, 1, E.st);  // r = s - omega t
+    E.launches += 2;
+    rel = nrm(ws.r) / bnorm;
+    rep.history.push_back(rel);
+    if (!std::isfinite(rel)) throw Error(E_NONFINITE, "non-finite residual in Bi-CGSTAB");
+    if (rel <= stop.rel_tol) {
+      conv = true;
+      break;
+    }
+    rho = rho_new;
+  }
+  A(x, ws.tmp);  // final true residual (krylov.py:275)
+  launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
+  E.launches++;
+  if (shard) dist->reduce(E.dscal + kSlotH);
+  E.fetch(kSlotH + 1);
+  rep.iterations = its;
+  rep.final_relres = E.fetch_norm(kSlotH) / bnorm;
+  rep.converged = conv;
+  return rep;
+}
+
 // -------------------------------------------------------------- multigrid
 static int dirichlet_mask(const OpCoef& c) {
   int m = 0;
@@ -672,6 +788,15 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     return;
   }
   const LevelOp* M = L.M;
+  if (L.cslp == CSLP_BICGSTAB) {  // madp.py:292-297: a breakdown still yields a usable iterate
+    LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
+    L.ws_bicg.halo = M->halo_elems();
+    bool brk = false;
+    std::string why;
+    KReport r = bicgstab(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_bicg, nullptr, M, &brk, &why);
+    rep.cslp_iters[l].push_back(r.iterations);
+    return;
+  }
   if (!M->sharded && resident_mode(M->n, L.cslp_stop.max_iters) >= 0) {
     if (dused >= dcap) flush_counts();
     L.small_cslp.ensure(M, L.cslp_stop.max_iters);

@@ -130,6 +130,18 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
                const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr,
                const LevelOp* dist = nullptr);
 
+// Bi-CGSTAB workspace and solver (krylov.py:185-276); on breakdown *breakdown is
+// set and x holds the best iterate (the caller decides, as madp.py:293-297 does)
+struct BWS {
+  long long n = 0, halo = 0;
+  cd *r = nullptr, *rhat = nullptr, *p = nullptr, *v = nullptr, *s = nullptr, *t = nullptr, *ph = nullptr,
+     *sh = nullptr, *tmp = nullptr;
+  void ensure(long long n_);
+  ~BWS();
+};
+KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, BWS& ws,
+                 const cd* x0, const LevelOp* dist, bool* breakdown, std::string* why);
+
 // Krylov solves on levels that fit the resident working set run as ONE
 // device-resident launch (kernels_resident.cu): cluster mode up to
 // HDB_SMALL_N points (default 12k), whole-grid cooperative mode up to
@@ -176,7 +188,7 @@ struct Multigrid {
   ~Multigrid();
 };
 
-enum { CSLP_NONE = 0, CSLP_MG = 1, CSLP_GMRES = 2 };
+enum { CSLP_NONE = 0, CSLP_MG = 1, CSLP_GMRES = 2, CSLP_BICGSTAB = 3 };
 
 struct MadpLevel {
   const LevelOp* A = nullptr;
@@ -185,6 +197,7 @@ struct MadpLevel {
   int cslp = CSLP_NONE;
   Stop cslp_stop{0.1, 1}, cycle_stop{1.0, 1};
   KWS ws_defl, ws_cslp;
+  BWS ws_bicg;
   SmallSolve small_cslp;
   cd *vhat = nullptr, *vtil = nullptr;            // this level's input / output as a deflation system
   cd *t = nullptr, *rhs = nullptr, *r = nullptr;  // A-DEF1 temporaries of P_l

@@ -32,6 +32,8 @@ void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st
 void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd* x, long long n, cudaStream_t st);
 void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st);
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st);
+void launch_axpy(const cd* y, cd a, const cd* x, cd* out, long long n, int sub, cudaStream_t st);
+void launch_bicg_p(const cd* r, cd* p, const cd* v, cd beta, cd omega, long long n, cudaStream_t st);
 void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st);
 
 // device-resident GMRES (kernels_resident.cu).  mode 0: one cluster, 1: whole grid

@@ -136,6 +136,22 @@ __global__ void k_add(const cd* __restrict__ a, const cd* __restrict__ b, cd* __
     out[p] = sub ? c_sub(a[p], b[p]) : c_add(a[p], b[p]);
 }
 
+// out = y + a x  (sub = 0)  /  out = y - a x  (sub = 1); numpy scalar*array then add/sub
+__global__ void k_axpy(const cd* __restrict__ y, cd a, const cd* __restrict__ x, cd* __restrict__ out, long long n,
+                       int sub) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const cd t = c_mul_np(a, x[p]);
+    out[p] = sub ? c_sub(y[p], t) : c_add(y[p], t);
+  }
+}
+
+// Bi-CGSTAB direction (krylov.py:218): p = r + beta * (p - omega * v)
+__global__ void k_bicg_p(const cd* __restrict__ r, cd* __restrict__ pv, const cd* __restrict__ v, cd beta, cd omega,
+                         long long n) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x)
+    pv[p] = c_add(r[p], c_mul_np(beta, c_sub(pv[p], c_mul_np(omega, v[p]))));
+}
+
 // small dense complex GEMV  x = Ainv b  (MG coarsest solve, n <= 4096)
 __global__ void __launch_bounds__(256) k_gemv(const cd* __restrict__ A, const cd* __restrict__ b, cd* __restrict__ x,
                                               int n) {
@@ -182,6 +198,12 @@ void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd
 }
 void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st) {
   k_add<<<ew_blocks(n), 256, 0, st>>>(a, b, out, n, sub);
+}
+void launch_axpy(const cd* y, cd a, const cd* x, cd* out, long long n, int sub, cudaStream_t st) {
+  k_axpy<<<ew_blocks(n), 256, 0, st>>>(y, a, x, out, n, sub);
+}
+void launch_bicg_p(const cd* r, cd* p, const cd* v, cd beta, cd omega, long long n, cudaStream_t st) {
+  k_bicg_p<<<ew_blocks(n), 256, 0, st>>>(r, p, v, beta, omega, n);
 }
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st) {
   k_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(A, b, x, n);

@@ -26,7 +26,7 @@ import numpy as np
 from . import device as dev
 from ._lib import ITER_FN, LINOP_FN, check, lib
 
-__all__ = ["StopRule", "KrylovReport", "fgmres", "gmres", "cslp_iteration_cap", "device_callable"]
+__all__ = ["StopRule", "KrylovReport", "fgmres", "gmres", "bicgstab", "cslp_iteration_cap", "device_callable"]
 
 
 @dataclass(frozen=True)
@@ -136,3 +136,31 @@ def fgmres(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None, on_iteration=
 def gmres(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None, on_iteration=None):
     """GMRES with a fixed right preconditioner (same engine as fgmres)."""
     return fgmres(apply_A, apply_M, b, stop, x0=x0, dot=dot, on_iteration=on_iteration)
+
+
+def bicgstab(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None):
+    """Right-preconditioned Bi-CGSTAB (krylov.py:185-276).  Raises BreakdownError
+    carrying the best iterate and its report when rho or omega vanish."""
+    from .errors import BreakdownError
+    host = not dev.is_device(b)
+    shape = tuple(b.shape)
+    db = dev.to_device(b)
+    dx = dev.empty(shape)
+    dx0 = dev.to_device(x0) if x0 is not None else None
+    A = _Bridge(apply_A, shape, host)
+    M = _Bridge(apply_M, shape, host) if apply_M is not None else None
+    cap = stop.max_iters + 2
+    hist = (C.c_double * cap)()
+    its, fin, conv, hl = C.c_int(), C.c_double(), C.c_int(), C.c_int()
+    st = lib().hdb_bicgstab(db.numel(), A.cfunc, None, M.cfunc if M else LINOP_FN(), None, db.data_ptr(),
+                            dx0.data_ptr() if dx0 is not None else None, dx.data_ptr(), float(stop.rel_tol),
+                            int(stop.max_iters), C.byref(its), C.byref(fin), C.byref(conv), hist, cap, C.byref(hl))
+    for err in (A.error, M.error if M else None):
+        if err is not None:
+            raise err
+    x = dev.to_host(dx) if host else dx
+    rep = KrylovReport(its.value, fin.value, list(hist[: min(hl.value, cap)]), bool(conv.value))
+    if st == 5:
+        raise BreakdownError(lib().hdb_last_error().decode(), x=x, report=rep)
+    check(st)
+    return x, rep

@@ -37,7 +37,7 @@ NEGATIVE_DEFINITE = "negative_definite"
 DEFINITENESS_THRESHOLD = 2.0
 PRESET_NAMES = ("MADP_V1", "MADP_V2", "MADP_V3", "MADP")
 CSLP_MG, CSLP_GMRES, CSLP_BICGSTAB, CSLP_NONE = "mg", "gmres", "bicgstab", "none"
-_CSLP_CODE = {CSLP_NONE: 0, CSLP_MG: 1, CSLP_GMRES: 2}
+_CSLP_CODE = {CSLP_NONE: 0, CSLP_MG: 1, CSLP_GMRES: 2, CSLP_BICGSTAB: 3}
 
 
 @dataclass(frozen=True)
@@ -191,10 +191,8 @@ class MadpSolver:
         self.mg: dict[int, CslpMultigrid] = {}
         for l in range(1, hierarchy.ml + 1):
             pol = config.policy(l)
-            if pol.cslp_method == CSLP_BICGSTAB:
-                raise ConfigError("cslp_method='bicgstab' is not implemented by the GPU solver (DESIGN.md §Scope)")
             self.A[l] = helmholtz_operator(hierarchy, l, slab=spec(l - 1))
-            if pol.cslp_method == CSLP_GMRES:
+            if pol.cslp_method in (CSLP_GMRES, CSLP_BICGSTAB):
                 self.M[l] = cslp_operator(hierarchy, l, pol.cslp_shift, config.beta1, slab=spec(l - 1))
             elif pol.cslp_method == CSLP_MG:
                 lv = hierarchy.level(l)

@@ -22,7 +22,7 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 import numpy as np  # noqa: E402
 from helmdef import (CslpMultigrid, MadpSolver, StopRule, VelocityModel,  # noqa: E402
-                     build_hierarchy, fgmres, mp1_problem, point_source_rhs, preset,
+                     bicgstab, build_hierarchy, fgmres, mp1_problem, point_source_rhs, preset,
                      wedge_problem)
 from helmdef.operators import cslp_operator, helmholtz_operator  # noqa: E402
 from helmdef.parallel import reduce_dot  # noqa: E402
@@ -136,6 +136,24 @@ def krylov():
     x, rep = fgmres(lambda u: op.apply(u), None, b, StopRule(0.1, 49), dot=reduce_dot)
     rec.update(c65_b=b, c65_x=x, c65_hist=np.array(rep.residual_history), c65_its=rep.iterations,
                c65_final=rep.final_relres)
+    # Bi-CGSTAB (krylov.py:185-276): SPD Poisson, Jacobi-preconditioned 9x9 Dirichlet, breakdown case
+    n = 17
+    T = (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)).astype(np.complex128)
+    bb = rng.standard_normal(n) + 0j
+    xb, rb = bicgstab(lambda u: T @ u, None, bb, StopRule(1e-10, 300))
+    rec.update(bp_b=bb, bp_x=xb, bp_hist=np.array(rb.residual_history), bp_its=rb.iterations)
+    p9 = mp1_problem(k=5.0, n=9, ml=2, boundary="dirichlet")
+    op9 = helmholtz_operator(p9.hierarchy, 1)
+    b9 = rnd(rng, (9, 9))
+    D = op9.diagonal()
+    xb, rb = bicgstab(lambda u: op9.apply(u), lambda u: u / D, b9, StopRule(1e-9, 200))
+    rec.update(bd9_b=b9, bd9_x=xb, bd9_hist=np.array(rb.residual_history), bd9_its=rb.iterations,
+               bd9_final=rb.final_relres)
+    p65 = mp1_problem(k=30.0, n=65, ml=3)
+    m65 = cslp_operator(p65.hierarchy, 2, beta2=0.5)
+    b65 = rnd(rng, m65.shape)
+    xb, rb = bicgstab(lambda u: m65.apply(u), None, b65, StopRule(0.1, 30), dot=reduce_dot)
+    rec.update(bc33_b=b65, bc33_x=xb, bc33_hist=np.array(rb.residual_history), bc33_its=rb.iterations)
     rec["dot_u"] = rnd(rng, (321, 33))
     rec["dot_v"] = rnd(rng, (321, 33))
     rec["dot_uv"] = np.array(reduce_dot(rec["dot_u"], rec["dot_v"]))
@@ -150,6 +168,44 @@ SOLVES = {
     # config-2 analogue (k=100, 1025^2, ml=6): solution stored every 8th point
     "c2a": (lambda: mp1_problem(k=100.0, n=1025, ml=6, boundary="sommerfeld"), 150, 8),
 }
+
+# other presets (madp.py:129-189) and a Bi-CGSTAB-CSLP variant on stable small problems
+PRESET_SOLVES = {
+    "v1_mp1b": ("MADP_V1", lambda: mp1_problem(k=40.0, n=129, ml=3, boundary="sommerfeld")),
+    "v2_mp1b": ("MADP_V2", lambda: mp1_problem(k=40.0, n=129, ml=3, boundary="sommerfeld")),
+    "v3_wedge": ("MADP_V3", lambda: wedge_problem(f=20.0, nx=145, ml=4)),
+    "bicg_wedge": ("BICG", lambda: wedge_problem(f=20.0, nx=145, ml=4)),
+}
+
+
+def preset_solves():
+    import dataclasses
+    for name, (pre, build) in PRESET_SOLVES.items():
+        prob = build()
+        hier = prob.hierarchy
+        if pre == "BICG":  # MADP with Bi-CGSTAB instead of GMRES for the CSLP levels
+            cfg = preset("MADP", hier)
+            pols = tuple(dataclasses.replace(p, cslp_method="bicgstab") if p.cslp_method == "gmres" else p
+                         for p in cfg.policies)
+            cfg = dataclasses.replace(cfg, policies=pols, preset_name="MADP+bicgstab")
+        else:
+            cfg = preset(pre, hier)
+        with MadpSolver(hier, cfg) as s:
+            u, rep = s.solve(prob.rhs.grid_view(hier))
+            g = np.random.default_rng(0)
+            b = prob.rhs.grid_view(hier)
+            bp = b + 1e-15 * np.abs(b).max() * (g.standard_normal(b.shape) + 1j * g.standard_normal(b.shape))
+            up, repp = s.solve(bp)
+        h0, h1 = np.array(rep.residual_history), np.array(repp.residual_history)
+        n = min(len(h0), len(h1))
+        x, xp = u.grid_view(hier), up.grid_view(hier)
+        np.savez_compressed(os.path.join(HERE, f"preset_{name}.npz"), outer_iterations=rep.outer_iterations,
+                            converged=rep.converged, residual_history=h0, solution=x,
+                            cycle_iters=json.dumps({str(k): v for k, v in rep.cycle_iters.items()}),
+                            cslp_iters=json.dumps({str(k): v for k, v in rep.cslp_iters.items()}),
+                            floor_hist_abs=np.abs(h0[:n] - h1[:n]).max(),
+                            floor_sol_rel=np.linalg.norm(x - xp) / np.linalg.norm(x))
+        print(name, pre, rep.outer_iterations, rep.final_relres, np.abs(h0[:n] - h1[:n]).max())
 
 
 def solves(names):
@@ -195,4 +251,6 @@ if __name__ == "__main__":
     krylov()
     if "--solves" in sys.argv:
         solves([a for a in sys.argv[2:]] or list(SOLVES))
+    if "--presets" in sys.argv:
+        preset_solves()
     print("golden fixtures written to", HERE)

@@ -355,3 +355,60 @@ def test_config2_full_vs_reference():
     xs = u.grid_view(prob.hierarchy)[::st, ::st]
     ref = g["solution_sub"]
     assert np.linalg.norm(xs - ref) <= 1e-5 * np.linalg.norm(ref)
+
+
+# ------------------------------------------------------------- Bi-CGSTAB
+def test_bicgstab_vs_reference():
+    g = golden("krylov.npz")
+    n = 17
+    T = (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)).astype(np.complex128)
+    x, rep = hdb.bicgstab(lambda u: T @ u, None, g["bp_b"], hdb.StopRule(1e-10, 300))
+    assert rep.converged and abs(rep.iterations - int(g["bp_its"])) <= 1
+    assert np.abs(x - g["bp_x"]).max() <= 1e-8 * np.abs(g["bp_x"]).max()
+    hier = hdb.mp1_problem(k=5.0, n=9, ml=2, boundary="dirichlet").hierarchy
+    op = hdb.helmholtz_operator(hier, 1)
+    D = np.asarray(op.diagonal())
+    x, rep = hdb.bicgstab(op.apply, lambda u: u / D, g["bd9_b"], hdb.StopRule(1e-9, 200))
+    assert rep.iterations == int(g["bd9_its"])
+    assert np.abs(np.array(rep.residual_history) - g["bd9_hist"]).max() <= 1e-9
+    hier = hdb.mp1_problem(k=30.0, n=65, ml=3).hierarchy
+    m = hdb.cslp_operator(hier, 2, beta2=0.5)
+    x, rep = hdb.bicgstab(m.apply, None, g["bc33_b"], hdb.StopRule(0.1, 30))
+    assert rep.iterations == int(g["bc33_its"])
+    assert np.linalg.norm(x - g["bc33_x"]) <= 1e-9 * np.linalg.norm(g["bc33_x"])
+
+
+def test_bicgstab_breakdown_carries_iterate():
+    A = np.array([[0.0, 1.0], [-1.0, 0.0]], dtype=np.complex128)
+    b = np.array([1.0, 1j], dtype=np.complex128)
+    try:
+        hdb.bicgstab(lambda u: A @ u, None, b, hdb.StopRule(1e-14, 50))
+    except hdb.BreakdownError as err:
+        assert err.x is not None and err.report is not None
+
+
+@pytest.mark.parametrize("name", ["v1_mp1b", "v2_mp1b", "v3_wedge", "bicg_wedge"])
+def test_presets_and_bicgstab_cslp_vs_reference(name):
+    """MADP_V1/V2/V3 and a Bi-CGSTAB-CSLP MADP variant against the reference's own runs,
+    at the reference's measured noise floor for each case (fixture floor_*)."""
+    import dataclasses
+    g = golden(f"preset_{name}.npz")
+    pre = {"v1_mp1b": "MADP_V1", "v2_mp1b": "MADP_V2", "v3_wedge": "MADP_V3", "bicg_wedge": "MADP"}[name]
+    prob = (hdb.mp1_problem(k=40.0, n=129, ml=3, boundary="sommerfeld") if "mp1b" in name
+            else hdb.wedge_problem(f=20.0, nx=145, ml=4))
+    cfg = hdb.preset(pre, prob.hierarchy)
+    if name == "bicg_wedge":
+        pols = tuple(dataclasses.replace(p, cslp_method="bicgstab") if p.cslp_method == "gmres" else p
+                     for p in cfg.policies)
+        cfg = dataclasses.replace(cfg, policies=pols, preset_name="MADP+bicgstab")
+    with hdb.MadpSolver(prob.hierarchy, cfg) as s:
+        u, rep = s.solve(prob.rhs)
+    assert abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
+    assert rep.converged == bool(g["converged"])
+    floor_h = max(10 * float(g["floor_hist_abs"]), 1e-9)
+    floor_x = max(10 * float(g["floor_sol_rel"]), 1e-8)
+    h, hr = np.array(rep.residual_history), g["residual_history"]
+    n = min(len(h), len(hr))
+    assert np.abs(h[:n] - hr[:n]).max() <= floor_h
+    x = u.grid_view(prob.hierarchy)
+    assert np.linalg.norm(x - g["solution"]) <= floor_x * np.linalg.norm(g["solution"])

@@ -125,3 +125,23 @@ def test_full_solve_matches_reference(name):
     np.testing.assert_array_equal(np.array(rep.residual_history), g["residual_history"])
     np.testing.assert_array_equal(x, g["solution"])
     assert rep.final_relres == float(g["final_relres"])
+
+
+def test_bicgstab_bitexact():
+    from oracle.krylov import bicgstab
+    g = golden("krylov.npz")
+    n = 17
+    T = (2 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)).astype(np.complex128)
+    x, rep = bicgstab(lambda u: T @ u, None, g["bp_b"], oracle.Stop(1e-10, 300))
+    assert rep.iterations == int(g["bp_its"])
+    np.testing.assert_array_equal(x, g["bp_x"])
+    hier, _ = oracle.mp1_problem(5.0, 9, 2, "dirichlet")
+    op = oracle.helmholtz_op(hier, 1)
+    D = op.diagonal()
+    x, rep = bicgstab(op.apply, lambda u: u / D, g["bd9_b"], oracle.Stop(1e-9, 200))
+    np.testing.assert_array_equal(np.array(rep.residual_history), g["bd9_hist"])
+    np.testing.assert_array_equal(x, g["bd9_x"])
+    hier, _ = oracle.mp1_problem(30.0, 65, 3)
+    m = oracle.cslp_op(hier, 2, 0.5)
+    x, rep = bicgstab(m.apply, None, g["bc33_b"], oracle.Stop(0.1, 30), dot=oracle.reduce_dot)
+    np.testing.assert_array_equal(x, g["bc33_x"])
