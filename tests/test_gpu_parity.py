@@ -415,3 +415,22 @@ def test_presets_and_bicgstab_cslp_vs_reference(name):
     assert np.abs(h[:n] - hr[:n]).max() <= floor_h
     x = u.grid_view(prob.hierarchy)
     assert np.linalg.norm(x - g["solution"]) <= floor_x * np.linalg.norm(g["solution"])
+
+
+@pytest.mark.parametrize("f", [10, 20, 40])
+def test_config3_wedge_vs_reference(f):
+    """BASELINE configs[2]: wedge with the BASELINE interfaces, h = 0.5 m (1201 x 2001), 5 levels,
+    against the reference's own full runs (tests/golden/solve_c3_*.npz)."""
+    g = golden(f"solve_c3_{f}.npz")
+    prob = hdb.wedge_problem(f=float(f), nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS)
+    with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
+        u, rep = s.solve(prob.rhs)
+    assert abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
+    assert rep.converged and rep.final_relres <= 1e-6
+    h, hr = np.array(rep.residual_history), g["residual_history"]
+    n = min(len(h), len(hr))
+    assert np.abs(h[:n] - hr[:n]).max() <= 1e-6
+    st = int(g["solution_stride"])
+    xs = u.grid_view(prob.hierarchy)[::st, ::st]
+    ref = g["solution_sub"]
+    assert np.linalg.norm(xs - ref) <= 1e-6 * np.linalg.norm(ref)
