@@ -53,16 +53,14 @@ CONFIGS = {
     "c3_40": ("BASELINE configs[2] @40 Hz: wedge 600x1000 m, h=0.5 m, 1201x2001, ml=5, MADP",
               lambda hdb: hdb.wedge_problem(f=40.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS)),
     "c5": ("BASELINE configs[4] weak scaling: 8193 x (8192 P + 1) per P GPUs, h=1/8192, k^3 h^2 = 0.5, ml=7",
-           lambda hdb, P=1: c5_problem(hdb, P)),
+           lambda hdb, P=1: hdb.c5_problem(P)),
+    "c4_40": ("BASELINE configs[3] @40 Hz: seeded folded/faulted layers 9192x3000 m, h=0.75 m (12257x4001), ml=6",
+              lambda hdb: hdb.synthetic_layered_problem(40.0, 0.75, 6)),
 }
 
 
 def c5_problem(hdb, P):
-    """[0,1] x [0,P], h = 1/8192, k = (0.5 / h^2)^(1/3), Sommerfeld, centre source."""
-    h = 1.0 / 8192
-    k = (0.5 / h ** 2) ** (1.0 / 3.0)
-    hier = hdb.build_hierarchy(((0.0, 1.0), (0.0, float(P))), h=h, ml=7, k=k, boundary="sommerfeld")
-    return hdb.grid.Problem("c5", hier, hdb.point_source_rhs(hier, (0.5, P / 2.0)))
+    return hdb.c5_problem(P)
 
 
 def _peaks():

@@ -178,6 +178,26 @@ PRESET_SOLVES = {
 }
 
 
+def c4_solve():
+    """BASELINE configs[3] model (this package's seeded generator, raster fed to the
+    reference as a gridfile VelocityModel) at h = 6 m, 40 Hz, 3 levels."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+    from paper_2412_04980_b200.models import C4_DOMAIN, C4_SOURCE, synthetic_layered_velocity
+    v = synthetic_layered_velocity(2412, dx=6.0)
+    vel = VelocityModel(kind="gridfile", values=v.values, dx=v.dx, dy=v.dy, x0=v.x0, y0=v.y0)
+    hier = build_hierarchy(C4_DOMAIN, h=6.0, ml=3, velocity=vel, f=40.0)
+    b = point_source_rhs(hier, C4_SOURCE).grid_view(hier)
+    with MadpSolver(hier, preset("MADP", hier)) as s:
+        u, rep = s.solve(b)
+    x = u.grid_view(hier)
+    np.savez_compressed(os.path.join(HERE, "solve_c4_h6_f40.npz"), outer_iterations=rep.outer_iterations,
+                        converged=rep.converged, final_relres=rep.final_relres,
+                        residual_history=np.array(rep.residual_history), solution_stride=np.array(4),
+                        solution_sub=x[::4, ::4], ksq_checksum=np.array([hier.ksq[0].sum(), hier.ksq[2].sum()]),
+                        cycle_iters=json.dumps({str(k): v for k, v in rep.cycle_iters.items()}))
+    print("c4", rep.outer_iterations, rep.final_relres, rep.wall_ms)
+
+
 def preset_solves():
     import dataclasses
     for name, (pre, build) in PRESET_SOLVES.items():
@@ -253,4 +273,6 @@ if __name__ == "__main__":
         solves([a for a in sys.argv[2:]] or list(SOLVES))
     if "--presets" in sys.argv:
         preset_solves()
+    if "--c4" in sys.argv:
+        c4_solve()
     print("golden fixtures written to", HERE)

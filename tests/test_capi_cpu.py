@@ -144,3 +144,22 @@ def test_slab_partition_nesting():
             if l > 1:  # coarse slab starts are injections of fine slab starts
                 fine = part.level_slabs(l - 1)
                 assert all(c.j0 * 2 == f.j0 for c, f in zip(slabs, fine))
+
+
+def test_synthetic_layered_model_is_seeded_and_in_range():
+    from paper_2412_04980_b200.models import synthetic_layered_velocity
+    a = synthetic_layered_velocity(7, dx=24.0)
+    b = synthetic_layered_velocity(7, dx=24.0)
+    c = synthetic_layered_velocity(8, dx=24.0)
+    np.testing.assert_array_equal(a.values, b.values)
+    assert not np.array_equal(a.values, c.values)
+    assert a.values.min() >= 1500.0 and a.values.max() <= 5500.0
+    # velocity increases with depth on average (row 0 is the bottom, y = -3000 m)
+    assert a.values[0].mean() > a.values[-1].mean() + 2000.0
+    # the same raster through the oracle's grid builder (reference bilinear rule) gives the same k^2
+    from paper_2412_04980_b200.models import C4_DOMAIN
+    hier = hdb.build_hierarchy(C4_DOMAIN, h=24.0, ml=2, velocity=a, f=10.0)
+    from oracle.grid import build_hierarchy as obuild
+    import paper_2412_04980_b200.grid as pg
+    oh = obuild(C4_DOMAIN, 24.0, 2, speed=lambda x, y: pg._raster(a, x, y), f=10.0)
+    np.testing.assert_array_equal(hier.ksq_at(1), oh.ksq_at(1))

@@ -434,3 +434,20 @@ def test_config3_wedge_vs_reference(f):
     xs = u.grid_view(prob.hierarchy)[::st, ::st]
     ref = g["solution_sub"]
     assert np.linalg.norm(xs - ref) <= 1e-6 * np.linalg.norm(ref)
+
+
+def test_config4_synthetic_layered_vs_reference():
+    """BASELINE configs[3] model (seeded generator, models.py) at h = 6 m, 40 Hz, 3 levels, against
+    the reference solving the same raster (tests/golden/solve_c4_h6_f40.npz)."""
+    g = golden("solve_c4_h6_f40.npz")
+    prob = hdb.synthetic_layered_problem(40.0, 6.0, 3)
+    hier = prob.hierarchy
+    np.testing.assert_allclose([hier.ksq[0].sum(), hier.ksq[2].sum()], g["ksq_checksum"], rtol=0, atol=0)
+    with hdb.MadpSolver(hier, hdb.preset("MADP", hier)) as s:
+        u, rep = s.solve(prob.rhs)
+    assert abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
+    h, hr = np.array(rep.residual_history), g["residual_history"]
+    n = min(len(h), len(hr))
+    assert np.abs(h[:n] - hr[:n]).max() <= 1e-6
+    st = int(g["solution_stride"])
+    assert np.linalg.norm(u.grid_view(hier)[::st, ::st] - g["solution_sub"]) <= 1e-6 * np.linalg.norm(g["solution_sub"])

@@ -22,7 +22,11 @@ CASES = {
     "c3_10": lambda: hdb.wedge_problem(f=10.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS),
     "c3_20": lambda: hdb.wedge_problem(f=20.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS),
     "c3_40": lambda: hdb.wedge_problem(f=40.0, nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS),
-    "c5": lambda: __import__("bench").c5_problem(hdb, 1),
+    "c5": lambda: hdb.c5_problem(1),
+    "c4_40": lambda: hdb.synthetic_layered_problem(40.0, 0.75, 6),
+    "c4_20": lambda: hdb.synthetic_layered_problem(20.0, 0.75, 6),
+    "c4_10": lambda: hdb.synthetic_layered_problem(10.0, 0.75, 6),
+    "c4s": lambda: hdb.synthetic_layered_problem(40.0, 6.0, 3),
 }
 
 
