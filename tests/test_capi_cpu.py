@@ -158,8 +158,8 @@ def test_synthetic_layered_model_is_seeded_and_in_range():
     assert a.values[0].mean() > a.values[-1].mean() + 2000.0
     # the same raster through the oracle's grid builder (reference bilinear rule) gives the same k^2
     from paper_2412_04980_b200.models import C4_DOMAIN
-    hier = hdb.build_hierarchy(C4_DOMAIN, h=24.0, ml=2, velocity=a, f=10.0)
+    hier = hdb.build_hierarchy(C4_DOMAIN, h=12.0, ml=2, velocity=a, f=10.0)
     from oracle.grid import build_hierarchy as obuild
     import paper_2412_04980_b200.grid as pg
-    oh = obuild(C4_DOMAIN, 24.0, 2, speed=lambda x, y: pg._raster(a, x, y), f=10.0)
+    oh = obuild(C4_DOMAIN, 12.0, 2, speed=lambda x, y: pg._raster(a, x, y), f=10.0)
     np.testing.assert_array_equal(hier.ksq_at(1), oh.ksq_at(1))
