@@ -37,6 +37,24 @@ static int guarded(F&& f) {
   }
 }
 
+// constant-k^2 levels get the per-tap coefficient table (same rounding as per point)
+static void set_uniform(OpCoef& c, const double* ksq, long long n) {
+  c.uniform = 0;
+  if (n < 1) return;
+  const double k0 = ksq[0];
+  for (long long i = 1; i < n; ++i)
+    if (ksq[i] != k0) return;
+  c.uniform = 1;
+  c.ku = k0;
+  const int N = 2 * c.radius + 1;
+  for (int t = 0; t < N * N; ++t) {
+    volatile double mk_r = c.mass[t].x * k0;  // separate roundings, as __dmul_rn / __dadd_rn on device
+    volatile double mk_i = c.mass[t].y * k0;
+    volatile double re = c.lap[t] + mk_r;
+    c.ucoef[t] = mkc(re, mk_i);
+  }
+}
+
 static void check_launch() {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw Error(E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -94,6 +112,7 @@ int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int*
     }
     L.g.nx = nx; L.g.ny = ny; L.g.row0 = 0; L.g.nyg = ny;
     L.n = (long long)nx * ny;
+    set_uniform(L.c, ksq_host, L.n);
     L.ksq = (double*)E.alloc_bytes(sizeof(double) * L.n);
     HDB_CUDA(cudaMemcpyAsync(L.ksq, ksq_host, sizeof(double) * L.n, cudaMemcpyHostToDevice, E.st));
     HDB_CUDA(cudaStreamSynchronize(E.st));
@@ -127,6 +146,7 @@ int hdb_op_create_slab(hdb_op** out, int nx, int ny_global, int radius, double h
     double* base = (double*)E.alloc_bytes(sizeof(double) * (L.n + 2 * hel));
     HDB_CUDA(cudaMemsetAsync(base, 0, sizeof(double) * (L.n + 2 * hel), E.st));
     L.ksq = base + hel;
+    set_uniform(L.c, ksq_full_host, (long long)nx * ny_global);
     const int r_lo = std::max(0, row0 - halo), r_hi = std::min(ny_global, row0 + ny_local + halo);
     HDB_CUDA(cudaMemcpyAsync(L.ksq + (long long)(r_lo - row0) * nx, ksq_full_host + (long long)r_lo * nx,
                              sizeof(double) * (size_t)(r_hi - r_lo) * nx, cudaMemcpyHostToDevice, E.st));

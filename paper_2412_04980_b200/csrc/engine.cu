@@ -263,7 +263,7 @@ void SmallSolve::ensure(const LevelOp* o, int cap_) {
   cap = cap_;
   basis = E.alloc((long long)(cap + 1) * o->n);
   Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap);
-  gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1));
+  gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
 }
 
 bool SmallSolve::try_run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {
@@ -366,7 +366,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     // else one fused launch per coefficient
     bool coop = false;
     if (!shard && n >= coop_mgs_min()) {
-      if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1));
+      if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
       if (ws.dV_cap < j + 1) {
         E.free(ws.dV);
         ws.dV_cap = std::max(2 * (j + 1), 64);

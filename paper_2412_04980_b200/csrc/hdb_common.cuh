@@ -63,6 +63,9 @@ struct OpCoef {
   double E;              // radius 1: (-s*2)*h  (Sommerfeld diagonal increment factor)
   double lap[49];        // (2r+1)^2 row-major lap_coef
   cd mass[49];           // (2r+1)^2 row-major mass_coef
+  int uniform;           // k^2 is one constant on this level (host-checked): ucoef valid
+  double ku;             // that constant
+  cd ucoef[49];          // lap + mass * ku per tap, same rounded operations as the per-point form
 };
 
 constexpr int kReduceThreads = 256;

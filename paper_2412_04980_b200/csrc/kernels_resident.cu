@@ -303,19 +303,40 @@ struct GridSync {
   __device__ int nranks() const { return (int)gridDim.x; }
   __device__ void barrier() { gr.sync(); }
   __device__ void init(RSmem&, void*) {}
-  // s.pv[0..m) -> out[0..m), fixed rank order
+  // s.pv[0..m) -> out[0..m), fixed rank order.  Two phases when m is large:
+  // CTA i sums element i over the P partials (one column each), publishes it,
+  // then every CTA reads the m sums; small m: every CTA sums everything itself.
   __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd* gpart) {
     const int P = nranks();
-    for (int i = threadIdx.x; i < m; i += blockDim.x) __stcg(&gpart[((long long)buf * P + blockIdx.x) * kVecCap + i], s.pv[i]);
+    cd* col = gpart + (long long)buf * P * kVecCap;
+    for (int i = threadIdx.x; i < m; i += blockDim.x) __stcg(&col[(long long)blockIdx.x * kVecCap + i], s.pv[i]);
     gr.sync();
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      cd q = mkc(0.0, 0.0);
-      for (int r = 0; r < P; ++r) {
-        const cd z = __ldcg(&gpart[((long long)buf * P + r) * kVecCap + i]);
-        q.x += z.x;
-        q.y += z.y;
+    if (m <= 4) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        cd q = mkc(0.0, 0.0);
+        for (int r = 0; r < P; ++r) {
+          const cd z = __ldcg(&col[(long long)r * kVecCap + i]);
+          q.x += z.x;
+          q.y += z.y;
+        }
+        out[i] = q;
       }
-      out[i] = q;
+    } else {
+      cd* sums = gpart + 2LL * P * kVecCap + (long long)buf * kVecCap;  // published element sums
+      for (int i = blockIdx.x; i < m; i += P) {
+        if (threadIdx.x < 32) {
+          cd q = mkc(0.0, 0.0);
+          for (int r = threadIdx.x; r < P; r += 32) {
+            const cd z = __ldcg(&col[(long long)r * kVecCap + i]);
+            q.x += z.x;
+            q.y += z.y;
+          }
+          q = warp_sum_c(q);
+          if (threadIdx.x == 0) __stcg(&sums[i], q);
+        }
+      }
+      gr.sync();
+      for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = __ldcg(&sums[i]);
     }
     __syncthreads();
     buf ^= 1;
