@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
 // ------------------------------------------------------------------------
 static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny + 7) / 8); }
 static inline dim3 grid_r1s(const Geom& g) { return dim3((g.nx + SX - 1) / SX, (g.ny + SY * RB - 1) / (SY * RB)); }
-static inline bool use_strip(const Geom& g) { return g.nx >= 64 && g.ny >= SY * RB; }
+static inline bool use_strip(const Geom& g) { return g.nx >= 512 && g.ny >= 512; }  // small grids: all blocks are boundary blocks
 
 void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
                   int mode, cudaStream_t st) {

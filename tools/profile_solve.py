@@ -41,12 +41,15 @@ def main():
     s = hdb.MadpSolver(prob.hierarchy, cfg)
     b = torch.from_numpy(prob.rhs.grid_view(prob.hierarchy).copy()).cuda()
     x = torch.empty_like(b)
+    dms = []
     for r in range(a.repeat):
         t0 = time.perf_counter()
         rep = s.solve_device(b, x)
         wall = time.perf_counter() - t0
+        dms.append(rep.device_ms)
     out = {"case": a.case, "outer": rep.outer_iterations, "converged": rep.converged,
            "final_relres": rep.final_relres, "device_ms": rep.device_ms, "wall_s": wall,
+           "device_ms_all": [round(v, 1) for v in dms],
            "cycle_max": {l: rep.cycle_max(l) for l in range(2, prob.hierarchy.ml + 1)},
            "cslp_max": {l: rep.cslp_max(l) for l in range(1, prob.hierarchy.ml + 1)},
            "cslp_calls": {l: len(v) for l, v in rep.cslp_iters.items()},
