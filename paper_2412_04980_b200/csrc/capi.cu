@@ -16,7 +16,13 @@ struct hdb_op {
   int* dres = nullptr;  // its (int) + relres (double)
 };
 struct hdb_mg { Multigrid mg; };
-struct hdb_solver { MadpSolver s; };
+struct hdb_solver {
+  MadpSolver s;
+  cd *db = nullptr, *dx = nullptr;  // device staging for host-buffer solves (kept across calls)
+  ~hdb_solver() {
+    if (engine_ready()) { engine().free(db); engine().free(dx); }
+  }
+};
 
 static thread_local std::string g_err;
 
@@ -409,21 +415,19 @@ int hdb_solver_solve(hdb_solver* s, const void* b, void* x, int host_buffers) {
       s->s.solve((const cd*)b, (cd*)x);
       return;
     }
-    cd* db = E.alloc(n);
-    cd* dx = E.alloc(n);
+    if (!s->db) {
+      s->db = E.alloc(n);
+      s->dx = E.alloc(n);
+    }
     try {
-      HDB_CUDA(cudaMemcpyAsync(db, b, sizeof(cd) * n, cudaMemcpyHostToDevice, E.st));
-      s->s.solve(db, dx);
-      HDB_CUDA(cudaMemcpyAsync(x, dx, sizeof(cd) * n, cudaMemcpyDeviceToHost, E.st));
+      HDB_CUDA(cudaMemcpyAsync(s->db, b, sizeof(cd) * n, cudaMemcpyHostToDevice, E.st));
+      s->s.solve(s->db, s->dx);
+      HDB_CUDA(cudaMemcpyAsync(x, s->dx, sizeof(cd) * n, cudaMemcpyDeviceToHost, E.st));
       E.sync();
     } catch (...) {
       E.sync();
-      E.free(db);
-      E.free(dx);
       throw;
     }
-    E.free(db);
-    E.free(dx);
   });
 }
 int hdb_solver_report(hdb_solver* s, int* its, int* conv, double* fin, double* wall, int* hl) {
