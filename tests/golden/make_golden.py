@@ -198,6 +198,22 @@ def c4_solve():
     print("c4", rep.outer_iterations, rep.final_relres, rep.wall_ms)
 
 
+def io_files():
+    """Reference-written report / field / config files (format compatibility fixtures)."""
+    import helmdef.io as hio
+    cfg = hio.parse_config("problem = mp1b\nwavenumber = 50\nnx = 129\nlevels = 2\nlevel2.cycle_tol = 0.3\n")
+    prob = hio.build_problem(cfg)
+    with MadpSolver(prob.hierarchy, hio.build_solver_config(cfg, prob.hierarchy)) as s:
+        u, rep = s.solve(prob.rhs)
+    hio.write_report(rep, os.path.join(HERE, "ref_report_c1s.csv"))
+    p9 = mp1_problem(k=5.0, n=9, ml=2)
+    from helmdef import ComplexField
+    z = np.random.default_rng(4).standard_normal(81) + 1j * np.random.default_rng(5).standard_normal(81)
+    hio.write_field(ComplexField(1, z), p9.hierarchy, os.path.join(HERE, "ref_field_9.csv"))
+    with open(os.path.join(HERE, "ref_config_render.txt"), "w") as fh:
+        fh.write(hio.render_config(cfg))
+
+
 def preset_solves():
     import dataclasses
     for name, (pre, build) in PRESET_SOLVES.items():
@@ -275,4 +291,6 @@ if __name__ == "__main__":
         preset_solves()
     if "--c4" in sys.argv:
         c4_solve()
+    if "--io" in sys.argv:
+        io_files()
     print("golden fixtures written to", HERE)
