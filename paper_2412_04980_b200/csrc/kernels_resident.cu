@@ -474,52 +474,19 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   if (t == 0) s.g[0] = mkc(beta, 0.0);
   int its = 0;
   long long tprev_ = clock64();
-  for (int j = 0; j < A.cap; ++j) {
-    sy.barrier();  // V_j complete everywhere
-    PHASE(0);
-    const cd* vj = V(j);
+  // ws = M V_j for this CTA's points (stencil from the shared-memory windows).
+  // `givens_j` >= 0: thread 0 first applies the rotations of step givens_j,
+  // overlapping that serial work with everybody else's stencil points.
+  auto apply_M = [&](int jv, int givens_j, double hn_prev) {
+    const cd* vj = V(jv);
     if (A.tiled) {
       if (cnt > 0) load_u_tile<R>(ut, T, vj, A.ksq, A.g, A.c);
       __syncthreads();
-      for (int q = t; q < cnt; q += kRT) {
-        const long long p = p0 + q;
-        ws[q] = op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, (int)(p / nx) + A.g.row0, (int)(p % nx));
-      }
-    } else {
-      for (int q = t; q < cnt; q += kRT) {
-        const long long p = p0 + q;
-        ws[q] = op_point<R>(A.c, A.g, vj, A.ksq, (int)(p / nx) + A.g.row0, (int)(p % nx));
-      }
     }
-    PHASE(1);
-    if (ORTHO == 0) {
-      // modified Gram-Schmidt (krylov.py:121-124): h_i = <V_i, w>; w -= h_i V_i
-      for (int i = 0; i <= j; ++i) {
-        const cd* vi = V(i) + p0;
-        cd a = mkc(0.0, 0.0);
-        for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
-        const cd h = sy.reduce(a, s, buf, A.gpart);
-        if (t == 0) s.hcol[i] = h;
-        for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
-      }
-    } else {
-      // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
-      // Hessenberg column in exact arithmetic, two reductions instead of j+1
-      __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
-      for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
-      __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
-      for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
-      __syncthreads();
-    }
-    PHASE(2);
-    cd a = mkc(0.0, 0.0);
-    for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
-    const double hn = sqrt(fmax(sy.reduce(a, s, buf, A.gpart).x, 0.0));
-    PHASE(3);
-    if (t == 0) {
+    if (givens_j >= 0 && t == 0) {
       // rotations (krylov.py:126-151), identical in every CTA
+      const int j = givens_j;
+      const double hn = hn_prev;
       cd* col = s.hcol;
       col[j + 1] = mkc(hn, 0.0);
       bool finite = true;
@@ -557,23 +524,67 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       const double rel = cabs_(s.g[j + 1]) / bnorm;
       s.decision = !finite ? 2 : ((hn < 1e-30 || rel <= A.tol) ? 1 : 0);
     }
-    __syncthreads();
-    PHASE(4);
-    its = j + 1;
-    const int dec = s.decision;
-    if (dec == 2) {
-      if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = its; }
-      sy.barrier();
-      return;
+    if (jv < A.cap) {  // the stencil of step jv (skipped past the cap)
+      for (int q = t; q < cnt; q += kRT) {
+        const long long p = p0 + q;
+        const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
+        ws[q] = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, gj, i)
+                        : op_point<R>(A.c, A.g, vj, A.ksq, gj, i);
+      }
     }
-    if (dec == 1) break;
+    __syncthreads();
+  };
+  sy.barrier();  // V_0 complete everywhere
+  apply_M(0, -1, 0.0);
+  PHASE(1);
+  int dec = 0;
+  for (int j = 0; j < A.cap; ++j) {
+    if (ORTHO == 0) {
+      // modified Gram-Schmidt (krylov.py:121-124): h_i = <V_i, w>; w -= h_i V_i
+      for (int i = 0; i <= j; ++i) {
+        const cd* vi = V(i) + p0;
+        cd a = mkc(0.0, 0.0);
+        for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
+        const cd h = sy.reduce(a, s, buf, A.gpart);
+        if (t == 0) s.hcol[i] = h;
+        for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
+      }
+    } else {
+      // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
+      // Hessenberg column in exact arithmetic, two reductions instead of j+1
+      __syncthreads();
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
+      for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
+      __syncthreads();
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
+      for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
+      __syncthreads();
+    }
+    PHASE(2);
+    cd a = mkc(0.0, 0.0);
+    for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+    const double hn = sqrt(fmax(sy.reduce(a, s, buf, A.gpart).x, 0.0));
+    PHASE(3);
+    // V_{j+1} = w / ||w|| (harmless if step j turns out to be the last)
     const double inv = 1.0 / hn;
     cd* vn = V(j + 1) + p0;
     for (int q = t; q < cnt; q += kRT) {
       const cd v = ws[q];
       vn[q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
     }
+    sy.barrier();  // V_{j+1} complete everywhere
     PHASE(5);
+    // Givens of step j on thread 0 while the stencil of step j+1 runs
+    apply_M(j + 1, j, hn);
+    PHASE(4);
+    its = j + 1;
+    dec = s.decision;
+    if (dec != 0) break;
+  }
+  if (dec == 2) {
+    if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = its; }
+    sy.barrier();
+    return;
   }
   // least squares (krylov.py:161-168) on rank 0, y broadcast through global memory
   if (rank == 0 && t == 0) {
