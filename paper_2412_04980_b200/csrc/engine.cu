@@ -235,6 +235,12 @@ int resident_ortho() {
   return o;
 }
 
+bool step1_enabled() {
+  static int v = -1;
+  if (v < 0) v = (int)env_ll("HDB_STEP1", 1);
+  return v != 0;
+}
+
 long long coop_mgs_min() {
   static long long v = -1;
   if (v < 0) v = env_ll("HDB_COOP_MGS_N", 150000);
@@ -301,7 +307,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   };
   Engine& E = engine();
   if (stop.max_iters < 1) throw Error(E_ARG, "max_iters must be >= 1");
-  if (stop.max_iters + kSlotH + 2 >= kSlotMgPost) throw Error(E_ARG, "Krylov iteration cap too large");
+  if (stop.max_iters + kSlotH + 2 >= 900) throw Error(E_ARG, "Krylov iteration cap too large (max 896)");
   ws.ensure(n, stop.max_iters, M != nullptr);
   KReport rep;
 
@@ -466,6 +472,44 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   rep.final_relres = fin;
   rep.converged = conv;
   return rep;
+}
+
+// ------------------------------------------------------ one-step FGMRES
+// device scalar slots of the step: 5 per level (nested steps at deeper levels run
+// inside M and must not overwrite this level's scalars), above any Hessenberg column
+constexpr int kS1Base = 900;
+
+void fgmres_step1(long long n, const LinOp& A, const LinOp& M, const cd* b, cd* x, KWS& ws, int* its_dev,
+                  const LevelOp* dist, int level) {
+  Engine& E = engine();
+  if (level < 1 || kS1Base + 5 * level + 4 >= kSlotMgR0) throw Error(E_ARG, "one-step FGMRES level out of range");
+  const int kS1B = kS1Base + 5 * level, kS1H0 = kS1B + 1, kS1HN = kS1B + 2, kS1Y = kS1B + 3, kS1F = kS1B + 4;
+  ws.ensure(n, 1, true);
+  const bool shard = dist && dist->sharded;
+  auto red = [&](int slot) {
+    if (shard) dist->reduce(E.dscal + slot);
+  };
+  cd* S = E.dscal;
+  launch_dot(b, b, n, E.red, S + kS1B, E.st);  // ||b||^2 (krylov.py:92)
+  red(kS1B);
+  launch_scale_dev(b, ws.v(0), S + kS1B, n, E.st);  // V0 = r0 / beta
+  M(ws.v(0), ws.z(0));
+  cd* w = ws.v(1);
+  A(ws.z(0), w);
+  launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, S + kS1H0, E.st);  // h0 = <V0, w>
+  red(kS1H0);
+  launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st);  // w -= h0 V0; ||w||^2
+  red(kS1HN);
+  launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st);
+  ws.hbasis[0] = ws.z(0);
+  HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*), cudaMemcpyHostToDevice, E.st));
+  launch_lincomb(ws.dbasis, S + kS1Y, 1, nullptr, x, n, E.st);  // x = y0 Z0
+  // explicit true residual: only its finiteness matters to the caller (krylov.py:174-176)
+  A(x, ws.tmp);
+  launch_subnorm(b, ws.tmp, n, E.red, S + kS1F, E.st);
+  red(kS1F);
+  launch_finite_guard(S + kS1F, S + kSlotFlag, E.st);
+  E.launches += 9;
 }
 
 // --------------------------------------------------------------- Bi-CGSTAB
@@ -712,7 +756,7 @@ void MadpSolver::set_levels(int ml_) {
 void MadpSolver::setup() {
   Engine& E = engine();
   if (!dcounts) {
-    dcap = 1 << 16;
+    dcap = 1 << 20;  // never flushed mid-solve: a reserved slot may still be awaiting its kernel
     dcounts = (int*)E.alloc_bytes(sizeof(int) * dcap);
     drel = (double*)E.alloc_bytes(sizeof(double) * dcap);
   }
@@ -798,18 +842,31 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     return;
   }
   if (!M->sharded && resident_mode(M->n, L.cslp_stop.max_iters) >= 0) {
-    if (dused >= dcap) flush_counts();
     L.small_cslp.ensure(M, L.cslp_stop.max_iters);
-    if (L.small_cslp.try_run(rhs, out, L.cslp_stop, dcounts + dused, drel + dused)) {
-      rep.cslp_iters[l].push_back(-1);
-      pending.emplace_back(l, (int)rep.cslp_iters[l].size() - 1);
-      dused++;
-      return;
-    }
+    const int slot = reserve_count(l);
+    if (L.small_cslp.try_run(rhs, out, L.cslp_stop, dcounts + slot, drel + slot)) return;
+    unreserve_count(l);  // did not fit: the launch path below reports its own count
   }
   LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
   KReport r = fgmres(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_cslp, nullptr, nullptr, M);
   rep.cslp_iters[l].push_back(r.iterations);
+}
+
+// count slot for a device-side solve at `level` (< 0: deflation cycle of -level,
+// > 0: CSLP of level); its report entry is filled by flush_counts at the end
+int MadpSolver::reserve_count(int level) {
+  if (dused >= dcap) throw Error(E_ARG, "too many device-side solves in one call (raise dcap)");
+  auto& lst = level < 0 ? rep.cycle_iters[-level] : rep.cslp_iters[level];
+  lst.push_back(-1);
+  pending.emplace_back(level, (int)lst.size() - 1);
+  return dused++;
+}
+
+void MadpSolver::unreserve_count(int level) {
+  auto& lst = level < 0 ? rep.cycle_iters[-level] : rep.cslp_iters[level];
+  lst.pop_back();
+  pending.pop_back();
+  dused--;
 }
 
 // copy device-resident iteration counts into the report
@@ -819,7 +876,11 @@ void MadpSolver::flush_counts() {
     std::vector<int> h(dused);
     HDB_CUDA(cudaMemcpyAsync(h.data(), dcounts, sizeof(int) * dused, cudaMemcpyDeviceToHost, E.st));
     E.fetch(1);  // sync + flag check
-    for (int k = 0; k < dused; ++k) rep.cslp_iters[pending[k].first][pending[k].second] = h[k];
+    for (int k = 0; k < dused; ++k) {
+      const int lvl = pending[k].first;
+      if (lvl < 0) rep.cycle_iters[-lvl][pending[k].second] = h[k];
+      else rep.cslp_iters[lvl][pending[k].second] = h[k];
+    }
   }
   dused = 0;
   pending.clear();
@@ -837,12 +898,17 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   LinOp Mop;
   if (nxt == ml) Mop = [this, nxt](const cd* in, cd* o) { cslp_apply(nxt, in, o); };
   else Mop = [this, nxt](const cd* in, cd* o) { precond(nxt, in, o); };
-  KReport r;
   {
     ProfScope pd(rep, nxt, PROF_DEFL);
-    r = fgmres(N.A->n, Aop, &Mop, N.vhat, N.vtil, N.cycle_stop, N.ws_defl, nullptr, nullptr, N.A);
+    if (N.cycle_stop.rel_tol >= 1.0 && step1_enabled()) {  // exactly one iteration: no host round trip
+      // reserve the count slot BEFORE the call: nested solves inside M reserve their own
+      const int slot = reserve_count(-nxt);
+      fgmres_step1(N.A->n, Aop, Mop, N.vhat, N.vtil, N.ws_defl, dcounts + slot, N.A, nxt);
+    } else {
+      KReport r = fgmres(N.A->n, Aop, &Mop, N.vhat, N.vtil, N.cycle_stop, N.ws_defl, nullptr, nullptr, N.A);
+      rep.cycle_iters[nxt].push_back(r.iterations);
+    }
   }
-  rep.cycle_iters[nxt].push_back(r.iterations);
   prolong_levels(*N.A, *L.A, N.vtil, nullptr, L.t);
   rep.matvecs[l] += 1;
   L.A->residual(v, L.t, L.rhs);  // v - A t

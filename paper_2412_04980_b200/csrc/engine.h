@@ -130,6 +130,12 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
                const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr,
                const LevelOp* dist = nullptr);
 
+// One-iteration FGMRES (StopRule tol >= 1, zero guess) entirely on device: no host
+// synchronisation; the iteration count lands in *its_dev, failures raise the
+// device flag (checked at the next host read).  Same arithmetic as fgmres().
+void fgmres_step1(long long n, const LinOp& A, const LinOp& M, const cd* b, cd* x, KWS& ws, int* its_dev,
+                  const LevelOp* dist, int level);
+
 // Bi-CGSTAB workspace and solver (krylov.py:185-276); on breakdown *breakdown is
 // set and x holds the best iterate (the caller decides, as madp.py:293-297 does)
 struct BWS {
@@ -149,7 +155,8 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
 // 0 disables a mode.
 int resident_mode(long long n, int cap);  // -1: launch-driven path
 int resident_ortho();  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
-long long coop_mgs_min();  // levels >= this many points use the cooperative MGS step (HDB_COOP_MGS_N)
+long long coop_mgs_min();
+bool step1_enabled();  // HDB_STEP1=0 forces the host-driven path for one-iteration FGMRES  // levels >= this many points use the cooperative MGS step (HDB_COOP_MGS_N)
 
 struct SmallSolve {  // device-resident GMRES on one level operator
   const LevelOp* op = nullptr;
@@ -226,6 +233,8 @@ struct MadpSolver {
   int dcap = 0, dused = 0;
   std::vector<std::pair<int, int>> pending;  // (level, index into cslp_iters[level]) per slot
   void flush_counts();
+  int reserve_count(int level);
+  void unreserve_count(int level);
   std::vector<MadpLevel> lv;  // index 1..ml
   Stop outer{1e-6, 150};
   SolveReport rep;

@@ -32,6 +32,9 @@ void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st
 void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd* x, long long n, cudaStream_t st);
 void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st);
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st);
+void launch_scale_dev(const cd* x, cd* out, const cd* nrm2, long long n, cudaStream_t st);
+void launch_step1(const cd* b2, const cd* h0, const cd* hn2, cd* y, int* its, cd* flag, cudaStream_t st);
+void launch_finite_guard(const cd* v, cd* flag, cudaStream_t st);
 void launch_axpy(const cd* y, cd a, const cd* x, cd* out, long long n, int sub, cudaStream_t st);
 void launch_bicg_p(const cd* r, cd* p, const cd* v, cd beta, cd omega, long long n, cudaStream_t st);
 void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st);

@@ -168,6 +168,53 @@ __global__ void __launch_bounds__(256) k_gemv(const cd* __restrict__ A, const cd
   if (lane == 0) x[warp] = acc;
 }
 
+// out = x * (1/sqrt(max(nrm2->x, 0)))  (V0 = r0 / beta with beta on device; 0 if beta == 0)
+__global__ void k_scale_dev(const cd* __restrict__ x, cd* __restrict__ out, const cd* nrm2, long long n) {
+  const double beta = sqrt(fmax(nrm2->x, 0.0));
+  const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const cd v = x[p];
+    out[p] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+  }
+}
+
+// One-step FGMRES closure on device (krylov.py:130-168 with m = 1): from
+// b2 = ||b||^2, h0 = <V0, A z0>, hn2 = ||w||^2 form the Givens rotation, the
+// recurrence residual and y0 = c*beta / (c h0 + s hn).  Writes y0, the
+// iteration count (0 when b = 0) and raises the non-finite flag (2.0).
+__global__ void k_step1(const cd* b2, const cd* h0p, const cd* hn2, cd* y_out, int* its_out, cd* flag) {
+  const double beta = sqrt(fmax(b2->x, 0.0));
+  if (beta == 0.0) {
+    *y_out = mkc(0.0, 0.0);
+    *its_out = 0;
+    return;
+  }
+  const cd h1 = *h0p;
+  const double hn = sqrt(fmax(hn2->x, 0.0));
+  const bool finite = isfinite(h1.x) && isfinite(h1.y) && isfinite(hn) && isfinite(beta);
+  const double a1 = hypot(h1.x, h1.y), a2 = hn;
+  double c, sr, si;  // s = (sr, si)
+  if (a2 == 0.0) { c = 1.0; sr = 0.0; si = 0.0; }
+  else if (a1 == 0.0) { c = 0.0; sr = 1.0; si = 0.0; }
+  else {
+    const double t = hypot(a1, a2);
+    c = a1 / t;
+    sr = (h1.x / a1) * hn / t;  // (h1/|h1|) conj(hn) / t with hn real
+    si = (h1.y / a1) * hn / t;
+  }
+  const double rr = c * h1.x + sr * hn, ri = c * h1.y + si * hn;  // R00 = c h1 + s h2
+  const double g = c * beta;
+  const double d = rr * rr + ri * ri;
+  *y_out = mkc(g * rr / d, -g * ri / d);
+  *its_out = 1;
+  if (!finite || !(d > 0.0)) flag->x = 2.0;
+}
+
+// non-finite guard on a device scalar (explicit final residual, krylov.py:174-176)
+__global__ void k_finite_guard(const cd* v, cd* flag) {
+  if (!isfinite(v->x)) flag->x = 2.0;
+}
+
 // MG divergence guard (mg.py:133-138): flag |= sqrt(post2) > guard*sqrt(bn2)
 __global__ void k_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag) {
   const double post = sqrt(fmax(post2->x, 0.0)), bn = sqrt(fmax(bn2->x, 0.0));
@@ -208,6 +255,13 @@ void launch_bicg_p(const cd* r, cd* p, const cd* v, cd beta, cd omega, long long
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st) {
   k_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(A, b, x, n);
 }
+void launch_scale_dev(const cd* x, cd* out, const cd* nrm2, long long n, cudaStream_t st) {
+  k_scale_dev<<<ew_blocks(n), 256, 0, st>>>(x, out, nrm2, n);
+}
+void launch_step1(const cd* b2, const cd* h0, const cd* hn2, cd* y, int* its, cd* flag, cudaStream_t st) {
+  k_step1<<<1, 1, 0, st>>>(b2, h0, hn2, y, its, flag);
+}
+void launch_finite_guard(const cd* v, cd* flag, cudaStream_t st) { k_finite_guard<<<1, 1, 0, st>>>(v, flag); }
 void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st) {
   k_guard<<<1, 1, 0, st>>>(post2, bn2, r02, guard, flag);
 }
