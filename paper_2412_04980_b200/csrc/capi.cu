@@ -481,7 +481,9 @@ int hdb_solver_profile(hdb_solver* s, double* ms_host, long long* calls_host, in
   return guarded([&] {
     const SolveReport& r = s->s.rep;
     for (int i = 0; i < cap && i < (int)r.prof_ms.size(); ++i) {
-      ms_host[i] = r.prof_ms[i];
+      // device time when HDB_PROFILE=1 recorded it, else host wall time
+      const bool dev = i < (int)r.dev_ms.size() && r.dev_ms[i] > 0.0;
+      ms_host[i] = dev ? r.dev_ms[i] : r.prof_ms[i];
       calls_host[i] = r.prof_calls[i];
     }
     *syncs = r.syncs;

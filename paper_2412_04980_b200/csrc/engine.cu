@@ -212,6 +212,8 @@ cd* KWS::z(int i) {
 KWS::~KWS() {
   if (!engine_ready()) return;
   Engine& E = engine();
+  E.free(gst);
+  if (hflags) cudaFreeHost(hflags);
   E.free(dV);
   E.free(gpart);
   for (auto p : V) E.free_h(p, halo);
@@ -472,6 +474,96 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   rep.final_relres = fin;
   rep.converged = conv;
   return rep;
+}
+
+// --------------------------------------------- device-driven GMRES (launch path)
+static bool gmres_device_enabled() {
+  static int v = -1;
+  if (v < 0) v = (int)env_ll("HDB_GMRES_DEV", 1);
+  return v != 0;
+}
+
+// make V_0..V_upto exist and their pointers visible in the device table ws.dV
+static void ensure_vtab(KWS& ws, int upto) {
+  Engine& E = engine();
+  ws.v(upto);
+  if (ws.dV_cap < upto + 1) {
+    E.free(ws.dV);
+    ws.dV_cap = std::max(2 * (upto + 1), 64);
+    ws.dV = (cd**)E.alloc_bytes(sizeof(cd*) * ws.dV_cap);
+    ws.dV_n = 0;
+  }
+  if (ws.dV_n < upto + 1) {
+    HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, &ws.V[ws.dV_n], sizeof(cd*) * (upto + 1 - ws.dV_n),
+                             cudaMemcpyHostToDevice, E.st));
+    HDB_CUDA(cudaStreamSynchronize(E.st));  // pageable source: keep it alive until copied
+    ws.dV_n = upto + 1;
+  }
+}
+
+bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int* its_dev, double* rel_dev) {
+  const long long n = op->n;
+  const int cap = stop.max_iters;
+  if (!gmres_device_enabled() || op->sharded || n < coop_mgs_min() || cap < 1 || cap + kSlotH + 2 >= 900 ||
+      !(stop.rel_tol < 1.0) || !mgs_grid_fits(n))
+    return false;
+  Engine& E = engine();
+  ws.ensure(n, cap, false);
+  if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
+  if (ws.gst_cap < cap) {
+    E.free(ws.gst);
+    ws.gst = E.alloc(gm_state_elems(cap));
+    ws.gst_cap = cap;
+  }
+  if (!ws.hflags) HDB_CUDA(cudaMallocHost(&ws.hflags, 4 * sizeof(int)));
+  cd* st = ws.gst;
+  const int lay = ws.gst_cap;
+  const int* skip = gm_flags(st);
+  cd* hcol = E.dscal + kSlotH;
+  cd* flag = E.dscal + kSlotFlag;
+  ensure_vtab(ws, 0);
+  launch_dot(b, b, n, E.red, hcol, E.st);
+  launch_gm_init(hcol, st, lay, flag, E.st);
+  launch_gm_scale(b, ws.v(0), st, n, E.st);  // krylov.py:92-115 with x0 = 0
+  E.launches += 3;
+  OpCoef cs = op->c;
+  cs.skip = skip;
+  // first batch: one short of the previous solve's count (the counts of one
+  // level's CSLP solves are close), then small batches until the flag is up
+  int batch = ws.last_its > 1 ? ws.last_its - 1 : 4;
+  int j = 0;
+  for (;;) {
+    const int jend = std::min(cap, j + batch);
+    ensure_vtab(ws, jend);
+    for (; j < jend; ++j) {
+      launch_apply(cs, op->g, ws.v(j), nullptr, op->ksq, ws.v(j + 1), 0, E.st);  // krylov.py:119
+      if (launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip) != 0) {
+        const cudaError_t err = cudaGetLastError();
+        throw Error(E_CUDA, std::string("cooperative MGS launch: ") + cudaGetErrorString(err));
+      }
+      launch_gm_givens(j, hcol, st, lay, cap, stop.rel_tol, flag, E.st);
+      E.launches += 3;
+    }
+    HDB_CUDA(cudaMemcpyAsync(ws.hflags, skip, 2 * sizeof(int), cudaMemcpyDeviceToHost, E.st));
+    HDB_CUDA(cudaStreamSynchronize(E.st));
+    E.syncs++;
+    if (ws.hflags[0] || j >= cap) break;
+    batch = 3;
+  }
+  const int its = ws.hflags[1];
+  if (its == 0) {
+    HDB_CUDA(cudaMemsetAsync(x, 0, sizeof(cd) * n, E.st));  // b = 0 (or non-finite ||b||: flag raised)
+  } else {
+    launch_gm_solve(st, lay, E.st);  // krylov.py:161-168
+    launch_lincomb((const cd* const*)ws.dV, gm_y(st, lay), its, nullptr, x, n, E.st);  // 169-172
+    op->apply(x, ws.tmp);                                                               // 174
+    launch_subnorm(b, ws.tmp, n, E.red, hcol, E.st);
+    E.launches += 3;
+  }
+  launch_gm_final(hcol, st, lay, its_dev, rel_dev, flag, E.st);
+  E.launches++;
+  ws.last_its = its;
+  return true;
 }
 
 // ------------------------------------------------------ one-step FGMRES
@@ -777,6 +869,7 @@ void MadpSolver::setup() {
 }
 
 MadpSolver::~MadpSolver() {
+  for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
   if (!engine_ready()) return;
   Engine& E = engine();
   for (auto& L : lv) {
@@ -796,18 +889,63 @@ void MadpSolver::reset_report() {
   rep.cslp_iters.assign(ml + 1, {});
   rep.matvecs.assign(ml + 1, 0);
   rep.prof_ms.assign((ml + 1) * PROF_KINDS, 0.0);
+  rep.dev_ms.assign((ml + 1) * PROF_KINDS, 0.0);
+  evs.clear();
+  ev_used = 0;
   rep.prof_calls.assign((ml + 1) * PROF_KINDS, 0);
+}
+
+static bool dev_profiling() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HDB_PROFILE");
+    v = (e && *e && *e != '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+cudaEvent_t MadpSolver::ev_get() {
+  if (ev_used == ev_pool.size()) {
+    cudaEvent_t e;
+    HDB_CUDA(cudaEventCreate(&e));
+    ev_pool.push_back(e);
+  }
+  return ev_pool[ev_used++];
+}
+
+void MadpSolver::ev_resolve() {
+  if (evs.empty()) return;
+  HDB_CUDA(cudaEventSynchronize(evs.back().b));
+  for (const EvRec& r : evs) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) rep.dev_ms[r.slot] += ms;
+  }
+  evs.clear();
+  ev_used = 0;
 }
 
 namespace {
 struct ProfScope {
-  SolveReport& r;
+  MadpSolver& s;
   int slot;
   std::chrono::steady_clock::time_point t0;
-  ProfScope(SolveReport& r_, int level, int kind) : r(r_), slot(level * PROF_KINDS + kind), t0(std::chrono::steady_clock::now()) {}
+  cudaEvent_t ea = nullptr;
+  ProfScope(MadpSolver& s_, int level, int kind)
+      : s(s_), slot(level * PROF_KINDS + kind), t0(std::chrono::steady_clock::now()) {
+    if (dev_profiling()) {
+      ea = s.ev_get();
+      cudaEventRecord(ea, engine().st);
+    }
+  }
   ~ProfScope() {
-    r.prof_ms[slot] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    r.prof_calls[slot] += 1;
+    s.rep.prof_ms[slot] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    s.rep.prof_calls[slot] += 1;
+    if (ea) {
+      cudaEvent_t eb = s.ev_get();
+      cudaEventRecord(eb, engine().st);
+      s.evs.push_back({slot, ea, eb});
+      if (s.evs.size() > 20000) s.ev_resolve();
+    }
   }
 };
 }  // namespace
@@ -819,7 +957,7 @@ void MadpSolver::A(int l, const cd* u, cd* out) {
 
 // madp.py:277-299
 void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
-  ProfScope ps(rep, l, PROF_CSLP);
+  ProfScope ps(*this, l, PROF_CSLP);
   MadpLevel& L = lv[l];
   Engine& E = engine();
   if (L.cslp == CSLP_NONE) {
@@ -846,6 +984,11 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
     const int slot = reserve_count(l);
     if (L.small_cslp.try_run(rhs, out, L.cslp_stop, dcounts + slot, drel + slot)) return;
     unreserve_count(l);  // did not fit: the launch path below reports its own count
+  }
+  {
+    const int slot = reserve_count(l);
+    if (gmres_device(M, rhs, out, L.cslp_stop, L.ws_cslp, dcounts + slot, drel + slot)) return;
+    unreserve_count(l);
   }
   LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
   KReport r = fgmres(M->n, Mop, nullptr, rhs, out, L.cslp_stop, L.ws_cslp, nullptr, nullptr, M);
@@ -888,7 +1031,7 @@ void MadpSolver::flush_counts() {
 
 // madp.py:301-327  (A-DEF1, lambda = 1)
 void MadpSolver::precond(int l, const cd* v, cd* out) {
-  ProfScope ps(rep, l, PROF_ADEF);
+  ProfScope ps(*this, l, PROF_ADEF);
   Engine& E = engine();
   MadpLevel& L = lv[l];
   MadpLevel& N = lv[l + 1];
@@ -899,7 +1042,7 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   if (nxt == ml) Mop = [this, nxt](const cd* in, cd* o) { cslp_apply(nxt, in, o); };
   else Mop = [this, nxt](const cd* in, cd* o) { precond(nxt, in, o); };
   {
-    ProfScope pd(rep, nxt, PROF_DEFL);
+    ProfScope pd(*this, nxt, PROF_DEFL);
     if (N.cycle_stop.rel_tol >= 1.0 && step1_enabled()) {  // exactly one iteration: no host round trip
       // reserve the count slot BEFORE the call: nested solves inside M reserve their own
       const int slot = reserve_count(-nxt);
@@ -945,6 +1088,7 @@ void MadpSolver::solve(const cd* b, cd* x) {
       rep.outer = fgmres(n1, Aop, &Mop, b, x, outer, lv[1].ws_defl, &hook);
     }
     flush_counts();
+    ev_resolve();
   } catch (...) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -118,6 +118,10 @@ struct KWS {
   cd** hbasis = nullptr;   // pinned staging
   cd* hy = nullptr;
   int cap = 0;
+  cd* gst = nullptr;       // device-driven GMRES state (gmres_device)
+  int gst_cap = 0;
+  int* hflags = nullptr;   // pinned copy of its {done, its} flags
+  int last_its = 0;        // previous solve's count: sizes the first launch batch
   void ensure(long long n_, int cap_, bool flexible);
   cd* v(int i);
   cd* z(int i);
@@ -129,6 +133,14 @@ struct KWS {
 KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
                const std::function<void(int, double)>* hook = nullptr, const cd* x0 = nullptr,
                const LevelOp* dist = nullptr);
+
+// Unpreconditioned GMRES with zero guess driven from the device (large,
+// unsharded levels whose MGS step runs as one cooperative launch): Arnoldi
+// steps are enqueued in batches, Givens/stopping/least squares run on device
+// and the host reads one flag per batch instead of a column per step.  The
+// count and true relative residual land in *its_dev / *rel_dev.  Returns false
+// (nothing launched) when the level does not qualify.
+bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int* its_dev, double* rel_dev);
 
 // One-iteration FGMRES (StopRule tol >= 1, zero guess) entirely on device: no host
 // synchronisation; the iteration count lands in *its_dev, failures raise the
@@ -218,6 +230,7 @@ enum { PROF_DEFL = 0, PROF_CSLP = 1, PROF_ADEF = 2, PROF_KINDS = 3 };
 struct SolveReport {
   KReport outer;
   std::vector<double> prof_ms;        // (ml+1) * PROF_KINDS
+  std::vector<double> dev_ms;         // same layout, device time from CUDA events (HDB_PROFILE=1)
   std::vector<long long> prof_calls;  // same layout
   long long syncs = 0, launches = 0;
   std::vector<std::vector<int>> cycle_iters, cslp_iters;  // index = level
@@ -233,6 +246,13 @@ struct MadpSolver {
   int dcap = 0, dused = 0;
   std::vector<std::pair<int, int>> pending;  // (level, index into cslp_iters[level]) per slot
   void flush_counts();
+  // device timing (HDB_PROFILE=1): event pairs per (level, kind), resolved at the end of a solve
+  struct EvRec { int slot; cudaEvent_t a, b; };
+  std::vector<EvRec> evs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  cudaEvent_t ev_get();
+  void ev_resolve();
   int reserve_count(int level);
   void unreserve_count(int level);
   std::vector<MadpLevel> lv;  // index 1..ml

@@ -66,6 +66,7 @@ struct OpCoef {
   int uniform;           // k^2 is one constant on this level (host-checked): ucoef valid
   double ku;             // that constant
   cd ucoef[49];          // lap + mass * ku per tap, same rounded operations as the per-point form
+  const int* skip = nullptr;  // device flag: nonzero -> the launch does nothing (device-driven loops)
 };
 
 constexpr int kReduceThreads = 256;

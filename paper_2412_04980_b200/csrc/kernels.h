@@ -48,7 +48,18 @@ int resident_grid_ctas();
 int resident_vec_cap();
 void resident_set_profile(long long* dev_counters);
 // one Arnoldi step's MGS chain in a cooperative launch (large levels); 1 = does not fit
-int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st);  // 8 per-phase cycle counters or null
+int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
+                    const int* skip = nullptr);
+bool mgs_grid_fits(long long n);
+// device-driven GMRES control (launch path; kernels_resident.cu)
+long long gm_state_elems(int cap);
+void launch_gm_init(const cd* nn, cd* st, int cap, cd* flag, cudaStream_t s);
+void launch_gm_scale(const cd* b, cd* v0, const cd* st, long long n, cudaStream_t s);
+void launch_gm_givens(int j, const cd* hcol, cd* st, int cap, int maxit, double tol, cd* flag, cudaStream_t s);
+void launch_gm_solve(cd* st, int cap, cudaStream_t s);
+void launch_gm_final(const cd* nn, const cd* st, int cap, int* its_out, double* rel_out, cd* flag, cudaStream_t s);
+const int* gm_flags(const cd* st);
+cd* gm_y(cd* st, int cap);  // 8 per-phase cycle counters or null
 // ortho 0: modified Gram-Schmidt (reference order), 1: CGS2 (caps <= resident_vec_cap())
 int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
                           cd* basis, cd* Rg, cd* gpart, long long n, double tol, int cap, int* its_out,

@@ -743,6 +743,15 @@ static bool launch_grid(ResidentArgs a, cudaStream_t st) {
 }
 
 int resident_max_cap() { return kMaxCap; }
+
+long long mgs_global_tier_bytes() {
+  static long long v = -1;
+  if (v < 0) {
+    const char* e = getenv("HDB_MGS_L2_BYTES");
+    v = e ? atoll(e) : 80LL << 20;  // w up to 80 MB rides in the 126 MB L2
+  }
+  return v;
+}
 int resident_vec_cap() { return kVecCap - 1; }  // gpart stride - 1
 
 long long resident_cluster_points() {
@@ -795,10 +804,41 @@ namespace hdb {
 // and, as the launch path does after the host's stopping test, V_{j+1} =
 // w * (1/||w||) into w's buffer (harmless when the step converges).
 // Same arithmetic as k_mgs (krylov.py:121-124).
+// Bulk L2 prefetch of [p, p + n) (TMA engine, no registers or shared memory):
+// issued for V_{i+1} at the top of MGS step i, its HBM read overlaps step i's
+// dot product and grid reduction.  Threads 0..k each issue one 64 KB piece.
+__device__ __forceinline__ void prefetch_l2_span(const cd* p, long long n) {
+  constexpr long long kPiece = 4096;  // elements (64 KB)
+  const long long pieces = (n + kPiece - 1) / kPiece;
+  for (long long k = threadIdx.x; k < pieces; k += blockDim.x) {
+    const long long e0 = k * kPiece, ne = n - e0 < kPiece ? n - e0 : kPiece;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + e0), "r"((unsigned)(ne * sizeof(cd)))
+                 : "memory");
+  }
+}
+
+// w slice -> shared memory with 16 loads in flight per thread
+__device__ __forceinline__ void load_slice_smem(cd* dst, const cd* src, int cnt) {
+  for (int base = threadIdx.x; base < cnt; base += 16 * kRT) {
+    cd r[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int q = base + k * kRT;
+      r[k] = q < cnt ? src[q] : mkc(0.0, 0.0);
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int q = base + k * kRT;
+      if (q < cnt) dst[q] = r[k];
+    }
+  }
+}
+
 constexpr int kMgsPPT = 16;  // points per thread held in registers
 
 __global__ void __launch_bounds__(kRT) k_mgs_grid(cd* w, const cd* const* V, int j, long long n, cd* gpart,
-                                                  cd* hout) {
+                                                  cd* hout, const int* skip) {
+  if (skip && *skip) return;  // grid-uniform: every CTA reads the same flag
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RSmem& s = *reinterpret_cast<RSmem*>(smem_raw);
   cd* ws = reinterpret_cast<cd*>(smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);
@@ -807,9 +847,11 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid(cd* w, const cd* const* V, int
   const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
   const int cnt = (int)(p1 - p0);
   int buf = 0;
-  for (int q = t; q < cnt; q += kRT) ws[q] = w[p0 + q];
+  if (cnt > 0) prefetch_l2_span(V[0] + p0, cnt);
+  load_slice_smem(ws, w + p0, cnt);
   for (int i = 0; i <= j; ++i) {
     const cd* vi = V[i] + p0;
+    if (i < j && cnt > 0) prefetch_l2_span(V[i + 1] + p0, cnt);
     cd vr[kMgsPPT];
     cd a = mkc(0.0, 0.0);
 #pragma unroll
@@ -844,19 +886,318 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid(cd* w, const cd* const* V, int
   }
 }
 
-// returns 0 when launched, 1 when the level does not fit (caller: launch chain)
-int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st) {
+// Larger levels: this CTA's slice of w lives partly in shared memory (slots
+// k < ks of q = t + k*kRT) and partly in registers (up to kMgsReg slots), so w
+// of up to ~22k points per SM (3.3M points) stays on chip for the whole chain;
+// V_i is read from HBM once for the dot and re-read from L2 for the update.
+constexpr int kMgsReg = 16;
+
+struct MgsSmem {
+  cd warp[kRT / 32];
+  cd bcast[2];
+};
+
+__device__ __forceinline__ cd grid_reduce_small(cd v, MgsSmem& s, int& buf, cd* gpart, cg::grid_group& gr) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, P = gridDim.x;
+  v = warp_sum_c(v);
+  if (lane == 0) s.warp[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    cd t = lane < kRT / 32 ? s.warp[lane] : mkc(0.0, 0.0);
+    t = warp_sum_c(t);
+    if (lane == 0) __stcg(&gpart[((long long)buf * P + blockIdx.x) * kVecCap], t);
+  }
+  gr.sync();
+  if (wid == 0) {
+    cd q = mkc(0.0, 0.0);
+    for (int r = lane; r < P; r += 32) {
+      const cd z = __ldcg(&gpart[((long long)buf * P + r) * kVecCap]);
+      q.x += z.x;
+      q.y += z.y;
+    }
+    q = warp_sum_c(q);
+    if (lane == 0) s.bcast[buf] = q;
+  }
+  __syncthreads();
+  const cd r = s.bcast[buf];
+  buf ^= 1;
+  return r;
+}
+
+__global__ void __launch_bounds__(kRT) k_mgs_grid2(cd* w, const cd* const* V, int j, long long n, cd* gpart,
+                                                   cd* hout, int ks, const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MgsSmem& s = *reinterpret_cast<MgsSmem*>(smem_raw);
+  cd* ws = reinterpret_cast<cd*>(smem_raw + ((sizeof(MgsSmem) + 15) / 16) * 16);
+  cg::grid_group gr = cg::this_grid();
+  const int P = gridDim.x, rank = blockIdx.x, t = threadIdx.x;
+  const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
+  const int cnt = (int)(p1 - p0);
+  int buf = 0;
+  cd wr[kMgsReg];
+  const cd* wg = w + p0;
+  // (no L2 prefetch of V here: it would evict the L2-resident tier of w)
+  load_slice_smem(ws, wg, min(cnt, ks * kRT));  // slot k of thread t = element t + k*kRT
+#pragma unroll
+  for (int k = 0; k < kMgsReg; ++k) {
+    const int q = t + (ks + k) * kRT;
+    wr[k] = q < cnt ? wg[q] : mkc(0.0, 0.0);
+  }
+  const int qg = t + (ks + kMgsReg) * kRT;  // first point of the global (L2-resident) tier
+  cd* wgl = w + p0;
+  for (int i = 0; i <= j; ++i) {
+    const cd* vi = V[i] + p0;
+    cd a = mkc(0.0, 0.0);
+    for (int k = 0; k < ks; ++k) {
+      const int q = t + k * kRT;
+      if (q < cnt) a = c_conjmul_acc(a, vi[q], ws[k * kRT + t]);
+    }
+#pragma unroll
+    for (int k = 0; k < kMgsReg; ++k) {
+      const int q = t + (ks + k) * kRT;
+      if (q < cnt) a = c_conjmul_acc(a, vi[q], wr[k]);
+    }
+    for (int q = qg; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], wgl[q]);
+    const cd h = grid_reduce_small(a, s, buf, gpart, gr);
+    if (rank == 0 && t == 0) hout[i] = h;
+    for (int k = 0; k < ks; ++k) {
+      const int q = t + k * kRT;
+      if (q < cnt) ws[k * kRT + t] = c_sub(ws[k * kRT + t], c_mul_np(h, vi[q]));
+    }
+#pragma unroll
+    for (int k = 0; k < kMgsReg; ++k) {
+      const int q = t + (ks + k) * kRT;
+      if (q < cnt) wr[k] = c_sub(wr[k], c_mul_np(h, vi[q]));
+    }
+    for (int q = qg; q < cnt; q += kRT) wgl[q] = c_sub(wgl[q], c_mul_np(h, vi[q]));
+  }
+  cd a = mkc(0.0, 0.0);
+  for (int k = 0; k < ks; ++k)
+    if (t + k * kRT < cnt) a = c_conjmul_acc(a, ws[k * kRT + t], ws[k * kRT + t]);
+#pragma unroll
+  for (int k = 0; k < kMgsReg; ++k)
+    if (t + (ks + k) * kRT < cnt) a = c_conjmul_acc(a, wr[k], wr[k]);
+  for (int q = qg; q < cnt; q += kRT) a = c_conjmul_acc(a, wgl[q], wgl[q]);
+  const cd nn = grid_reduce_small(a, s, buf, gpart, gr);
+  if (rank == 0 && t == 0) hout[j + 1] = nn;
+  const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
+  const double inv = 1.0 / hn;
+  cd* wo = w + p0;
+  for (int k = 0; k < ks; ++k) {
+    const int q = t + k * kRT;
+    if (q < cnt) {
+      const cd v = ws[k * kRT + t];
+      wo[q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMgsReg; ++k) {
+    const int q = t + (ks + k) * kRT;
+    if (q < cnt) {
+      const cd v = wr[k];
+      wo[q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+    }
+  }
+  if (hn > 0.0)
+    for (int q = qg; q < cnt; q += kRT) {
+      const cd v = wo[q];
+      wo[q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+    }
+}
+
+// Launch plan of the cooperative MGS step for length n: 1 = k_mgs_grid (w in
+// registers + shared memory), 2 = k_mgs_grid2 with `ks` shared-memory slots,
+// 0 = does not fit (caller: launch chain).
+static int mgs_grid_plan(long long n, long long& ks_out) {
   init_limits();
   const long long chunk = (n + g_grid - 1) / g_grid;
   const size_t sm = smem_for(chunk, false);
-  if (sm > g_smem_optin || chunk > (long long)kMgsPPT * kRT * 2) return 1;
+  if (sm <= g_smem_optin && chunk <= (long long)kMgsPPT * kRT * 2) return 1;
+  // hybrid shared-memory + register slice of w; beyond those the slice stays in
+  // w itself (L2-resident up to mgs_global_tier_bytes(); larger levels keep
+  // the launch chain)
+  const size_t head = ((sizeof(MgsSmem) + 15) / 16) * 16;
+  const long long slots = (chunk + kRT - 1) / kRT;
+  const long long ks_max = (long long)((g_smem_optin - head) / (sizeof(cd) * kRT));
+  if (n * (long long)sizeof(cd) > mgs_global_tier_bytes() && std::max(0LL, slots - kMgsReg) > ks_max) return 0;
+  ks_out = std::min(std::max(0LL, slots - kMgsReg), ks_max);
+  return 2;
+}
+
+bool mgs_grid_fits(long long n) {
+  long long ks = 0;
+  return mgs_grid_plan(n, ks) != 0;
+}
+
+// returns 0 when launched, 1 when the level does not fit (caller: launch chain)
+int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
+                    const int* skip) {
+  long long ks = 0;
+  const int plan = mgs_grid_plan(n, ks);
+  if (plan == 0) return 1;
+  if (plan == 2) {
+    const size_t head = ((sizeof(MgsSmem) + 15) / 16) * 16;
+    const size_t sm2 = head + (size_t)ks * kRT * sizeof(cd);
+    static size_t configured2 = 0;
+    if (sm2 > configured2) {
+      cudaFuncSetAttribute(k_mgs_grid2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      configured2 = sm2;
+    }
+    int ksi = (int)ks;
+    void* args2[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &ksi, (void*)&skip};
+    return cudaLaunchCooperativeKernel((void*)k_mgs_grid2, dim3(g_grid), dim3(kRT), args2, sm2, st) == cudaSuccess ? 0 : 1;
+  }
+  const size_t sm = smem_for((n + g_grid - 1) / g_grid, false);
   static size_t configured = 0;
   if (sm > configured) {
     cudaFuncSetAttribute(k_mgs_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     configured = sm;
   }
-  void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout};
+  void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, (void*)&skip};
   return cudaLaunchCooperativeKernel((void*)k_mgs_grid, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
 }
+
+// ---------------------------------------------------------------------------
+// Device-driven GMRES control for the launch path (large levels): the host
+// enqueues Arnoldi steps in batches without reading anything back; the Givens
+// update, the stopping test and the least-squares solve run in single-thread
+// kernels with the resident kernel's arithmetic (krylov.py:126-168), and a
+// `done` flag makes every later launch of the batch return at once.
+// State layout (cd units): [0] (bnorm, 1/bnorm); [1] int flags {done, its,
+// status, -}; then g[cap+1], sn[cap], cs[cap] (.x), R[cap(cap+1)/2], y[cap].
+namespace {
+struct GmView {
+  cd* hdr;
+  int* fl;
+  cd *g, *sn, *cs, *R, *y;
+  __device__ GmView(cd* st, int cap) {
+    hdr = st;
+    fl = reinterpret_cast<int*>(st + 1);
+    g = st + 2;
+    sn = g + cap + 1;
+    cs = sn + cap;
+    R = cs + cap;
+    y = R + (long long)cap * (cap + 1) / 2;
+  }
+};
+}  // namespace
+
+long long gm_state_elems(int cap) { return 2 + (cap + 1) + 2LL * cap + (long long)cap * (cap + 1) / 2 + cap; }
+
+__global__ void k_gm_init(const cd* nn, cd* st, int cap, cd* flag) {
+  GmView v(st, cap);
+  const double bnorm = sqrt(fmax(nn->x, 0.0));
+  v.hdr[0] = mkc(bnorm, 1.0 / bnorm);
+  v.fl[1] = 0;
+  v.fl[2] = 0;
+  v.g[0] = mkc(bnorm, 0.0);
+  if (!isfinite(bnorm)) {
+    flag->x = 2.0;
+    v.fl[2] = 2;
+  }
+  v.fl[0] = (bnorm == 0.0 || !isfinite(bnorm)) ? 1 : 0;  // krylov.py:96-97: b = 0 -> x = 0
+}
+
+// V0 = b * (1/beta)  (zero initial guess: r0 = b, beta = ||b||)
+__global__ void k_gm_scale(const cd* __restrict__ b, cd* __restrict__ v0, const cd* st, long long n) {
+  if (reinterpret_cast<const int*>(st + 1)[0]) return;
+  const double inv = st[0].y;
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const cd x = b[p];
+    v0[p] = mkc(__dmul_rn(x.x, inv), __dmul_rn(x.y, inv));
+  }
+}
+
+// rotations of step j (krylov.py:126-151) from the Hessenberg column the MGS
+// step left in hcol[0..j] and ||w||^2 in hcol[j+1].x; stopping test
+__global__ void k_gm_givens(int j, const cd* hcol, cd* st, int cap, int maxit, double tol, cd* flag) {
+  GmView v(st, cap);
+  if (v.fl[0]) return;
+  const double bnorm = v.hdr[0].x;
+  const double hn = sqrt(fmax(hcol[j + 1].x, 0.0));
+  cd* Rc = v.R + (long long)j * (j + 1) / 2;  // column j: R[0..j]
+  bool finite = isfinite(hn);
+  for (int i = 0; i <= j; ++i) {
+    Rc[i] = hcol[i];
+    finite &= isfinite(hcol[i].x) && isfinite(hcol[i].y);
+  }
+  for (int i = 0; i < j; ++i) {  // rotation i touches entries i, i+1 <= j
+    const cd ci = Rc[i], cn = Rc[i + 1];
+    const double c = v.cs[i].x;
+    const cd sc = cmul_(v.sn[i], cn);
+    const cd nb = cmul_(mkc(-v.sn[i].x, v.sn[i].y), ci);
+    Rc[i] = mkc(c * ci.x + sc.x, c * ci.y + sc.y);
+    Rc[i + 1] = mkc(nb.x + c * cn.x, nb.y + c * cn.y);
+  }
+  const cd h1 = Rc[j], h2 = mkc(hn, 0.0);
+  double c;
+  cd sn;
+  const double a1 = cabs_(h1), a2 = cabs_(h2);
+  if (a2 == 0.0) { c = 1.0; sn = mkc(0.0, 0.0); }
+  else if (a1 == 0.0) { c = 0.0; sn = mkc(1.0, 0.0); }
+  else {
+    const double tt = hypot(a1, a2);
+    c = a1 / tt;
+    const cd q = cmul_(mkc(h1.x / a1, h1.y / a1), mkc(h2.x, -h2.y));
+    sn = mkc(q.x / tt, q.y / tt);
+  }
+  v.cs[j] = mkc(c, 0.0);
+  v.sn[j] = sn;
+  const cd sh = cmul_(sn, h2);
+  Rc[j] = mkc(c * h1.x + sh.x, c * h1.y + sh.y);
+  const cd gj = v.g[j];
+  v.g[j + 1] = cmul_(mkc(-sn.x, sn.y), gj);
+  v.g[j] = mkc(c * gj.x, c * gj.y);
+  const double rel = cabs_(v.g[j + 1]) / bnorm;
+  v.fl[1] = j + 1;
+  if (!finite) {
+    flag->x = 2.0;
+    v.fl[2] = 2;
+    v.fl[0] = 1;
+  } else if (hn < 1e-30 || rel <= tol || j + 1 >= maxit) {
+    v.fl[0] = 1;
+  }
+}
+
+// least squares R y = g (krylov.py:161-168), its = flags[1]
+__global__ void k_gm_solve(cd* st, int cap) {
+  GmView v(st, cap);
+  const int its = v.fl[1];
+  for (int i = its - 1; i >= 0; --i) {
+    cd accy = v.g[i];
+    for (int k = i + 1; k < its; ++k) {
+      const cd pr = cmul_(v.R[(long long)k * (k + 1) / 2 + i], v.y[k]);
+      accy = mkc(accy.x - pr.x, accy.y - pr.y);
+    }
+    v.y[i] = cdiv_(accy, v.R[(long long)i * (i + 1) / 2 + i]);
+  }
+}
+
+// explicit true residual norm (krylov.py:174) -> the solve's count / relres slots
+__global__ void k_gm_final(const cd* nn, const cd* st, int cap, int* its_out, double* rel_out, cd* flag) {
+  const int* fl = reinterpret_cast<const int*>(st + 1);
+  const double bnorm = st[0].x;
+  const double fin = bnorm > 0.0 ? sqrt(fmax(nn->x, 0.0)) / bnorm : 0.0;
+  if (its_out) *its_out = fl[1];
+  if (rel_out) *rel_out = fin;
+  if (!isfinite(fin)) flag->x = 2.0;
+  (void)cap;
+}
+
+void launch_gm_init(const cd* nn, cd* st, int cap, cd* flag, cudaStream_t s) { k_gm_init<<<1, 1, 0, s>>>(nn, st, cap, flag); }
+void launch_gm_scale(const cd* b, cd* v0, const cd* st, long long n, cudaStream_t s) {
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 4 * 148);
+  k_gm_scale<<<blocks, 256, 0, s>>>(b, v0, st, n);
+}
+void launch_gm_givens(int j, const cd* hcol, cd* st, int cap, int maxit, double tol, cd* flag, cudaStream_t s) {
+  k_gm_givens<<<1, 1, 0, s>>>(j, hcol, st, cap, maxit, tol, flag);
+}
+void launch_gm_solve(cd* st, int cap, cudaStream_t s) { k_gm_solve<<<1, 1, 0, s>>>(st, cap); }
+void launch_gm_final(const cd* nn, const cd* st, int cap, int* its_out, double* rel_out, cd* flag, cudaStream_t s) {
+  k_gm_final<<<1, 1, 0, s>>>(nn, st, cap, its_out, rel_out, flag);
+}
+const int* gm_flags(const cd* st) { return reinterpret_cast<const int*>(st + 1); }
+cd* gm_y(cd* st, int cap) { return st + 2 + (cap + 1) + 2LL * cap + (long long)cap * (cap + 1) / 2; }
 
 }  // namespace hdb

@@ -4,6 +4,8 @@
 // Reference: _kernels.py:14-68, operators.py:130-178, mg.py:88-102.
 // Memory-bound: 40 B/pt algorithmic for an apply (u 16 + k^2 8 + out 16),
 // 56 B/pt for the residual / A-DEF1 form (+ b 16), 56 B/pt per Jacobi sweep.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "stencil.cuh"
 
@@ -20,6 +22,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_r1(const cd* __restrict__ u, const cd* __restrict__ b,
                                             const double* __restrict__ k, cd* __restrict__ out,
                                             Geom g, OpCoef c, double omega) {
+  if (c.skip && *c.skip) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;  // local row
   if (i >= g.nx || j >= g.ny) return;
@@ -61,9 +64,10 @@ __global__ void __launch_bounds__(256) k_r1(const cd* __restrict__ u, const cd* 
 constexpr int SX = 32, SY = 4, RB = 16;  // block 32x4 threads, 16 rows per thread
 
 template <int MODE>
-__global__ void __launch_bounds__(SX * SY, 8) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
+__global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
                                                  const double* __restrict__ k, cd* __restrict__ out, Geom g,
                                                  OpCoef c, double omega) {
+  if (c.skip && *c.skip) return;
   const int i = blockIdx.x * SX + threadIdx.x;
   const int jbeg = (blockIdx.y * SY + threadIdx.y) * RB;  // local row
   const int gi0 = blockIdx.x * SX, gj0 = g.row0 + blockIdx.y * SY * RB;
@@ -125,28 +129,43 @@ __global__ void __launch_bounds__(SX * SY, 8) k_r1s(const cd* __restrict__ u, co
     }
     return;
   }
-  cd s_ = up[-nx], c_ = up[0];
-#pragma unroll 2
+  // software pipeline: row r+1's loads are issued before row r is computed
+  const double* kp = k + (long long)jbeg * nx + i;
+  const cd* bp = b ? b + (long long)jbeg * nx + i : nullptr;
+  cd* op = out + (long long)jbeg * nx + i;
+  cd s_ = up[-nx], c_ = up[0], n_ = up[nx];
+  double kc = kp[0];
+  cd bc = (MODE != 0) ? bp[0] : mkc(0.0, 0.0);
+  cd wl = (lane == 0) ? up[-1] : mkc(0.0, 0.0), el = (lane == SX - 1) ? up[1] : mkc(0.0, 0.0);
+#pragma unroll (MODE == 2 ? 2 : 4)
   for (int r = 0; r < RB; ++r) {
     const long long o = (long long)r * nx;
-    const cd n_ = up[o + nx];
+    // prefetch row r+1 (its north row r+2, k, b, warp-edge neighbours)
+    const bool more = r + 1 < RB;
+    cd n2 = mkc(0.0, 0.0), b2 = mkc(0.0, 0.0), wl2 = mkc(0.0, 0.0), el2 = mkc(0.0, 0.0);
+    double k2 = 0.0;
+    if (more) {
+      n2 = up[o + 2 * nx];
+      k2 = kp[o + nx];
+      if (MODE != 0) b2 = bp[o + nx];
+      if (lane == 0) wl2 = up[o + nx - 1];
+      if (lane == SX - 1) el2 = up[o + nx + 1];
+    }
     cd w_, e_;
     w_.x = __shfl_up_sync(0xffffffffu, c_.x, 1);
     w_.y = __shfl_up_sync(0xffffffffu, c_.y, 1);
     e_.x = __shfl_down_sync(0xffffffffu, c_.x, 1);
     e_.y = __shfl_down_sync(0xffffffffu, c_.y, 1);
-    if (lane == 0) w_ = up[o - 1];
-    if (lane == SX - 1) e_ = up[o + 1];
-    const long long pp = (long long)(jbeg + r) * nx + i;
-    const cd Au = five_point(c.s, c.mc, k[pp], c_, w_, e_, s_, n_);
+    if (lane == 0) w_ = wl;
+    if (lane == SX - 1) e_ = el;
+    const cd Au = five_point(c.s, c.mc, kc, c_, w_, e_, s_, n_);
     if (MODE == 0) {
-      out[pp] = Au;
+      op[o] = Au;
     } else {
-      const cd r1 = c_sub(b[pp], Au);
+      const cd r1 = c_sub(bc, Au);
       if (MODE == 1) {
-        out[pp] = r1;
+        op[o] = r1;
       } else {
-        const double kc = k[pp];
         const double dr = __dadd_rn(4.0 * c.s, __dmul_rn(c.mc.x, kc)), di = __dmul_rn(c.mc.y, kc);
         cd d;
         if (fabs(dr) >= fabs(di)) {
@@ -156,11 +175,16 @@ __global__ void __launch_bounds__(SX * SY, 8) k_r1s(const cd* __restrict__ u, co
           const double rat = __ddiv_rn(dr, di), scl = __ddiv_rn(1.0, __dadd_rn(di, __dmul_rn(dr, rat)));
           d = mkc(__dmul_rn(rat, scl), -scl);
         }
-        out[pp] = c_add(c_, c_mul(c_scale(omega, d), r1));
+        op[o] = c_add(c_, c_mul(c_scale(omega, d), r1));
       }
     }
     s_ = c_;
     c_ = n_;
+    n_ = n2;
+    kc = k2;
+    bc = b2;
+    wl = wl2;
+    el = el2;
   }
 }
 
@@ -176,6 +200,7 @@ template <int R, int MODE>
 __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const cd* __restrict__ b,
                                                const double* __restrict__ k, cd* __restrict__ out,
                                                Geom g, OpCoef c) {
+  if (c.skip && *c.skip) return;
   constexpr int W = TX + 2 * R, H = TY + 2 * R, N = 2 * R + 1;
   __shared__ cd su[H][W];
   __shared__ double sk[H][W];
@@ -223,6 +248,108 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
   out[p] = MODE == 0 ? acc : c_sub(b[p], acc);
 }
 
+// Register-blocked form for large grids: each thread owns RYB vertically
+// adjacent outputs of one column and streams the input window rows top to
+// bottom, so every shared-memory (u, k^2) tap value is read once per thread
+// instead of once per output.  Output row r receives tap (a, bb) from input row
+// r + a; rows arrive in increasing a and, within a row, increasing bb, so each
+// output still accumulates in the reference's row-major tap order.
+constexpr int TYB = 4, RYB = 8, THB = TYB * RYB;
+
+// Per-tap coefficients are staged in shared memory and read through a volatile
+// pointer at each use (warp-broadcast loads); held in registers across the
+// unrolled window they would cost 2 * 3 * 25 registers and halve occupancy.
+// Used for radius 2 (k_rg at ~55% of either roofline); k_rg<3> already runs at
+// ~80% of the FP64 issue rate, which blocking cannot improve.
+struct TapCoef {
+  double lap, mx, my;
+};
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(TX * TYB) k_rgb(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                 const double* __restrict__ k, cd* __restrict__ out,
+                                                 Geom g, OpCoef c) {
+  if (c.skip && *c.skip) return;
+  constexpr int W = TX + 2 * R, H = THB + 2 * R, N = 2 * R + 1;
+  __shared__ cd su[H][W];
+  __shared__ double sk[H][W];
+  __shared__ TapCoef sc[N * N];
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * THB;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  const bool fast = c.uniform && i0 >= R && i0 + TX + R <= g.nx && g.row0 + j0 >= R &&
+                    g.row0 + j0 + THB + R <= g.nyg;
+  for (int t = tid; t < N * N; t += TX * TYB) {
+    if (fast) sc[t] = TapCoef{c.ucoef[t].x, c.ucoef[t].y, 0.0};
+    else sc[t] = TapCoef{c.lap[t], c.mass[t].x, c.mass[t].y};
+  }
+  if (fast) {
+    for (int t = tid; t < H * W; t += TX * TYB) {
+      const int ty = t / W, tx = t % W;
+      su[ty][tx] = U(u, g, g.row0 + j0 + ty - R, i0 + tx - R);
+    }
+  } else {
+    for (int t = tid; t < H * W; t += TX * TYB) {
+      const int ty = t / W, tx = t % W;
+      const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+      su[ty][tx] = upad(u, k, g, c, gj, gi);
+      sk[ty][tx] = kpad(k, g, c, gj, gi);
+    }
+  }
+  __syncthreads();
+  const volatile TapCoef* vc = sc;
+  const int tx = threadIdx.x, jr = threadIdx.y * RYB;
+  cd acc[RYB];
+#pragma unroll
+  for (int r = 0; r < RYB; ++r) acc[r] = mkc(0.0, 0.0);
+  if (fast) {
+#pragma unroll
+    for (int t = 0; t < RYB + 2 * R; ++t) {
+#pragma unroll
+      for (int bb = 0; bb < N; ++bb) {
+        const cd uv = su[jr + t][tx + bb];
+#pragma unroll
+        for (int r = 0; r < RYB; ++r) {
+          const int a = t - r;
+          if (a < 0 || a >= N) continue;
+          const cd coef = mkc(vc[a * N + bb].lap, vc[a * N + bb].mx);
+          acc[r] = c_add(acc[r], c_mul(coef, uv));
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < RYB + 2 * R; ++t) {
+#pragma unroll
+      for (int bb = 0; bb < N; ++bb) {
+        const cd uv = su[jr + t][tx + bb];
+        const double kp = sk[jr + t][tx + bb];
+#pragma unroll
+        for (int r = 0; r < RYB; ++r) {
+          const int a = t - r;
+          if (a < 0 || a >= N) continue;
+          const double lap = vc[a * N + bb].lap, mx = vc[a * N + bb].mx, my = vc[a * N + bb].my;
+          const cd coef = mkc(__dadd_rn(lap, __dmul_rn(mx, kp)), __dmul_rn(my, kp));
+          acc[r] = c_add(acc[r], c_mul(coef, uv));
+        }
+      }
+    }
+  }
+  const int i = i0 + tx;
+  if (i >= g.nx) return;
+#pragma unroll
+  for (int r = 0; r < RYB; ++r) {
+    const int j = j0 + jr + r;
+    if (j >= g.ny) break;
+    const long long p = (long long)j * g.nx + i;
+    if (pinned(g, c, j + g.row0, i)) {
+      const cd uc = su[jr + r + R][tx + R];
+      out[p] = MODE == 0 ? uc : c_sub(b[p], uc);
+    } else {
+      out[p] = MODE == 0 ? acc[r] : c_sub(b[p], acc[r]);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------
 static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny + 7) / 8); }
 static inline dim3 grid_r1s(const Geom& g) { return dim3((g.nx + SX - 1) / SX, (g.ny + SY * RB - 1) / (SY * RB)); }
@@ -240,6 +367,16 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
     const dim3 blk(32, 8), grd = grid_r1(g);
     if (mode == 0) k_r1<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
     else k_r1<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+    return;
+  }
+  static const bool blocked = [] {
+    const char* e = getenv("HDB_RG_BLOCKED");
+    return !e || atoi(e) != 0;
+  }();
+  if (blocked && c.radius == 2 && g.nx >= 256 && g.ny >= 256) {
+    const dim3 blk(TX, TYB), grd((g.nx + TX - 1) / TX, (g.ny + THB - 1) / THB);
+    if (mode == 0) k_rgb<2, 0><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+    else k_rgb<2, 1><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
     return;
   }
   const dim3 blk(TX, TY), grd((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);

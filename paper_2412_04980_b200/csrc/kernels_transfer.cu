@@ -11,6 +11,8 @@
 // Slab form (TGeom): fine rows [f_row0, f_row0 + f_ny) of a grid with nfy_g
 // rows are local; rows just outside are halo rows (filled by the exchange) or,
 // at the physical edges, zero extension.  Coarse rows likewise.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "hdb_common.cuh"
 
@@ -97,6 +99,76 @@ __global__ void __launch_bounds__(256) k_restrict2(const cd* __restrict__ f, cd*
   c[(long long)cy * t.ncx + cx] = zrow(zero_mask, cx, cyg, t) ? mkc(0.0, 0.0) : mkc(ar, ai);
   if (cy + 1 < t.c_ny)
     c[(long long)(cy + 1) * t.ncx + cx] = zrow(zero_mask, cx, cyg + 1, t) ? mkc(0.0, 0.0) : mkc(br, bi);
+}
+
+// Strip form for large grids: one thread per coarse column, RRB coarse rows
+// per thread.  Fine rows are streamed top to bottom; each is read once per warp
+// as a coalesced even/odd pair (fine 2cx, 2cx+1) and the (2cx-2, 2cx-1, 2cx+2)
+// neighbours come from warp shuffles.  A fine row y contributes to the coarse
+// rows with b = y - 2cy + 2 in [0, 4] in increasing-b order, so every coarse
+// sum is accumulated in the reference's (b, a) order (bit-identical).
+constexpr int RSX = 32, RSY = 4, RRB = 8;
+__host__ __device__ constexpr double kw5(int i) { return i == 0 || i == 4 ? 1.0 : (i == 2 ? 6.0 : 4.0); }
+__host__ __device__ constexpr double kW16(int i) { return kw5(i) / 16; }
+
+__global__ void __launch_bounds__(RSX * RSY) k_restrict_s(const cd* __restrict__ f, cd* __restrict__ c, TGeom t,
+                                                          int zero_mask) {
+  const int lane = threadIdx.x;
+  const int cx = blockIdx.x * RSX + lane;
+  const int cy0 = (blockIdx.y * RSY + threadIdx.y) * RRB;  // local coarse row (warp-uniform)
+  if (cy0 >= t.c_ny) return;
+  const int ncy = min(RRB, t.c_ny - cy0);
+  const int cyg0 = cy0 + t.c_row0;
+  const int x0 = 2 * cx;
+  bool va[5];
+#pragma unroll
+  for (int a = 0; a < 5; ++a) va[a] = (x0 + a - 2 >= 0) && (x0 + a - 2 < t.nfx);
+  double ar[RRB], ai[RRB];
+#pragma unroll
+  for (int k = 0; k < RRB; ++k) ar[k] = ai[k] = 0.0;
+#pragma unroll
+  for (int r = 0; r < 2 * RRB + 3; ++r) {
+    const int y = 2 * cyg0 - 2 + r;
+    if (r <= 2 * (ncy - 1) + 4 && y >= 0 && y < t.nfy_g) {  // warp-uniform
+      const cd* row = f + (long long)(y - t.f_row0) * t.nfx;
+      const cd E = (x0 < t.nfx) ? row[x0] : mkc(0.0, 0.0);
+      const cd O = (x0 + 1 < t.nfx) ? row[x0 + 1] : mkc(0.0, 0.0);
+      cd v[5];
+      v[2] = E;
+      v[3] = O;
+      v[0].x = __shfl_up_sync(0xffffffffu, E.x, 1);
+      v[0].y = __shfl_up_sync(0xffffffffu, E.y, 1);
+      v[1].x = __shfl_up_sync(0xffffffffu, O.x, 1);
+      v[1].y = __shfl_up_sync(0xffffffffu, O.y, 1);
+      v[4].x = __shfl_down_sync(0xffffffffu, E.x, 1);
+      v[4].y = __shfl_down_sync(0xffffffffu, E.y, 1);
+      if (lane == 0) {
+        v[0] = va[0] ? row[x0 - 2] : mkc(0.0, 0.0);
+        v[1] = va[1] ? row[x0 - 1] : mkc(0.0, 0.0);
+      }
+      if (lane == RSX - 1) v[4] = va[4] ? row[x0 + 2] : mkc(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < RRB; ++k) {
+        const int b = r - 2 * k;
+        if (b < 0 || b > 4) continue;  // compile-time
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+          if (!va[a]) continue;
+          const double w = kW16(b) * kW16(a);
+          ar[k] = __dadd_rn(ar[k], __dmul_rn(w, v[a].x));
+          ai[k] = __dadd_rn(ai[k], __dmul_rn(w, v[a].y));
+        }
+      }
+    }
+    // coarse row k is complete after its b = 4 fine row (r = 2k + 4)
+    if (r >= 4 && ((r - 4) & 1) == 0) {
+      const int k = (r - 4) / 2;
+      if (k < ncy && cx < t.ncx) {
+        const int cyg = cyg0 + k;
+        c[(long long)(cy0 + k) * t.ncx + cx] = zrow(zero_mask, cx, cyg, t) ? mkc(0.0, 0.0) : mkc(ar[k], ai[k]);
+      }
+    }
+  }
 }
 
 // fine point (y, x) gathers (w8_b w8_a) coarse((y+2-b)/2, (x+2-a)/2) over the
@@ -193,7 +265,16 @@ TGeom full_tgeom(int nfx, int nfy) {
 }
 
 void launch_restrict(const cd* fine, cd* coarse, const TGeom& t, int zero_mask, cudaStream_t st) {
-  if (t.ncx >= 64 && t.c_ny >= 64) {
+  static const int mode = [] {
+    const char* e = getenv("HDB_RESTRICT");
+    return e ? atoi(e) : 2;
+  }();
+  if (mode == 2 && t.ncx >= 256 && t.c_ny >= 256) {
+    const dim3 blk(RSX, RSY), grd((t.ncx + RSX - 1) / RSX, (t.c_ny + RSY * RRB - 1) / (RSY * RRB));
+    k_restrict_s<<<grd, blk, 0, st>>>(fine, coarse, t, zero_mask);
+    return;
+  }
+  if (mode >= 1 && t.ncx >= 64 && t.c_ny >= 64) {
     const dim3 blk(32, 8), grd((t.ncx + 31) / 32, ((t.c_ny + 1) / 2 + 7) / 8);
     k_restrict2<<<grd, blk, 0, st>>>(fine, coarse, t, zero_mask);
     return;

@@ -60,7 +60,7 @@ def test_operator_heterogeneous_and_mixed_bc_bitexact():
         np.testing.assert_array_equal(op.apply(g[f"mixed_L{l}_M_u"]), g[f"mixed_L{l}_M_v"])
 
 
-@pytest.mark.parametrize("shape", [(129, 129), (65, 257), (257, 33)])
+@pytest.mark.parametrize("shape", [(129, 129), (65, 257), (257, 33), (300, 270), (289, 513)])
 @pytest.mark.parametrize("level", [1, 2, 3])
 def test_operator_bitexact_vs_oracle_larger(shape, level):
     rng = _rng(level)
@@ -76,6 +76,26 @@ def test_operator_bitexact_vs_oracle_larger(shape, level):
     u = _rand(rng, shape)
     np.testing.assert_array_equal(op.apply(u), ref.apply(u))
     b = _rand(rng, shape)
+    np.testing.assert_array_equal(op.residual(b, u), b - ref.apply(u))
+
+
+@pytest.mark.parametrize("level", [2, 3])
+@pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
+def test_operator_uniform_k_large_bitexact(level, bnd):
+    """Constant-k^2 level on a grid large enough for the register-blocked tile
+    kernel (interior tiles take the precomputed-coefficient fast path)."""
+    rng = _rng(40 + level)
+    ny, nx = 321, 290
+    ksq = np.full((ny, nx), 523.25)
+    lv = hdb.level_kernels(level)
+    op = hdb.LevelOperator(level, nx, ny, 1.0 / 96, ksq, bnd, lv[0], lv[1], shift=complex(1.0, 0.5),
+                           level_scale=4.0 ** (level - 1))
+    lt, ld, mt, md, _ = oracle.level_kernels(level)
+    ref = oracle.CpuLevelOp(nx, ny, 1.0 / 96, ksq, bnd, lt, ld, mt, md, shift=complex(1.0, 0.5),
+                            level_scale=4.0 ** (level - 1))
+    u = _rand(rng, (ny, nx))
+    np.testing.assert_array_equal(op.apply(u), ref.apply(u))
+    b = _rand(rng, (ny, nx))
     np.testing.assert_array_equal(op.residual(b, u), b - ref.apply(u))
 
 
@@ -295,23 +315,29 @@ def test_solve_device_tensor_roundtrip():
 
 
 def test_device_resident_and_launch_paths_agree():
-    """HDB_SMALL_N=0 forces the launch-driven Krylov path on every level; both
-    engines must give the same counts and histories to rounding."""
+    """HDB_SMALL_N=0 forces the launch-driven Krylov path on every level (with
+    the MGS chain, the cooperative MGS step, or the device-driven GMRES loop);
+    every engine must give the same counts and histories to rounding."""
     import subprocess
     import sys
     code = ("import json,sys; sys.path.insert(0,'.'); import paper_2412_04980_b200 as h;"
             "p=h.wedge_problem(f=20.0,nx=145,ml=4); s=h.MadpSolver(p.hierarchy,h.preset('MADP',p.hierarchy));"
             "u,r=s.solve(p.rhs); print(json.dumps([r.outer_iterations,r.residual_history,r.cslp_iters[4]]))")
     outs = []
-    for env in ({"HDB_SMALL_N": "0", "HDB_GRID_N": "0"}, {}):
+    launch = {"HDB_SMALL_N": "0", "HDB_GRID_N": "0"}
+    for env in (launch,                                                   # host-driven, MGS launch chain
+                dict(launch, HDB_COOP_MGS_N="300", HDB_GMRES_DEV="0"),   # host-driven, cooperative MGS
+                dict(launch, HDB_COOP_MGS_N="300"),                      # device-driven GMRES
+                {}):                                                     # device-resident kernels
         import os
         e = dict(os.environ, **env)
         r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=e, cwd=ROOT_DIR)
         assert r.returncode == 0, r.stderr
         outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
-    (i0, h0, c0), (i1, h1, c1) = outs
-    assert i0 == i1 and c0 == c1
-    assert np.abs(np.array(h0) - np.array(h1)).max() <= 1e-12
+    i0, h0, c0 = outs[0]
+    for i1, h1, c1 in outs[1:]:
+        assert i0 == i1 and c0 == c1
+        assert np.abs(np.array(h0) - np.array(h1)).max() <= 1e-12
 
 
 ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
