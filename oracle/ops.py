@@ -20,6 +20,46 @@ from .grid import DIRICHLET
 
 _njit = nb.njit(cache=False, nogil=True)
 
+# Row-slab worker pool for the stencil loops (the reference runs its numba
+# kernels on disjoint output tiles in a ThreadPoolExecutor, parallel.py:1-7 and
+# WorkerPool).  Each slab computes the same per-point arithmetic, so results are
+# bit-identical for any worker count; 1 worker (the default, and what the tests
+# use) runs the loops inline.
+_WORKERS = 1
+_POOL = None
+
+
+def set_workers(n: int) -> int:
+    """Use up to `n` host threads for the stencil loops; returns the count set."""
+    global _WORKERS, _POOL
+    n = max(1, int(n))
+    if n != _WORKERS:
+        if _POOL is not None:
+            _POOL.shutdown()
+            _POOL = None
+        _WORKERS = n
+        if n > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            _POOL = ThreadPoolExecutor(max_workers=n)
+    return _WORKERS
+
+
+def workers() -> int:
+    return _WORKERS
+
+
+def _row_slabs(fn, ny, halo, padded_args, plain_args, scalars, out):
+    """fn(*padded[j0:j1+2*halo], *plain[j0:j1], out[j0:j1], *scalars) over row slabs."""
+    if _WORKERS == 1 or ny < 64:
+        fn(*padded_args, *plain_args, out, *scalars)
+        return
+    parts = min(_WORKERS, ny // 32)
+    cuts = [ny * t // parts for t in range(parts + 1)]
+    futs = [_POOL.submit(fn, *[a[j0:j1 + 2 * halo] for a in padded_args], *[a[j0:j1] for a in plain_args],
+                         out[j0:j1], *scalars) for j0, j1 in zip(cuts[:-1], cuts[1:])]
+    for f in futs:
+        f.result()
+
 
 @_njit
 def _five_point(up, ksq, out, s, mc):
@@ -127,9 +167,10 @@ class CpuLevelOp:
         up = self.pad(u)
         out = np.empty_like(u)
         if self.r == 1:
-            _five_point(up, self.ksq, out, self.lap[1, 1] / 4.0, self.mass[1, 1])
+            _row_slabs(_five_point, self.ny, 1, (up,), (self.ksq,), (self.lap[1, 1] / 4.0, self.mass[1, 1]), out)
         else:
-            _dense_taps(up, self.kpad, out, self.lap, self.mass)
+            _row_slabs(lambda up_, kp_, o_: _dense_taps(up_, kp_, o_, self.lap, self.mass), self.ny, self.r,
+                       (up, self.kpad), (), (), out)
         for sl in self.pinned():
             out[sl] = u[sl]
         return out
@@ -161,8 +202,8 @@ class CpuLevelOp:
         dinv = self.dinv()
         for _ in range(sweeps):
             out = np.empty_like(x)
-            _jacobi_sweep(self.pad(x), self.ksq, b, dinv, out, self.lap[1, 1] / 4.0,
-                          self.mass[1, 1], omega)
+            _row_slabs(_jacobi_sweep, self.ny, 1, (self.pad(x),), (self.ksq, b, dinv),
+                       (self.lap[1, 1] / 4.0, self.mass[1, 1], omega), out)
             for sl in self.pinned():
                 out[sl] = x[sl] + omega * (b[sl] - x[sl])
             x = out

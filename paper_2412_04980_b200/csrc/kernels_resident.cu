@@ -1110,67 +1110,99 @@ __global__ void k_gm_scale(const cd* __restrict__ b, cd* __restrict__ v0, const 
 }
 
 // rotations of step j (krylov.py:126-151) from the Hessenberg column the MGS
-// step left in hcol[0..j] and ||w||^2 in hcol[j+1].x; stopping test
-__global__ void k_gm_givens(int j, const cd* hcol, cd* st, int cap, int maxit, double tol, cd* flag) {
+// step left in hcol[0..j] and ||w||^2 in hcol[j+1].x; stopping test.  One warp:
+// the operands are staged into shared memory in parallel, thread 0 runs the
+// serial rotation chain on them.
+constexpr int kGmThreads = 32;
+__global__ void __launch_bounds__(kGmThreads) k_gm_givens(int j, const cd* hcol, cd* st, int cap, int maxit,
+                                                          double tol, cd* flag) {
+  __shared__ cd col[kMaxCap + 2];
+  __shared__ cd ssn[kMaxCap];
+  __shared__ double scs[kMaxCap];
   GmView v(st, cap);
   if (v.fl[0]) return;
-  const double bnorm = v.hdr[0].x;
-  const double hn = sqrt(fmax(hcol[j + 1].x, 0.0));
+  const int t = threadIdx.x;
+  for (int i = t; i <= j; i += kGmThreads) col[i] = hcol[i];
+  for (int i = t; i < j; i += kGmThreads) {
+    ssn[i] = v.sn[i];
+    scs[i] = v.cs[i].x;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double bnorm = v.hdr[0].x;
+    const double hn = sqrt(fmax(hcol[j + 1].x, 0.0));
+    bool finite = isfinite(hn);
+    for (int i = 0; i <= j; ++i) finite &= isfinite(col[i].x) && isfinite(col[i].y);
+    for (int i = 0; i < j; ++i) {  // rotation i touches entries i, i+1 <= j
+      const cd ci = col[i], cn = col[i + 1];
+      const double c = scs[i];
+      const cd sc = cmul_(ssn[i], cn);
+      const cd nb = cmul_(mkc(-ssn[i].x, ssn[i].y), ci);
+      col[i] = mkc(c * ci.x + sc.x, c * ci.y + sc.y);
+      col[i + 1] = mkc(nb.x + c * cn.x, nb.y + c * cn.y);
+    }
+    const cd h1 = col[j], h2 = mkc(hn, 0.0);
+    double c;
+    cd sn;
+    const double a1 = cabs_(h1), a2 = cabs_(h2);
+    if (a2 == 0.0) { c = 1.0; sn = mkc(0.0, 0.0); }
+    else if (a1 == 0.0) { c = 0.0; sn = mkc(1.0, 0.0); }
+    else {
+      const double tt = hypot(a1, a2);
+      c = a1 / tt;
+      const cd q = cmul_(mkc(h1.x / a1, h1.y / a1), mkc(h2.x, -h2.y));
+      sn = mkc(q.x / tt, q.y / tt);
+    }
+    v.cs[j] = mkc(c, 0.0);
+    v.sn[j] = sn;
+    const cd sh = cmul_(sn, h2);
+    col[j] = mkc(c * h1.x + sh.x, c * h1.y + sh.y);
+    const cd gj = v.g[j];
+    v.g[j + 1] = cmul_(mkc(-sn.x, sn.y), gj);
+    v.g[j] = mkc(c * gj.x, c * gj.y);
+    const double rel = cabs_(v.g[j + 1]) / bnorm;
+    v.fl[1] = j + 1;
+    if (!finite) {
+      flag->x = 2.0;
+      v.fl[2] = 2;
+      v.fl[0] = 1;
+    } else if (hn < 1e-30 || rel <= tol || j + 1 >= maxit) {
+      v.fl[0] = 1;
+    }
+  }
+  __syncthreads();
   cd* Rc = v.R + (long long)j * (j + 1) / 2;  // column j: R[0..j]
-  bool finite = isfinite(hn);
-  for (int i = 0; i <= j; ++i) {
-    Rc[i] = hcol[i];
-    finite &= isfinite(hcol[i].x) && isfinite(hcol[i].y);
-  }
-  for (int i = 0; i < j; ++i) {  // rotation i touches entries i, i+1 <= j
-    const cd ci = Rc[i], cn = Rc[i + 1];
-    const double c = v.cs[i].x;
-    const cd sc = cmul_(v.sn[i], cn);
-    const cd nb = cmul_(mkc(-v.sn[i].x, v.sn[i].y), ci);
-    Rc[i] = mkc(c * ci.x + sc.x, c * ci.y + sc.y);
-    Rc[i + 1] = mkc(nb.x + c * cn.x, nb.y + c * cn.y);
-  }
-  const cd h1 = Rc[j], h2 = mkc(hn, 0.0);
-  double c;
-  cd sn;
-  const double a1 = cabs_(h1), a2 = cabs_(h2);
-  if (a2 == 0.0) { c = 1.0; sn = mkc(0.0, 0.0); }
-  else if (a1 == 0.0) { c = 0.0; sn = mkc(1.0, 0.0); }
-  else {
-    const double tt = hypot(a1, a2);
-    c = a1 / tt;
-    const cd q = cmul_(mkc(h1.x / a1, h1.y / a1), mkc(h2.x, -h2.y));
-    sn = mkc(q.x / tt, q.y / tt);
-  }
-  v.cs[j] = mkc(c, 0.0);
-  v.sn[j] = sn;
-  const cd sh = cmul_(sn, h2);
-  Rc[j] = mkc(c * h1.x + sh.x, c * h1.y + sh.y);
-  const cd gj = v.g[j];
-  v.g[j + 1] = cmul_(mkc(-sn.x, sn.y), gj);
-  v.g[j] = mkc(c * gj.x, c * gj.y);
-  const double rel = cabs_(v.g[j + 1]) / bnorm;
-  v.fl[1] = j + 1;
-  if (!finite) {
-    flag->x = 2.0;
-    v.fl[2] = 2;
-    v.fl[0] = 1;
-  } else if (hn < 1e-30 || rel <= tol || j + 1 >= maxit) {
-    v.fl[0] = 1;
-  }
+  for (int i = t; i <= j; i += kGmThreads) Rc[i] = col[i];
 }
 
-// least squares R y = g (krylov.py:161-168), its = flags[1]
-__global__ void k_gm_solve(cd* st, int cap) {
+// least squares R y = g (krylov.py:161-168), its = flags[1]; R staged in shared
+// memory when it fits (its <= 63), serial substitution on thread 0
+constexpr int kGmRStage = 2048;
+__global__ void __launch_bounds__(kGmThreads) k_gm_solve(cd* st, int cap) {
+  __shared__ cd sR[kGmRStage];
+  __shared__ cd sg[64];
+  __shared__ cd ys[64];
   GmView v(st, cap);
   const int its = v.fl[1];
+  const long long nr = (long long)its * (its + 1) / 2;
+  const bool staged = nr <= kGmRStage && its <= 64;
+  if (staged) {
+    for (int i = threadIdx.x; i < nr; i += kGmThreads) sR[i] = v.R[i];
+    for (int i = threadIdx.x; i < its; i += kGmThreads) sg[i] = v.g[i];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const cd* R = staged ? sR : v.R;
+  const cd* g = staged ? sg : v.g;
   for (int i = its - 1; i >= 0; --i) {
-    cd accy = v.g[i];
+    cd accy = g[i];
     for (int k = i + 1; k < its; ++k) {
-      const cd pr = cmul_(v.R[(long long)k * (k + 1) / 2 + i], v.y[k]);
+      const cd pr = cmul_(R[(long long)k * (k + 1) / 2 + i], staged ? ys[k] : v.y[k]);
       accy = mkc(accy.x - pr.x, accy.y - pr.y);
     }
-    v.y[i] = cdiv_(accy, v.R[(long long)i * (i + 1) / 2 + i]);
+    const cd yi = cdiv_(accy, R[(long long)i * (i + 1) / 2 + i]);
+    if (staged) ys[i] = yi;
+    v.y[i] = yi;
   }
 }
 
@@ -1191,9 +1223,9 @@ void launch_gm_scale(const cd* b, cd* v0, const cd* st, long long n, cudaStream_
   k_gm_scale<<<blocks, 256, 0, s>>>(b, v0, st, n);
 }
 void launch_gm_givens(int j, const cd* hcol, cd* st, int cap, int maxit, double tol, cd* flag, cudaStream_t s) {
-  k_gm_givens<<<1, 1, 0, s>>>(j, hcol, st, cap, maxit, tol, flag);
+  k_gm_givens<<<1, kGmThreads, 0, s>>>(j, hcol, st, cap, maxit, tol, flag);
 }
-void launch_gm_solve(cd* st, int cap, cudaStream_t s) { k_gm_solve<<<1, 1, 0, s>>>(st, cap); }
+void launch_gm_solve(cd* st, int cap, cudaStream_t s) { k_gm_solve<<<1, kGmThreads, 0, s>>>(st, cap); }
 void launch_gm_final(const cd* nn, const cd* st, int cap, int* its_out, double* rel_out, cd* flag, cudaStream_t s) {
   k_gm_final<<<1, 1, 0, s>>>(nn, st, cap, its_out, rel_out, flag);
 }

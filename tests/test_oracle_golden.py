@@ -145,3 +145,34 @@ def test_bicgstab_bitexact():
     m = oracle.cslp_op(hier, 2, 0.5)
     x, rep = bicgstab(m.apply, None, g["bc33_b"], oracle.Stop(0.1, 30), dot=oracle.reduce_dot)
     np.testing.assert_array_equal(x, g["bc33_x"])
+
+
+def test_worker_count_invariance():
+    """The row-slab worker pool (the bench's multi-threaded reference arm) is
+    bit-identical to the inline loops, as the reference's WorkerPool is
+    (parallel.py:1-7); the full c1s solve still matches the fixture."""
+    from oracle import ops
+    rng = np.random.default_rng(5)
+    ny, nx = 300, 257
+    ksq = 400.0 + 300.0 * rng.random((ny, nx))
+    bnd = ("sommerfeld", "dirichlet", "sommerfeld", "sommerfeld")
+    u = rng.standard_normal((ny, nx)) + 1j * rng.standard_normal((ny, nx))
+    try:
+        for level in (1, 2, 3):
+            lt, ld, mt, md, _ = oracle.level_kernels(level)
+            op = oracle.CpuLevelOp(nx, ny, 1.0 / 128, ksq, bnd, lt, ld, mt, md, shift=complex(1.0, 0.5),
+                                   level_scale=4.0 ** (level - 1))
+            ops.set_workers(1)
+            a1 = op.apply(u)
+            j1 = op.jacobi(u, u, 0.8, 2) if level == 1 else None
+            ops.set_workers(4)
+            np.testing.assert_array_equal(op.apply(u), a1)
+            if level == 1:
+                np.testing.assert_array_equal(op.jacobi(u, u, 0.8, 2), j1)
+        g = golden("solve_c1s.npz")
+        hier, b = oracle.mp1_problem(50.0, 129, 2, "sommerfeld")
+        pols, outer = oracle.madp_preset(hier)
+        x, rep = oracle.CpuMadpSolver(hier, pols, outer).solve(b)
+        np.testing.assert_array_equal(x, g["solution"])
+    finally:
+        ops.set_workers(1)
