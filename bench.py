@@ -139,6 +139,20 @@ def _allmax(val, ws):
     return float(t.item())
 
 
+def ncu_traffic(kernel, config):
+    """dram read + write bytes per launch of `kernel` from the committed
+    `ncu --set full` capture (profiles/r01c_kernels_ncu.json, config-2 grids)."""
+    if config != "c2":
+        return None
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01c_kernels_ncu.json")
+    try:
+        with open(path) as f:
+            k = json.load(f)["kernels"][kernel]
+        return round(k["traffic_MB"] * 1e6)
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def kernel_roofline(hdb, hier, reps=20):
     """Time the fine-level 5-point apply (K1) and other path kernels live with CUDA
     events on the library stream (= torch's current stream)."""
@@ -398,7 +412,9 @@ def main():
                     "d2h_bytes_per_step": int(b_host.nbytes) * ws},
             "roofline": {"bound": "hbm", "kernel": "stencil5_apply (K1, fine level)",
                          "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
-                         "traffic": None, "peak_source": peak_src,
+                         "traffic": ncu_traffic("k_r1s<0>", args.config),
+                         "traffic_source": "profiles/r01c_kernels_ncu.json (ncu --set full, dram read+write per launch)",
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"]},
             "kernels": {k: {"gbs": round(v["gbs"], 1), "ms": round(v["ms"], 4), "frac": round(v["gbs"] / peak, 3)}
                         for k, v in kern.items()},

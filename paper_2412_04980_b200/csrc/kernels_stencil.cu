@@ -248,106 +248,110 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
   out[p] = MODE == 0 ? acc : c_sub(b[p], acc);
 }
 
-// Register-blocked form for large grids: each thread owns RYB vertically
-// adjacent outputs of one column and streams the input window rows top to
-// bottom, so every shared-memory (u, k^2) tap value is read once per thread
-// instead of once per output.  Output row r receives tap (a, bb) from input row
-// r + a; rows arrive in increasing a and, within a row, increasing bb, so each
-// output still accumulates in the reference's row-major tap order.
-constexpr int TYB = 4, RYB = 8, THB = TYB * RYB;
-
-// Per-tap coefficients are staged in shared memory and read through a volatile
-// pointer at each use (warp-broadcast loads); held in registers across the
-// unrolled window they would cost 2 * 3 * 25 registers and halve occupancy.
-// Used for radius 2 (k_rg at ~55% of either roofline); k_rg<3> already runs at
-// ~80% of the FP64 issue rate, which blocking cannot improve.
-struct TapCoef {
-  double lap, mx, my;
+// Horizontally blocked radius-2 form for large grids (radius 3 keeps k_rg: its
+// 49-tap body is already FP64/shared-memory co-limited and blocking measured
+// slower): each thread owns HX
+// adjacent outputs of one row.  For tap row a (a rolled, warp-uniform loop, so
+// the per-tap coefficients come from uniform registers) it loads its HX + 2R
+// window values once and feeds every (bb, r) tap; per output the taps still
+// arrive in the reference's row-major (a, bb) order.  Shared-memory columns are
+// skewed by one element every HX so a warp's 16-byte window loads are
+// conflict-free (lane stride (HX + 1) * 16 B).
+constexpr int HX = 4, HTY = 8, HTX = 32 * HX;
+__device__ __forceinline__ int hskew(int col) { return col + col / HX; }
+template <int R>
+struct HTile {
+  static constexpr int W = HTX + 2 * R, P = W + W / HX + 1, H = HTY + 2 * R;
+  static constexpr size_t bytes = (size_t)H * P * (sizeof(cd) + sizeof(double));
 };
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(TX * TYB) k_rgb(const cd* __restrict__ u, const cd* __restrict__ b,
+__global__ void __launch_bounds__(32 * HTY) k_rgh(const cd* __restrict__ u, const cd* __restrict__ b,
                                                  const double* __restrict__ k, cd* __restrict__ out,
                                                  Geom g, OpCoef c) {
   if (c.skip && *c.skip) return;
-  constexpr int W = TX + 2 * R, H = THB + 2 * R, N = 2 * R + 1;
-  __shared__ cd su[H][W];
-  __shared__ double sk[H][W];
-  __shared__ TapCoef sc[N * N];
-  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * THB;
-  const int tid = threadIdx.y * TX + threadIdx.x;
-  const bool fast = c.uniform && i0 >= R && i0 + TX + R <= g.nx && g.row0 + j0 >= R &&
-                    g.row0 + j0 + THB + R <= g.nyg;
-  for (int t = tid; t < N * N; t += TX * TYB) {
-    if (fast) sc[t] = TapCoef{c.ucoef[t].x, c.ucoef[t].y, 0.0};
-    else sc[t] = TapCoef{c.lap[t], c.mass[t].x, c.mass[t].y};
-  }
-  if (fast) {
-    for (int t = tid; t < H * W; t += TX * TYB) {
-      const int ty = t / W, tx = t % W;
-      su[ty][tx] = U(u, g, g.row0 + j0 + ty - R, i0 + tx - R);
-    }
-  } else {
-    for (int t = tid; t < H * W; t += TX * TYB) {
-      const int ty = t / W, tx = t % W;
-      const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
-      su[ty][tx] = upad(u, k, g, c, gj, gi);
-      sk[ty][tx] = kpad(k, g, c, gj, gi);
+  using T = HTile<R>;
+  constexpr int N = 2 * R + 1, W = T::W, P = T::P, H = T::H;
+  extern __shared__ __align__(16) unsigned char hsm[];
+  cd* su = reinterpret_cast<cd*>(hsm);
+  double* sk = reinterpret_cast<double*>(su + H * P);
+  const int i0 = blockIdx.x * HTX, j0 = blockIdx.y * HTY;
+  const bool fast = c.uniform && i0 >= R && i0 + HTX + R <= g.nx && g.row0 + j0 >= R &&
+                    g.row0 + j0 + HTY + R <= g.nyg;
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  for (int t = tid; t < H * W; t += 32 * HTY) {
+    const int ty = t / W, tx = t % W;
+    const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+    const int si = ty * P + hskew(tx);
+    if (fast) {
+      su[si] = U(u, g, gj, gi);
+    } else {
+      su[si] = upad(u, k, g, c, gj, gi);
+      sk[si] = kpad(k, g, c, gj, gi);
     }
   }
   __syncthreads();
-  const volatile TapCoef* vc = sc;
-  const int tx = threadIdx.x, jr = threadIdx.y * RYB;
-  cd acc[RYB];
+  const int ty = threadIdx.y, cx0 = threadIdx.x * HX;
+  cd acc[HX];
 #pragma unroll
-  for (int r = 0; r < RYB; ++r) acc[r] = mkc(0.0, 0.0);
-  if (fast) {
+  for (int r = 0; r < HX; ++r) acc[r] = mkc(0.0, 0.0);
+#pragma unroll 1
+  for (int a = 0; a < N; ++a) {
+    const cd* row = su + (ty + a) * P;
+    cd uv[HX + 2 * R];
 #pragma unroll
-    for (int t = 0; t < RYB + 2 * R; ++t) {
+    for (int q = 0; q < HX + 2 * R; ++q) uv[q] = row[hskew(cx0 + q)];
+    if (fast) {
 #pragma unroll
       for (int bb = 0; bb < N; ++bb) {
-        const cd uv = su[jr + t][tx + bb];
+        const cd cf = c.ucoef[a * N + bb];
 #pragma unroll
-        for (int r = 0; r < RYB; ++r) {
-          const int a = t - r;
-          if (a < 0 || a >= N) continue;
-          const cd coef = mkc(vc[a * N + bb].lap, vc[a * N + bb].mx);
-          acc[r] = c_add(acc[r], c_mul(coef, uv));
-        }
+        for (int r = 0; r < HX; ++r) acc[r] = c_add(acc[r], c_mul(cf, uv[r + bb]));
       }
-    }
-  } else {
+    } else {
+      const double* krow = sk + (ty + a) * P;
+      double kv[HX + 2 * R];
 #pragma unroll
-    for (int t = 0; t < RYB + 2 * R; ++t) {
+      for (int q = 0; q < HX + 2 * R; ++q) kv[q] = krow[hskew(cx0 + q)];
 #pragma unroll
       for (int bb = 0; bb < N; ++bb) {
-        const cd uv = su[jr + t][tx + bb];
-        const double kp = sk[jr + t][tx + bb];
+        const double lap = c.lap[a * N + bb];
+        const cd m = c.mass[a * N + bb];
 #pragma unroll
-        for (int r = 0; r < RYB; ++r) {
-          const int a = t - r;
-          if (a < 0 || a >= N) continue;
-          const double lap = vc[a * N + bb].lap, mx = vc[a * N + bb].mx, my = vc[a * N + bb].my;
-          const cd coef = mkc(__dadd_rn(lap, __dmul_rn(mx, kp)), __dmul_rn(my, kp));
-          acc[r] = c_add(acc[r], c_mul(coef, uv));
+        for (int r = 0; r < HX; ++r) {
+          const double kp = kv[r + bb];
+          const cd coef = mkc(__dadd_rn(lap, __dmul_rn(m.x, kp)), __dmul_rn(m.y, kp));
+          acc[r] = c_add(acc[r], c_mul(coef, uv[r + bb]));
         }
       }
     }
   }
-  const int i = i0 + tx;
-  if (i >= g.nx) return;
+  const int j = j0 + ty;
+  if (j >= g.ny) return;
 #pragma unroll
-  for (int r = 0; r < RYB; ++r) {
-    const int j = j0 + jr + r;
-    if (j >= g.ny) break;
+  for (int r = 0; r < HX; ++r) {
+    const int i = i0 + cx0 + r;
+    if (i >= g.nx) break;
     const long long p = (long long)j * g.nx + i;
     if (pinned(g, c, j + g.row0, i)) {
-      const cd uc = su[jr + r + R][tx + R];
+      const cd uc = su[(ty + R) * P + hskew(cx0 + r + R)];
       out[p] = MODE == 0 ? uc : c_sub(b[p], uc);
     } else {
       out[p] = MODE == 0 ? acc[r] : c_sub(b[p], acc[r]);
     }
   }
+}
+
+template <int R, int MODE>
+static void launch_rgh(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
+                       cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_rgh<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HTile<R>::bytes);
+    configured = true;
+  }
+  const dim3 blk(32, HTY), grd((g.nx + HTX - 1) / HTX, (g.ny + HTY - 1) / HTY);
+  k_rgh<R, MODE><<<grd, blk, HTile<R>::bytes, st>>>(u, b, k, out, g, c);
 }
 
 // ------------------------------------------------------------------------
@@ -373,10 +377,9 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
     const char* e = getenv("HDB_RG_BLOCKED");
     return !e || atoi(e) != 0;
   }();
-  if (blocked && c.radius == 2 && g.nx >= 256 && g.ny >= 256) {
-    const dim3 blk(TX, TYB), grd((g.nx + TX - 1) / TX, (g.ny + THB - 1) / THB);
-    if (mode == 0) k_rgb<2, 0><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
-    else k_rgb<2, 1><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+  if (blocked && c.radius == 2 && g.nx >= 256 && g.ny >= 64) {
+    if (mode == 0) launch_rgh<2, 0>(c, g, u, b, k, out, st);
+    else launch_rgh<2, 1>(c, g, u, b, k, out, st);
     return;
   }
   const dim3 blk(TX, TY), grd((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);
