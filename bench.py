@@ -194,10 +194,18 @@ def kernel_roofline(hdb, hier, reps=20):
     res["restrict"] = (20.0 * n, t)
     t = timeit(lambda: _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr())))
     res["prolong"] = (20.0 * n, t)
-    import ctypes as C
-    d = (C.c_double * 2)()
-    t = timeit(lambda: L.hdb_dot(u.data_ptr(), out.data_ptr(), n, d))  # includes a host sync per call
-    res["dot(sync)"] = (32.0 * n, t)
+    t = timeit(lambda: _lib.check(L.hdb_dot(u.data_ptr(), out.data_ptr(), n, None)))  # device-resident result
+    res["dot"] = (32.0 * n, t)
+    # fused matvec + residual + norms (MG divergence guard): one pass, residual not stored
+    t = timeit(lambda: _lib.check(L.hdb_op_resnorm(sop, b.data_ptr(), u.data_ptr(), None)))
+    res["stencil5_resnorm_fused"] = (40.0 * n, t)
+    # the unfused sequence it replaces: residual (56 B/pt) + 2 dots (32 B/pt each)
+    def unfused():
+        _lib.check(L.hdb_op_residual(sop, b.data_ptr(), u.data_ptr(), out.data_ptr()))
+        _lib.check(L.hdb_dot(out.data_ptr(), out.data_ptr(), n, None))
+        _lib.check(L.hdb_dot(b.data_ptr(), b.data_ptr(), n, None))
+    t = timeit(unfused)
+    res["stencil5_resnorm_unfused(3 launches)"] = (40.0 * n, t)
     if hier.ml < 3:
         return {k: {"bytes": bts, "ms": tt * 1e3, "gbs": bts / tt / 1e9} for k, (bts, tt) in res.items()}
     op3 = hdb.helmholtz_operator(hier, 3)

@@ -82,6 +82,11 @@ int hdb_op_create_slab(hdb_op** out, int nx, int ny_global, int radius, double h
 int hdb_op_apply(hdb_op* op, const void* u, void* out);
 /* out = b - A u  (MG residual mg.py:116, A-DEF1 v - A t madp.py:325-326) */
 int hdb_op_residual(hdb_op* op, const void* b, const void* u, void* out);
+/* fused matvec + residual + norms (MG divergence guard, mg.py:131-138):
+   out2 = { ||b - A u||^2, ||b||^2 }; the residual is not stored (radius 1: one
+   pass over u, b, k^2 — 40 B/pt); synchronises to return the values
+   (out2 == NULL: enqueue only, no sync — microbenchmarks) */
+int hdb_op_resnorm(hdb_op* op, const void* b, const void* u, double* out2);
 /* one damped-Jacobi sweep (_kernels.py:53-68 + mg.py:88-102); x == NULL: from zero */
 int hdb_op_jacobi(hdb_op* op, const void* x, const void* b, void* out, double omega);
 
@@ -92,6 +97,7 @@ int hdb_restrict(const void* fine, int nfy, int nfx, void* coarse, int zero_mask
 int hdb_prolong(const void* coarse, int nfy, int nfx, const void* base, void* fine);
 
 /* ---- reductions: replaces reduce_dot (parallel.py:168-195) ---------------- */
+/* out2_host == NULL: enqueue only (result stays on the device; microbenchmarks) */
 int hdb_dot(const void* u, const void* v, long long n, double* out2_host);
 
 /* ---- CSLP multigrid: replaces CslpMultigrid (mg.py:59-139) ---------------- */

@@ -41,6 +41,7 @@ SIGNATURES = {
     "hdb_thread_engine_end": [],
     "hdb_op_apply": [vp, vp, vp],
     "hdb_op_residual": [vp, vp, vp, vp],
+    "hdb_op_resnorm": [vp, vp, vp, P(f64)],
     "hdb_op_jacobi": [vp, vp, vp, vp, f64],
     "hdb_restrict": [vp, i32, i32, vp, i32],
     "hdb_prolong": [vp, i32, i32, vp, vp],

@@ -205,6 +205,23 @@ int hdb_op_apply(hdb_op* op, const void* u, void* out) {
 int hdb_op_residual(hdb_op* op, const void* b, const void* u, void* out) {
   return guarded([&] { op->op.residual((const cd*)b, (const cd*)u, (cd*)out); check_launch(); });
 }
+int hdb_op_resnorm(hdb_op* op, const void* b, const void* u, double* out2) {
+  return guarded([&] {
+    Engine& E = engine();
+    cd* scratch = op->op.c.radius == 1 ? nullptr : E.alloc(op->op.n);
+    op->op.resnorm((const cd*)b, (const cd*)u, E.dscal + kSlotMisc, scratch);
+    check_launch();
+    if (!out2) {  // timing form: result stays in the device slot, no sync
+      if (scratch) E.free(scratch);
+      return;
+    }
+    HDB_CUDA(cudaMemcpyAsync(E.hscal + kSlotMisc, E.dscal + kSlotMisc, sizeof(cd), cudaMemcpyDeviceToHost, E.st));
+    E.sync();
+    if (scratch) E.free(scratch);
+    out2[0] = E.hscal[kSlotMisc].x;
+    out2[1] = E.hscal[kSlotMisc].y;
+  });
+}
 int hdb_op_jacobi(hdb_op* op, const void* x, const void* b, void* out, double omega) {
   return guarded([&] {
     if (op->op.c.radius != 1) throw Error(E_ARG, "Jacobi is only defined for radius-1 operators");
@@ -235,6 +252,7 @@ int hdb_dot(const void* u, const void* v, long long n, double* out2) {
     Engine& E = engine();
     launch_dot((const cd*)u, (const cd*)v, n, E.red, E.dscal + kSlotMisc, E.st);
     check_launch();
+    if (!out2) return;  // timing form: result stays on the device, no sync
     HDB_CUDA(cudaMemcpyAsync(E.hscal + kSlotMisc, E.dscal + kSlotMisc, sizeof(cd), cudaMemcpyDeviceToHost, E.st));
     E.sync();
     out2[0] = E.hscal[kSlotMisc].x;

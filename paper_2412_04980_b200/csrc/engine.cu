@@ -22,7 +22,7 @@ Engine::Engine(int dev) : device(dev) {
   HDB_CUDA(cudaSetDevice(dev));
   HDB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   own_st = st;
-  HDB_CUDA(cudaMalloc(&red.partials, sizeof(cd) * kMaxReduceBlocks));
+  HDB_CUDA(cudaMalloc(&red.partials, sizeof(cd) * kMaxPartials));
   HDB_CUDA(cudaMalloc(&red.ticket, sizeof(unsigned)));
   HDB_CUDA(cudaMemset(red.ticket, 0, sizeof(unsigned)));
   HDB_CUDA(cudaMalloc(&dscal, sizeof(cd) * kScal));
@@ -125,6 +125,21 @@ void LevelOp::residual(const cd* b, const cd* u, cd* out) const {
   exchange(u, c.radius);
   launch_apply(c, g, u, b, ksq, out, 1, E.st);
   E.launches++;
+}
+void LevelOp::resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const {
+  Engine& E = engine();
+  exchange(u, c.radius);
+  if (c.radius == 1) {
+    launch_resnorm(c, g, u, b, ksq, E.red, slot, E.st);
+    E.launches++;
+  } else {
+    launch_apply(c, g, u, b, ksq, scratch, 1, E.st);
+    launch_dot(scratch, scratch, n, E.red, slot, E.st);
+    launch_dot(b, b, n, E.red, E.dscal + kSlotMgB, E.st);
+    launch_pack_im(slot, E.dscal + kSlotMgB, E.st);
+    E.launches += 4;
+  }
+  reduce(slot);
 }
 void LevelOp::jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const {
   Engine& E = engine();
@@ -823,15 +838,12 @@ void Multigrid::vcycle(const cd* b, cd* x, const cd* x0) {
     op->reduce(E.dscal + kSlotMgR0);
   }
   cycle(0, b, x, x0);
-  // divergence guard (mg.py:133-138), evaluated on device; raised at the next host sync
-  op->residual(b, x, R[0]);
-  launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgPost, E.st);
-  launch_dot(b, b, op->n, E.red, E.dscal + kSlotMgB, E.st);
-  op->reduce(E.dscal + kSlotMgPost);
-  op->reduce(E.dscal + kSlotMgB);
-  launch_guard(E.dscal + kSlotMgPost, E.dscal + kSlotMgB, x0 ? E.dscal + kSlotMgR0 : nullptr, guard,
-               E.dscal + kSlotFlag, E.st);
-  E.launches += 3;
+  // divergence guard (mg.py:133-138), evaluated on device; raised at the next host sync.
+  // One fused pass: (||b - M x||^2, ||b||^2) without storing the residual.
+  op->resnorm(b, x, E.dscal + kSlotMgPost, R[0]);
+  launch_guard(E.dscal + kSlotMgPost, nullptr, x0 ? E.dscal + kSlotMgR0 : nullptr, guard, E.dscal + kSlotFlag,
+               E.st);
+  E.launches += 1;
 }
 
 }  // namespace hdb

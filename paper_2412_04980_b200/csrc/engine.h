@@ -98,6 +98,9 @@ struct LevelOp {
   void apply(const cd* u, cd* out) const;                 // out = A u
   void residual(const cd* b, const cd* u, cd* out) const;  // out = b - A u
   void jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const;
+  // slot = (||b - A u||^2, ||b||^2), reduced over the distribution; `scratch`
+  // (a level vector) is used only by the unfused radius-2/3 form
+  void resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const;
   // reductions over this level's distribution (all-reduce when sharded)
   void reduce(cd* dev_slot) const;
 };

@@ -70,6 +70,7 @@ struct OpCoef {
 };
 
 constexpr int kReduceThreads = 256;
-constexpr int kMaxReduceBlocks = 592;  // 4 x 148 SMs
+constexpr int kMaxReduceBlocks = 592;  // 4 x 148 SMs (dot / MGS grids)
+constexpr int kMaxPartials = 1184;     // 8 x 148 SMs (fused stencil-norm grids); partials capacity
 
 }  // namespace hdb

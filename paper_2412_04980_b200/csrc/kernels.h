@@ -5,7 +5,7 @@
 namespace hdb {
 
 struct RedWS {  // per-stream reduction workspace
-  cd* partials = nullptr;   // kMaxReduceBlocks
+  cd* partials = nullptr;   // kMaxPartials
   unsigned* ticket = nullptr;
 };
 
@@ -14,6 +14,9 @@ int reduce_blocks(long long n);
 // mode 0: out = A u ; mode 1: out = b - A u
 void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out, int mode,
                   cudaStream_t st);
+// radius 1 only: dst = (||b - A u||^2, ||b||^2) in one pass (residual not stored)
+void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, RedWS& ws, cd* dst,
+                    cudaStream_t st);
 void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out, double omega,
                    bool from_zero, cudaStream_t st);
 // transfer geometry: fine rows [f_row0, f_row0+f_ny) of nfy_g, coarse rows [c_row0, c_row0+c_ny) of ncy_g
@@ -37,6 +40,7 @@ void launch_step1(const cd* b2, const cd* h0, const cd* hn2, cd* y, int* its, cd
 void launch_finite_guard(const cd* v, cd* flag, cudaStream_t st);
 void launch_axpy(const cd* y, cd a, const cd* x, cd* out, long long n, int sub, cudaStream_t st);
 void launch_bicg_p(const cd* r, cd* p, const cd* v, cd beta, cd omega, long long n, cudaStream_t st);
+void launch_pack_im(cd* dst, const cd* src, cudaStream_t st);  // dst->y = src->x
 void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st);
 
 // device-resident GMRES (kernels_resident.cu).  mode 0: one cluster, 1: whole grid

@@ -8,6 +8,7 @@
 // column once per Arnoldi step.
 #include "kernels.h"
 #include "hdb_common.cuh"
+#include "reduce.cuh"
 
 namespace hdb {
 
@@ -16,57 +17,6 @@ int reduce_blocks(long long n) {
   if (b < 1) b = 1;
   if (b > kMaxReduceBlocks) b = kMaxReduceBlocks;
   return (int)b;
-}
-
-__device__ __forceinline__ cd warp_sum(cd v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v.x += __shfl_down_sync(0xffffffffu, v.x, o);
-    v.y += __shfl_down_sync(0xffffffffu, v.y, o);
-  }
-  return v;
-}
-
-// block-wide sum in fixed order; result valid in thread 0
-__device__ __forceinline__ cd block_sum(cd v) {
-  __shared__ cd sw[kReduceThreads / 32];
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (lane == 0) sw[wid] = v;
-  __syncthreads();
-  if (wid == 0) {
-    v = lane < kReduceThreads / 32 ? sw[lane] : mkc(0.0, 0.0);
-    v = warp_sum(v);
-  }
-  __syncthreads();
-  return v;
-}
-
-// finish a grid reduction: every block deposits its partial; the last one
-// sums partials[0..G) in order and stores to *dst (optionally only the real
-// part as a squared norm).
-__device__ __forceinline__ void grid_finish(cd part, cd* partials, unsigned* ticket, cd* dst) {
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    partials[blockIdx.x] = part;
-    __threadfence();
-    const unsigned t = atomicAdd(ticket, 1u);
-    last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  cd v = mkc(0.0, 0.0);
-  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-    const volatile double* q = (const volatile double*)(partials + b);
-    v.x += q[0];
-    v.y += q[1];
-  }
-  v = block_sum(v);
-  if (threadIdx.x == 0) {
-    *dst = v;
-    *ticket = 0u;
-  }
 }
 
 // dst = <u, v> = sum conj(u) v
@@ -217,7 +167,8 @@ __global__ void k_finite_guard(const cd* v, cd* flag) {
 
 // MG divergence guard (mg.py:133-138): flag |= sqrt(post2) > guard*sqrt(bn2)
 __global__ void k_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag) {
-  const double post = sqrt(fmax(post2->x, 0.0)), bn = sqrt(fmax(bn2->x, 0.0));
+  // bn2 == nullptr: ||b||^2 rides in post2's imaginary part (fused k_resnorm)
+  const double post = sqrt(fmax(post2->x, 0.0)), bn = sqrt(fmax(bn2 ? bn2->x : post2->y, 0.0));
   const double r0 = r02 ? sqrt(fmax(r02->x, 0.0)) : bn;
   if (bn > 0.0 && post > guard * fmax(r0, bn)) flag->x = 1.0;
 }
@@ -262,6 +213,8 @@ void launch_step1(const cd* b2, const cd* h0, const cd* hn2, cd* y, int* its, cd
   k_step1<<<1, 1, 0, st>>>(b2, h0, hn2, y, its, flag);
 }
 void launch_finite_guard(const cd* v, cd* flag, cudaStream_t st) { k_finite_guard<<<1, 1, 0, st>>>(v, flag); }
+__global__ void k_pack_im(cd* dst, const cd* src) { dst->y = src->x; }
+void launch_pack_im(cd* dst, const cd* src, cudaStream_t st) { k_pack_im<<<1, 1, 0, st>>>(dst, src); }
 void launch_guard(const cd* post2, const cd* bn2, const cd* r02, double guard, cd* flag, cudaStream_t st) {
   k_guard<<<1, 1, 0, st>>>(post2, bn2, r02, guard, flag);
 }

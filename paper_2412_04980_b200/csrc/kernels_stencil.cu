@@ -8,6 +8,7 @@
 
 #include "kernels.h"
 #include "stencil.cuh"
+#include "reduce.cuh"
 
 namespace hdb {
 
@@ -61,6 +62,18 @@ __global__ void __launch_bounds__(256) k_r1(const cd* __restrict__ u, const cd* 
 // lane shuffles (edge lanes load their outer neighbour).  Blocks that touch a
 // physical boundary or a slab edge take the per-point closure path.  Same
 // arithmetic as k_r1 (bit-identical).
+// interior Jacobi reciprocal 1 / (4s + mc k^2) (no Sommerfeld terms), numpy's
+// Smith division (same operations as dinv_at)
+__device__ __forceinline__ cd interior_dinv(const OpCoef& c, double kc) {
+  const double dr = __dadd_rn(4.0 * c.s, __dmul_rn(c.mc.x, kc)), di = __dmul_rn(c.mc.y, kc);
+  if (fabs(dr) >= fabs(di)) {
+    const double rat = __ddiv_rn(di, dr), scl = __ddiv_rn(1.0, __dadd_rn(dr, __dmul_rn(di, rat)));
+    return mkc(scl, __dmul_rn(-rat, scl));
+  }
+  const double rat = __ddiv_rn(dr, di), scl = __ddiv_rn(1.0, __dadd_rn(di, __dmul_rn(dr, rat)));
+  return mkc(__dmul_rn(rat, scl), -scl);
+}
+
 constexpr int SX = 32, SY = 4, RB = 16;  // block 32x4 threads, 16 rows per thread
 
 template <int MODE>
@@ -112,20 +125,15 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
     const double* kp = k + (long long)jbeg * nx + i;
     const cd* bp = b + (long long)jbeg * nx + i;
     cd* op = out + (long long)jbeg * nx + i;
+    // the reciprocal depends on k^2 only: reuse it while k^2 repeats down the
+    // column (constant and layered models), bit-identical either way
+    double klast = kp[0];
+    cd dlast = interior_dinv(c, klast);
 #pragma unroll 4
     for (int r = 0; r < RB; ++r) {
       const double kc = kp[r * nx];
-      // interior diagonal: 4s + mc k (no Sommerfeld terms), Smith reciprocal
-      const double dr = __dadd_rn(4.0 * c.s, __dmul_rn(c.mc.x, kc)), di = __dmul_rn(c.mc.y, kc);
-      cd d;
-      if (fabs(dr) >= fabs(di)) {
-        const double rat = __ddiv_rn(di, dr), scl = __ddiv_rn(1.0, __dadd_rn(dr, __dmul_rn(di, rat)));
-        d = mkc(scl, __dmul_rn(-rat, scl));
-      } else {
-        const double rat = __ddiv_rn(dr, di), scl = __ddiv_rn(1.0, __dadd_rn(di, __dmul_rn(dr, rat)));
-        d = mkc(__dmul_rn(rat, scl), -scl);
-      }
-      op[r * nx] = c_mul(c_scale(omega, d), bp[r * nx]);
+      if (kc != klast) { klast = kc; dlast = interior_dinv(c, kc); }
+      op[r * nx] = c_mul(c_scale(omega, dlast), bp[r * nx]);
     }
     return;
   }
@@ -137,6 +145,9 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
   double kc = kp[0];
   cd bc = (MODE != 0) ? bp[0] : mkc(0.0, 0.0);
   cd wl = (lane == 0) ? up[-1] : mkc(0.0, 0.0), el = (lane == SX - 1) ? up[1] : mkc(0.0, 0.0);
+  double klast = 0.0;
+  cd dlast = mkc(0.0, 0.0);
+  if (MODE == 2) { klast = kc; dlast = interior_dinv(c, kc); }
 #pragma unroll (MODE == 2 ? 2 : 4)
   for (int r = 0; r < RB; ++r) {
     const long long o = (long long)r * nx;
@@ -166,16 +177,8 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
       if (MODE == 1) {
         op[o] = r1;
       } else {
-        const double dr = __dadd_rn(4.0 * c.s, __dmul_rn(c.mc.x, kc)), di = __dmul_rn(c.mc.y, kc);
-        cd d;
-        if (fabs(dr) >= fabs(di)) {
-          const double rat = __ddiv_rn(di, dr), scl = __ddiv_rn(1.0, __dadd_rn(dr, __dmul_rn(di, rat)));
-          d = mkc(scl, __dmul_rn(-rat, scl));
-        } else {
-          const double rat = __ddiv_rn(dr, di), scl = __ddiv_rn(1.0, __dadd_rn(di, __dmul_rn(dr, rat)));
-          d = mkc(__dmul_rn(rat, scl), -scl);
-        }
-        op[o] = c_add(c_, c_mul(c_scale(omega, d), r1));
+        if (kc != klast) { klast = kc; dlast = interior_dinv(c, kc); }
+        op[o] = c_add(c_, c_mul(c_scale(omega, dlast), r1));
       }
     }
     s_ = c_;
@@ -186,6 +189,88 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
     wl = wl2;
     el = el2;
   }
+}
+
+// ------------------------------------------------------------------------
+// Fused residual norm (the MG divergence guard, mg.py:131-138, and any
+// ||b - A u|| that only needs the norm): dst = (||b - A u||^2, ||b||^2) as one
+// complex slot (re, im), read in one pass over u, b, k^2 (40 B/pt); the
+// residual itself is never stored.  Persistent walk over 32 x (8*RB) strip
+// tiles (block q takes tiles q, q + G, ...), interior tiles with the k_r1s
+// sliding window, boundary tiles per point; per-block partials are combined in
+// block order by the last block, so the result is deterministic for a grid.
+constexpr int NRW = 4;  // warps per block (tile rows = NRW * RB)
+__global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                 const double* __restrict__ k, Geom g, OpCoef c, cd* partials,
+                                                 unsigned* ticket, cd* dst) {
+  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+  const int ntx = (g.nx + 31) / 32, nty = (g.ny + NRW * RB - 1) / (NRW * RB);
+  const long long ntiles = (long long)ntx * nty;
+  double rr = 0.0, bb = 0.0;
+  const long long nx = g.nx;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int bx = (int)(tile % ntx), by = (int)(tile / ntx);
+    const int i = bx * 32 + lane;
+    const int jbeg = (by * NRW + wy) * RB;
+    const int gi0 = bx * 32, gj0 = g.row0 + by * NRW * RB, gj1 = gj0 + NRW * RB;
+    const bool interior = gi0 >= 1 && gi0 + 32 <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
+                          by * NRW * RB + NRW * RB <= g.ny;
+    if (!interior) {
+      if (i < g.nx)
+        for (int r = 0; r < RB; ++r) {
+          const int j = jbeg + r;
+          if (j >= g.ny) break;
+          const int gj = j + g.row0;
+          const long long p = (long long)j * nx + i;
+          const cd bc = b[p], uc = u[p];
+          cd res;
+          if (pinned(g, c, gj, i)) {
+            res = c_sub(bc, uc);
+          } else {
+            const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
+                                     upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
+            res = c_sub(bc, Au);
+          }
+          rr = __fma_rn(res.x, res.x, rr); rr = __fma_rn(res.y, res.y, rr);
+          bb = __fma_rn(bc.x, bc.x, bb); bb = __fma_rn(bc.y, bc.y, bb);
+        }
+      continue;
+    }
+    const cd* up = u + (long long)jbeg * nx + i;
+    const double* kp = k + (long long)jbeg * nx + i;
+    const cd* bp = b + (long long)jbeg * nx + i;
+    cd s_ = up[-nx], c_ = up[0], n_ = up[nx];
+    double kc = kp[0];
+    cd bc = bp[0];
+    cd wl = (lane == 0) ? up[-1] : mkc(0.0, 0.0), el = (lane == 31) ? up[1] : mkc(0.0, 0.0);
+#pragma unroll 4
+    for (int r = 0; r < RB; ++r) {
+      const long long o = (long long)r * nx;
+      const bool more = r + 1 < RB;
+      cd n2 = mkc(0.0, 0.0), b2 = mkc(0.0, 0.0), wl2 = mkc(0.0, 0.0), el2 = mkc(0.0, 0.0);
+      double k2 = 0.0;
+      if (more) {
+        n2 = up[o + 2 * nx];
+        k2 = kp[o + nx];
+        b2 = bp[o + nx];
+        if (lane == 0) wl2 = up[o + nx - 1];
+        if (lane == 31) el2 = up[o + nx + 1];
+      }
+      cd w_, e_;
+      w_.x = __shfl_up_sync(0xffffffffu, c_.x, 1);
+      w_.y = __shfl_up_sync(0xffffffffu, c_.y, 1);
+      e_.x = __shfl_down_sync(0xffffffffu, c_.x, 1);
+      e_.y = __shfl_down_sync(0xffffffffu, c_.y, 1);
+      if (lane == 0) w_ = wl;
+      if (lane == 31) e_ = el;
+      const cd res = c_sub(bc, five_point(c.s, c.mc, kc, c_, w_, e_, s_, n_));
+      rr = __fma_rn(res.x, res.x, rr); rr = __fma_rn(res.y, res.y, rr);
+      bb = __fma_rn(bc.x, bc.x, bb); bb = __fma_rn(bc.y, bc.y, bb);
+      s_ = c_; c_ = n_; n_ = n2; kc = k2; bc = b2; wl = wl2; el = el2;
+    }
+  }
+  const cd part = block_sum<32 * NRW>(mkc(rr, bb));
+  grid_finish<32 * NRW>(part, partials, ticket, dst);
 }
 
 // ------------------------------------------------------------------------
@@ -403,6 +488,13 @@ void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, con
   const dim3 blk(32, 8), grd = grid_r1(g);
   if (from_zero) k_r1<3><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
   else k_r1<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+}
+
+void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, RedWS& ws, cd* dst,
+                    cudaStream_t st) {
+  const long long ntiles = (long long)((g.nx + 31) / 32) * ((g.ny + NRW * RB - 1) / (NRW * RB));
+  const int grid = (int)(ntiles < kMaxPartials ? ntiles : kMaxPartials);
+  k_resnorm<<<grid, 32 * NRW, 0, st>>>(u, b, k, g, c, ws.partials, ws.ticket, dst);
 }
 
 }  // namespace hdb

@@ -143,6 +143,14 @@ class LevelOperator:
         check(lib().hdb_op_residual(self.handle, db.data_ptr(), du.data_ptr(), dout.data_ptr()))
         return dev.to_host(dout) if host else dout
 
+    def residual_norms(self, b, u):
+        """(||b - A u||, ||b||) from one fused pass (the MG divergence guard's
+        quantities, mg.py:131-138); the residual is not stored."""
+        _, (du, db) = self._io(u, b)
+        out = (C.c_double * 2)()
+        check(lib().hdb_op_resnorm(self.handle, db.data_ptr(), du.data_ptr(), out))
+        return float(np.sqrt(max(out[0], 0.0))), float(np.sqrt(max(out[1], 0.0)))
+
     def jacobi(self, x, b, omega=0.8):
         """One damped Jacobi sweep out of place (mg.py:88-102); x=None: from zero."""
         if x is None:

@@ -99,6 +99,26 @@ def test_operator_uniform_k_large_bitexact(level, bnd):
     np.testing.assert_array_equal(op.residual(b, u), b - ref.apply(u))
 
 
+@pytest.mark.parametrize("shape", [(129, 129), (600, 300), (1025, 1025)])
+@pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
+def test_fused_residual_norms_vs_oracle(shape, bnd):
+    """One-pass (||b - A u||, ||b||) (the MG guard kernel, no residual stored)
+    against the oracle's bit-exact residual, normed in numpy: the sums differ
+    only in summation order (rel. 1e-13)."""
+    rng = _rng(sum(shape))
+    ny, nx = shape
+    ksq = 900.0 + 500.0 * rng.random((ny, nx))
+    ksq[: ny // 3] = 700.0  # constant band: exercises the interior fast path too
+    op = hdb.radius1_operator(nx, ny, 1.0 / 256, ksq, bnd, complex(1.0, 0.5))
+    ref = oracle.CpuLevelOp(nx, ny, 1.0 / 256, ksq, bnd, *oracle.level_kernels(1)[:4], shift=complex(1.0, 0.5),
+                            level_scale=1.0)
+    u, b = _rand(rng, shape), _rand(rng, shape)
+    rn, bn = op.residual_norms(b, u)
+    r = b - ref.apply(u)
+    assert abs(rn - np.linalg.norm(r)) <= 1e-13 * np.linalg.norm(r)
+    assert abs(bn - np.linalg.norm(b)) <= 1e-13 * np.linalg.norm(b)
+
+
 def test_zero_in_zero_out_and_edge_shapes():
     for shape in ((3, 3), (5, 3), (3, 9)):
         ny, nx = shape

@@ -5,7 +5,7 @@ for one `ncu --set full` capture of all of them:
         -o gpurun_out/targets python tools/ncu_targets.py
 
 Fine level (4097^2): 5-point apply / residual / Jacobi (K1-K3), restriction,
-prolongation, dot.  Coarse levels: radius-3 apply on level 3 (1025^2),
+prolongation, dot, fused residual norm (MG guard).  Coarse levels: radius-3 apply on level 3 (1025^2),
 radius-2 apply on level 2 (2049^2).
 """
 import ctypes as C
@@ -44,6 +44,7 @@ def main():
     _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr()))               # k_prolong_s
     d = (C.c_double * 2)()
     L.hdb_dot(u.data_ptr(), out.data_ptr(), lv.npoints, d)                                    # k_dot
+    _lib.check(L.hdb_op_resnorm(mg.levels[0].op.handle, b.data_ptr(), u.data_ptr(), d))       # k_resnorm
     if hier.ml >= 3:
         for lvl in (3, 2):
             o = hdb.helmholtz_operator(hier, lvl)
