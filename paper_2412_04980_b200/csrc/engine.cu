@@ -22,7 +22,7 @@ Engine::Engine(int dev) : device(dev) {
   HDB_CUDA(cudaSetDevice(dev));
   HDB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   own_st = st;
-  HDB_CUDA(cudaMalloc(&red.partials, sizeof(cd) * kMaxPartials));
+  HDB_CUDA(cudaMalloc(&red.partials, sizeof(cd) * kMaxReduceBlocks));
   HDB_CUDA(cudaMalloc(&red.ticket, sizeof(unsigned)));
   HDB_CUDA(cudaMemset(red.ticket, 0, sizeof(unsigned)));
   HDB_CUDA(cudaMalloc(&dscal, sizeof(cd) * kScal));
@@ -36,6 +36,7 @@ Engine::~Engine() {
   if (own_st) st = own_st;
   delete comm;
   cudaFree(red.partials);
+  cudaFree(red.big);
   cudaFree(red.ticket);
   cudaFree(dscal);
   cudaFreeHost(hscal);
@@ -130,8 +131,14 @@ void LevelOp::resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const {
   Engine& E = engine();
   exchange(u, c.radius);
   if (c.radius == 1) {
-    launch_resnorm(c, g, u, b, ksq, E.red, slot, E.st);
-    E.launches++;
+    const long long G = resnorm_partials(g);
+    if (G > E.red.big_cap) {  // grows once per new largest level
+      E.free(E.red.big);
+      E.red.big = (cd*)E.alloc_bytes(sizeof(cd) * (size_t)G);
+      E.red.big_cap = G;
+    }
+    launch_resnorm(c, g, u, b, ksq, E.red.big, slot, E.st);
+    E.launches += 2;
   } else {
     launch_apply(c, g, u, b, ksq, scratch, 1, E.st);
     launch_dot(scratch, scratch, n, E.red, slot, E.st);
@@ -246,8 +253,10 @@ static long long env_ll(const char* name, long long dflt) {
 int resident_ortho() {
   static int o = -1;
   if (o < 0) {
+    // dgks (default): CGS + DGKS re-orthogonalisation; cgs2: always two passes; mgs: the reference's order
     const char* e = getenv("HDB_ORTHO");
-    o = (e && std::string(e) == "mgs") ? 0 : 1;
+    const std::string v = e ? e : "dgks";
+    o = v == "mgs" ? 0 : (v == "cgs2" ? 1 : 2);
   }
   return o;
 }

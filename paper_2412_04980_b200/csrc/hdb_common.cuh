@@ -70,7 +70,6 @@ struct OpCoef {
 };
 
 constexpr int kReduceThreads = 256;
-constexpr int kMaxReduceBlocks = 592;  // 4 x 148 SMs (dot / MGS grids)
-constexpr int kMaxPartials = 1184;     // 8 x 148 SMs (fused stencil-norm grids); partials capacity
+constexpr int kMaxReduceBlocks = 592;  // 4 x 148 SMs
 
 }  // namespace hdb

@@ -5,8 +5,10 @@
 namespace hdb {
 
 struct RedWS {  // per-stream reduction workspace
-  cd* partials = nullptr;   // kMaxPartials
+  cd* partials = nullptr;   // kMaxReduceBlocks
   unsigned* ticket = nullptr;
+  cd* big = nullptr;        // per-tile partials of the fused stencil norms (grown on demand)
+  long long big_cap = 0;
 };
 
 int reduce_blocks(long long n);
@@ -15,8 +17,9 @@ int reduce_blocks(long long n);
 void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out, int mode,
                   cudaStream_t st);
 // radius 1 only: dst = (||b - A u||^2, ||b||^2) in one pass (residual not stored)
-void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, RedWS& ws, cd* dst,
-                    cudaStream_t st);
+long long resnorm_partials(const Geom& g);  // partial slots launch_resnorm needs
+void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* partials,
+                    cd* dst, cudaStream_t st);
 void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out, double omega,
                    bool from_zero, cudaStream_t st);
 // transfer geometry: fine rows [f_row0, f_row0+f_ny) of nfy_g, coarse rows [c_row0, c_row0+c_ny) of ncy_g

@@ -374,12 +374,14 @@ __device__ __forceinline__ cd cdiv_(cd a, cd b) {
 
 // CGS pass: out = V[0..m)^H w (warp per basis vector over this CTA's points),
 // then w -= V out.  Returns with out[] reduced cluster/grid-wide in s.hv.
+// with_norm: element m of the reduction carries <w, w> of the incoming w
 template <class Sync>
 __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n, long long p0, int cnt, int m,
-                         int& buf, cd* gpart) {
+                         int& buf, cd* gpart, bool with_norm = false) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = wid; i < m; i += kRT / 32) {
-    const cd* vi = basis + (long long)i * n + p0;
+  const int mm = m + (with_norm ? 1 : 0);
+  for (int i = wid; i < mm; i += kRT / 32) {
+    const cd* vi = i < m ? basis + (long long)i * n + p0 : ws;
     cd a = mkc(0.0, 0.0);
 #pragma unroll 8
     for (int q = lane; q < cnt; q += 32) a = c_conjmul_acc(a, vi[q], ws[q]);
@@ -387,7 +389,7 @@ __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long 
     if (lane == 0) s.pv[i] = a;
   }
   __syncthreads();
-  sy.reduce_vec(s, m, s.hv, buf, gpart);
+  sy.reduce_vec(s, mm, s.hv, buf, gpart);
   for (int q = threadIdx.x; q < cnt; q += kRT) {
     cd w = ws[q];
     const cd* vq = basis + p0 + q;
@@ -549,7 +551,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
         if (t == 0) s.hcol[i] = h;
         for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
       }
-    } else {
+    } else if (ORTHO == 1) {
       // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
       // Hessenberg column in exact arithmetic, two reductions instead of j+1
       __syncthreads();
@@ -560,10 +562,40 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
       __syncthreads();
     }
-    PHASE(2);
-    cd a = mkc(0.0, 0.0);
-    for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
-    const double hn = sqrt(fmax(sy.reduce(a, s, buf, A.gpart).x, 0.0));
+    double hn;
+    if (ORTHO == 2) {
+      // CGS with DGKS re-orthogonalisation: one reduction carries V^H w and
+      // <w, w>; ||w'||^2 = <w, w> - sum |h_i|^2 (Pythagoras, V orthonormal).
+      // Only when that drops below half of <w, w> (cancellation: w close to
+      // span V) is a second pass made, whose reduction carries <w', w'> and
+      // the (tiny) corrections.  Same Hessenberg column in exact arithmetic;
+      // every CTA takes the same branch (identically reduced scalars).
+      __syncthreads();
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true);
+      double nw = s.hv[j + 1].x, sh = 0.0;
+      for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
+      __syncthreads();
+      for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
+      double est = nw - sh;
+      if (!(est > 0.5 * nw)) {
+        __syncthreads();
+        cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true);
+        nw = s.hv[j + 1].x;
+        sh = 0.0;
+        for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
+        __syncthreads();
+        for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
+        est = nw - sh;
+      }
+      __syncthreads();
+      PHASE(2);
+      hn = sqrt(fmax(est, 0.0));
+    } else {
+      PHASE(2);
+      cd a = mkc(0.0, 0.0);
+      for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+      hn = sqrt(fmax(sy.reduce(a, s, buf, A.gpart).x, 0.0));
+    }
     PHASE(3);
     // V_{j+1} = w / ||w|| (harmless if step j turns out to be the last)
     const double inv = 1.0 / hn;
@@ -782,7 +814,9 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
   a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
   if (ortho == 1 && cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
-  const bool ok = ortho ? launch_any<1>(mode, a, c.radius, st) : launch_any<0>(mode, a, c.radius, st);
+  if (ortho == 2 && cap + 2 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
+  const bool ok = ortho == 2 ? launch_any<2>(mode, a, c.radius, st)
+                  : ortho == 1 ? launch_any<1>(mode, a, c.radius, st) : launch_any<0>(mode, a, c.radius, st);
   return ok ? 0 : 1;
 }
 
@@ -1006,12 +1040,115 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid2(cd* w, const cd* const* V, in
     }
 }
 
+// TMA-fed form (levels whose w slice AND one basis-vector slice fit shared
+// memory together, e.g. the 1025^2 level of config 2): V_{i+1}'s slice is
+// streamed HBM -> shared memory by the bulk-copy engine (cp.async.bulk,
+// mbarrier completion) while step i computes its dot, waits in the grid
+// reduction and applies its update, so the basis stream overlaps the
+// synchronisation instead of following it.  V_i is pulled from shared memory
+// into registers (kept for the update), then the buffer is handed to the copy
+// engine for V_{i+1}.  Same arithmetic and reduction tree as k_mgs_grid.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+// thread 0: arm the barrier for `bytes` and issue the slice copy in 32 KB pieces
+__device__ __forceinline__ void issue_slice(cd* dst, const cd* src, int cnt, uint64_t* bar) {
+  const uint32_t bytes = (uint32_t)cnt * (uint32_t)sizeof(cd);
+  mbar_arm(bar, bytes);
+  constexpr uint32_t kPiece = 32768;
+  for (uint32_t off = 0; off < bytes; off += kPiece) {
+    const uint32_t nb = bytes - off < kPiece ? bytes - off : kPiece;
+    bulk_g2s(reinterpret_cast<unsigned char*>(dst) + off, reinterpret_cast<const unsigned char*>(src) + off, nb, bar);
+  }
+}
+
+struct MgsTSmem {
+  MgsSmem red;
+  uint64_t bar;
+};
+
+__global__ void __launch_bounds__(kRT) k_mgs_grid_t(cd* w, const cd* const* V, int j, long long n, cd* gpart,
+                                                    cd* hout, const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  MgsTSmem& s = *reinterpret_cast<MgsTSmem*>(smem_raw);
+  constexpr size_t kHead = ((sizeof(MgsTSmem) + 127) / 128) * 128;
+  cg::grid_group gr = cg::this_grid();
+  const int P = gridDim.x, rank = blockIdx.x, t = threadIdx.x;
+  const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
+  const int cnt = (int)(p1 - p0);
+  const int cap = (int)((n + P - 1) / P);
+  cd* ws = reinterpret_cast<cd*>(smem_raw + kHead);
+  cd* vb = ws + ((cap + 7) / 8) * 8;  // 128-byte aligned
+  if (t == 0) {
+    mbar_init(&s.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0 && cnt > 0) issue_slice(vb, V[0] + p0, cnt, &s.bar);
+  load_slice_smem(ws, w + p0, cnt);
+  int buf = 0;
+  uint32_t parity = 0;
+  for (int i = 0; i <= j; ++i) {
+    cd vr[kMgsPPT];
+    if (cnt > 0) {
+      mbar_wait(&s.bar, parity);
+      parity ^= 1u;
+    }
+#pragma unroll
+    for (int k = 0; k < kMgsPPT; ++k) {
+      const int q = t + k * kRT;
+      vr[k] = q < cnt ? vb[q] : mkc(0.0, 0.0);
+    }
+    __syncthreads();  // every thread holds its V_i values: the buffer is free
+    if (i < j && t == 0 && cnt > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_slice(vb, V[i + 1] + p0, cnt, &s.bar);
+    }
+    cd a = mkc(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < kMgsPPT; ++k) {
+      const int q = t + k * kRT;
+      if (q < cnt) a = c_conjmul_acc(a, vr[k], ws[q]);
+    }
+    const cd h = grid_reduce_small(a, s.red, buf, gpart, gr);
+    if (rank == 0 && t == 0) hout[i] = h;
+#pragma unroll
+    for (int k = 0; k < kMgsPPT; ++k) {
+      const int q = t + k * kRT;
+      if (q < cnt) ws[q] = c_sub(ws[q], c_mul_np(h, vr[k]));
+    }
+  }
+  __syncthreads();
+  cd a = mkc(0.0, 0.0);
+  for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+  const cd nn = grid_reduce_small(a, s.red, buf, gpart, gr);
+  if (rank == 0 && t == 0) hout[j + 1] = nn;
+  const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
+  const double inv = 1.0 / hn;
+  for (int q = t; q < cnt; q += kRT) {
+    const cd v = ws[q];
+    w[p0 + q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+  }
+}
+
+static size_t mgs_t_smem(long long chunk) {
+  const size_t head = ((sizeof(MgsTSmem) + 127) / 128) * 128;
+  return head + 2 * (size_t)((chunk + 7) / 8) * 8 * sizeof(cd);
+}
+
 // Launch plan of the cooperative MGS step for length n: 1 = k_mgs_grid (w in
 // registers + shared memory), 2 = k_mgs_grid2 with `ks` shared-memory slots,
 // 0 = does not fit (caller: launch chain).
 static int mgs_grid_plan(long long n, long long& ks_out) {
   init_limits();
   const long long chunk = (n + g_grid - 1) / g_grid;
+  static const bool tma = [] {
+    const char* e = getenv("HDB_MGS_TMA");
+    return !e || atoi(e) != 0;
+  }();
+  if (tma && chunk <= (long long)kMgsPPT * kRT && mgs_t_smem(chunk) <= g_smem_optin) return 3;
   const size_t sm = smem_for(chunk, false);
   if (sm <= g_smem_optin && chunk <= (long long)kMgsPPT * kRT * 2) return 1;
   // hybrid shared-memory + register slice of w; beyond those the slice stays in
@@ -1047,6 +1184,16 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
     int ksi = (int)ks;
     void* args2[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &ksi, (void*)&skip};
     return cudaLaunchCooperativeKernel((void*)k_mgs_grid2, dim3(g_grid), dim3(kRT), args2, sm2, st) == cudaSuccess ? 0 : 1;
+  }
+  if (plan == 3) {
+    const size_t sm3 = mgs_t_smem((n + g_grid - 1) / g_grid);
+    static size_t configured3 = 0;
+    if (sm3 > configured3) {
+      cudaFuncSetAttribute(k_mgs_grid_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+      configured3 = sm3;
+    }
+    void* args3[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, (void*)&skip};
+    return cudaLaunchCooperativeKernel((void*)k_mgs_grid_t, dim3(g_grid), dim3(kRT), args3, sm3, st) == cudaSuccess ? 0 : 1;
   }
   const size_t sm = smem_for((n + g_grid - 1) / g_grid, false);
   static size_t configured = 0;

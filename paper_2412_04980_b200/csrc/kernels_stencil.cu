@@ -195,47 +195,42 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
 // Fused residual norm (the MG divergence guard, mg.py:131-138, and any
 // ||b - A u|| that only needs the norm): dst = (||b - A u||^2, ||b||^2) as one
 // complex slot (re, im), read in one pass over u, b, k^2 (40 B/pt); the
-// residual itself is never stored.  Persistent walk over 32 x (8*RB) strip
-// tiles (block q takes tiles q, q + G, ...), interior tiles with the k_r1s
-// sliding window, boundary tiles per point; per-block partials are combined in
-// block order by the last block, so the result is deterministic for a grid.
+// residual itself is never stored.  One block per 32 x (NRW*RB) strip tile
+// (interior tiles with the k_r1s sliding window, boundary tiles per point),
+// per-tile partials in tile order, then one ordered sum (k_sum_partials):
+// deterministic for a given grid.
 constexpr int NRW = 4;  // warps per block (tile rows = NRW * RB)
 __global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, const cd* __restrict__ b,
-                                                 const double* __restrict__ k, Geom g, OpCoef c, cd* partials,
-                                                 unsigned* ticket, cd* dst) {
+                                                      const double* __restrict__ k, Geom g, OpCoef c, cd* partials) {
   const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-  const int ntx = (g.nx + 31) / 32, nty = (g.ny + NRW * RB - 1) / (NRW * RB);
-  const long long ntiles = (long long)ntx * nty;
   double rr = 0.0, bb = 0.0;
   const long long nx = g.nx;
-  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int bx = (int)(tile % ntx), by = (int)(tile / ntx);
-    const int i = bx * 32 + lane;
-    const int jbeg = (by * NRW + wy) * RB;
-    const int gi0 = bx * 32, gj0 = g.row0 + by * NRW * RB, gj1 = gj0 + NRW * RB;
-    const bool interior = gi0 >= 1 && gi0 + 32 <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
-                          by * NRW * RB + NRW * RB <= g.ny;
-    if (!interior) {
-      if (i < g.nx)
-        for (int r = 0; r < RB; ++r) {
-          const int j = jbeg + r;
-          if (j >= g.ny) break;
-          const int gj = j + g.row0;
-          const long long p = (long long)j * nx + i;
-          const cd bc = b[p], uc = u[p];
-          cd res;
-          if (pinned(g, c, gj, i)) {
-            res = c_sub(bc, uc);
-          } else {
-            const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
-                                     upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
-            res = c_sub(bc, Au);
-          }
-          rr = __fma_rn(res.x, res.x, rr); rr = __fma_rn(res.y, res.y, rr);
-          bb = __fma_rn(bc.x, bc.x, bb); bb = __fma_rn(bc.y, bc.y, bb);
+  const int bx = blockIdx.x, by = blockIdx.y;
+  const int i = bx * 32 + lane;
+  const int jbeg = (by * NRW + wy) * RB;
+  const int gi0 = bx * 32, gj0 = g.row0 + by * NRW * RB, gj1 = gj0 + NRW * RB;
+  const bool interior = gi0 >= 1 && gi0 + 32 <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
+                        by * NRW * RB + NRW * RB <= g.ny;
+  if (!interior) {
+    if (i < g.nx)
+      for (int r = 0; r < RB; ++r) {
+        const int j = jbeg + r;
+        if (j >= g.ny) break;
+        const int gj = j + g.row0;
+        const long long p = (long long)j * nx + i;
+        const cd bc = b[p], uc = u[p];
+        cd res;
+        if (pinned(g, c, gj, i)) {
+          res = c_sub(bc, uc);
+        } else {
+          const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
+                                   upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
+          res = c_sub(bc, Au);
         }
-      continue;
-    }
+        rr = __fma_rn(res.x, res.x, rr); rr = __fma_rn(res.y, res.y, rr);
+        bb = __fma_rn(bc.x, bc.x, bb); bb = __fma_rn(bc.y, bc.y, bb);
+      }
+  } else {
     const cd* up = u + (long long)jbeg * nx + i;
     const double* kp = k + (long long)jbeg * nx + i;
     const cd* bp = b + (long long)jbeg * nx + i;
@@ -270,7 +265,21 @@ __global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, 
     }
   }
   const cd part = block_sum<32 * NRW>(mkc(rr, bb));
-  grid_finish<32 * NRW>(part, partials, ticket, dst);
+  if (threadIdx.x == 0) partials[(long long)by * gridDim.x + bx] = part;
+}
+
+// ordered sum of G partials (one block): thread t adds t, t + T, ... in order,
+// then the fixed block tree
+constexpr int kSumThreads = 1024;
+__global__ void __launch_bounds__(kSumThreads) k_sum_partials(const cd* __restrict__ partials, long long G, cd* dst) {
+  cd v = mkc(0.0, 0.0);
+  for (long long q = threadIdx.x; q < G; q += kSumThreads) {
+    const cd z = partials[q];
+    v.x += z.x;
+    v.y += z.y;
+  }
+  v = block_sum<kSumThreads>(v);
+  if (threadIdx.x == 0) *dst = v;
 }
 
 // ------------------------------------------------------------------------
@@ -490,11 +499,14 @@ void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, con
   else k_r1<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
 }
 
-void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, RedWS& ws, cd* dst,
-                    cudaStream_t st) {
-  const long long ntiles = (long long)((g.nx + 31) / 32) * ((g.ny + NRW * RB - 1) / (NRW * RB));
-  const int grid = (int)(ntiles < kMaxPartials ? ntiles : kMaxPartials);
-  k_resnorm<<<grid, 32 * NRW, 0, st>>>(u, b, k, g, c, ws.partials, ws.ticket, dst);
+long long resnorm_partials(const Geom& g) {
+  return (long long)((g.nx + 31) / 32) * ((g.ny + NRW * RB - 1) / (NRW * RB));
+}
+void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* partials,
+                    cd* dst, cudaStream_t st) {
+  const dim3 grd((g.nx + 31) / 32, (g.ny + NRW * RB - 1) / (NRW * RB));
+  k_resnorm<<<grd, 32 * NRW, 0, st>>>(u, b, k, g, c, partials);
+  k_sum_partials<<<1, kSumThreads, 0, st>>>(partials, (long long)grd.x * grd.y, dst);
 }
 
 }  // namespace hdb

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("case", nargs="?", default="c2")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--levels", default="")
+    ap.add_argument("--tol", type=float, default=0.1)
+    ap.add_argument("--cap", type=int, default=0)
     a = ap.parse_args()
     import torch
     prob = bench.CONFIGS[a.case][1](hdb)
@@ -41,7 +43,7 @@ def main():
         row = {"points": op.npoints, "cap": pol.cslp_stop.max_iters}
         for mode in (-1, 0, 1):
             its, rel = C.c_int(), C.c_double()
-            st = L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), 0.1, pol.cslp_stop.max_iters, mode,
+            st = L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), a.tol, a.cap or pol.cslp_stop.max_iters, mode,
                                 C.byref(its), C.byref(rel))
             if st != 0:
                 row[str(mode)] = L.hdb_last_error().decode()[:60]
@@ -49,14 +51,14 @@ def main():
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(a.reps):
-                L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), 0.1, pol.cslp_stop.max_iters, mode,
+                L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), a.tol, a.cap or pol.cslp_stop.max_iters, mode,
                                C.byref(its), C.byref(rel))
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) / a.reps * 1e3
             prof = (C.c_longlong * 8)()
             if mode >= 0:
                 L.hdb_resident_profile(1, None)
-                L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), 0.1, pol.cslp_stop.max_iters, mode,
+                L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), a.tol, a.cap or pol.cslp_stop.max_iters, mode,
                                C.byref(its), C.byref(rel))
                 L.hdb_resident_profile(0, prof)
             row[str(mode) + "_phase_us"] = [round(v / 1.965e3, 1) for v in prof[:6]]

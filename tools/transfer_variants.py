@@ -60,9 +60,8 @@ def child():
 
 
 def main():
-    modes = [("R2", {"HDB_RESTRICT": "2"}), ("R3", {"HDB_RESTRICT": "3"}), ("R4", {"HDB_RESTRICT": "4"}),
-             ("R5", {"HDB_RESTRICT": "5"}), ("P1", {"HDB_PROLONG": "1"}), ("P2", {"HDB_PROLONG": "2"}),
-             ("P3", {"HDB_PROLONG": "3"}), ("R0P0", {"HDB_RESTRICT": "0", "HDB_PROLONG": "0"})]
+    modes = [("R3", {"HDB_RESTRICT": "3"}), ("R4", {"HDB_RESTRICT": "4"}), ("R5", {"HDB_RESTRICT": "5"}),
+             ("R6", {"HDB_RESTRICT": "6"})]
     for name, env in modes:
         e = dict(os.environ)
         e.update(env)
