@@ -194,6 +194,11 @@ def kernel_roofline(hdb, hier, reps=20):
     res["restrict"] = (20.0 * n, t)
     t = timeit(lambda: _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr())))
     res["prolong"] = (20.0 * n, t)
+    # reference streams (torch kernels, not ours): pure write and read+write copy of one fine vector
+    t = timeit(lambda: out.fill_(0.5))
+    res["ref_write_only(torch fill)"] = (16.0 * n, t)
+    t = timeit(lambda: out.copy_(u))
+    res["ref_copy(torch)"] = (32.0 * n, t)
     t = timeit(lambda: _lib.check(L.hdb_dot(u.data_ptr(), out.data_ptr(), n, None)))  # device-resident result
     res["dot"] = (32.0 * n, t)
     # fused matvec + residual + norms (MG divergence guard): one pass, residual not stored

@@ -397,8 +397,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     // MGS chain (krylov.py:121-124): one cooperative launch on large levels,
     // else one fused launch per coefficient
     bool coop = false;
-    if (!shard && n >= coop_mgs_min()) {
-      if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
+    auto ensure_dv = [&] {
       if (ws.dV_cap < j + 1) {
         E.free(ws.dV);
         ws.dV_cap = std::max(2 * (j + 1), 64);
@@ -406,11 +405,14 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
         ws.dV_n = 0;
       }
       while (ws.dV_n < j + 1) {  // append V pointers (their addresses never change)
-        cd* p = ws.v(ws.dV_n);
+        ws.v(ws.dV_n);           // (allocates the vector if it does not exist yet)
         HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, &ws.V[ws.dV_n], sizeof(cd*), cudaMemcpyHostToDevice, E.st));
-        (void)p;
         ws.dV_n++;
       }
+    };
+    if (!shard && n >= coop_mgs_min()) {
+      if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
+      ensure_dv();
       coop = launch_mgs_grid(w, (const cd* const*)ws.dV, j, n, ws.gpart, E.dscal + kSlotH, E.st) == 0;
       if (coop) E.launches++;
     }

@@ -294,6 +294,9 @@ struct ClusterSync {
   __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd*) { gather_sum(s, m, out, buf); }
 };
 
+constexpr int kGridRounds = 5;  // ceil(148 SMs / 32): partial loads per lane in the grid reductions
+static_assert(32 * kGridRounds >= 148, "grid reductions assume <= 160 CTAs");
+
 struct GridSync {
   static constexpr bool kGather = false;
   static constexpr int kVecMax = kVecCap;
@@ -325,11 +328,18 @@ struct GridSync {
       cd* sums = gpart + 2LL * P * kVecCap + (long long)buf * kVecCap;  // published element sums
       for (int i = blockIdx.x; i < m; i += P) {
         if (threadIdx.x < 32) {
+          // all of this lane's partials in flight at once (P <= 32 * kGridRounds), then summed in rank order
+          cd z[kGridRounds];
+#pragma unroll
+          for (int u = 0; u < kGridRounds; ++u) {
+            const int r = threadIdx.x + 32 * u;
+            z[u] = r < P ? __ldcg(&col[(long long)r * kVecCap + i]) : mkc(0.0, 0.0);
+          }
           cd q = mkc(0.0, 0.0);
-          for (int r = threadIdx.x; r < P; r += 32) {
-            const cd z = __ldcg(&col[(long long)r * kVecCap + i]);
-            q.x += z.x;
-            q.y += z.y;
+#pragma unroll
+          for (int u = 0; u < kGridRounds; ++u) {
+            q.x += z[u].x;
+            q.y += z[u].y;
           }
           q = warp_sum_c(q);
           if (threadIdx.x == 0) __stcg(&sums[i], q);
@@ -348,11 +358,17 @@ struct GridSync {
     gr.sync();
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
+      cd z[kGridRounds];
+#pragma unroll
+      for (int u = 0; u < kGridRounds; ++u) {
+        const int r = lane + 32 * u;
+        z[u] = r < P ? __ldcg(&gpart[((long long)buf * P + r) * kVecCap]) : mkc(0.0, 0.0);
+      }
       cd q = mkc(0.0, 0.0);
-      for (int r = lane; r < P; r += 32) {
-        const cd z = __ldcg(&gpart[((long long)buf * P + r) * kVecCap]);
-        q.x += z.x;
-        q.y += z.y;
+#pragma unroll
+      for (int u = 0; u < kGridRounds; ++u) {
+        q.x += z[u].x;
+        q.y += z[u].y;
       }
       q = warp_sum_c(q);
       if (lane == 0) s.bcast[buf] = q;
@@ -708,7 +724,7 @@ static void init_limits() {
   cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   g_smem_optin = (size_t)v;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  g_grid = v;
+  g_grid = v > 32 * kGridRounds ? 32 * kGridRounds : v;  // reductions batch <= 32 * kGridRounds partials
 }
 
 template <class K>
@@ -1101,16 +1117,18 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid_t(cd* w, const cd* const* V, i
       const int q = t + k * kRT;
       vr[k] = q < cnt ? vb[q] : mkc(0.0, 0.0);
     }
-    __syncthreads();  // every thread holds its V_i values: the buffer is free
-    if (i < j && t == 0 && cnt > 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_slice(vb, V[i + 1] + p0, cnt, &s.bar);
-    }
     cd a = mkc(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < kMgsPPT; ++k) {
       const int q = t + k * kRT;
       if (q < cnt) a = c_conjmul_acc(a, vr[k], ws[q]);
+    }
+    // every thread has CONSUMED its V_i values (the dot above), so no shared
+    // load from the buffer is still in flight: hand it to the copy engine
+    __syncthreads();
+    if (i < j && t == 0 && cnt > 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_slice(vb, V[i + 1] + p0, cnt, &s.bar);
     }
     const cd h = grid_reduce_small(a, s.red, buf, gpart, gr);
     if (rank == 0 && t == 0) hout[i] = h;

@@ -193,6 +193,7 @@ constexpr uint32_t kTBoxBytes = 2u * TBC * 16u;
 template <int TST>
 struct TRing {
   uint64_t full[TST], empty[TST];
+  double scratch[64];  // consumer-side release dependencies
 };
 __device__ __forceinline__ uint32_t s_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
@@ -288,11 +289,18 @@ __global__ void __launch_bounds__(96) k_restrict_t(const __grid_constant__ CUten
     cd v0[5], v1[5];
     srow_taps(v0, r0, col, lane);
     srow_taps(v1, r0 + TBC, col, lane);
+    cd pr[5], pr1[5];
+    wprod(pr, v0, kW16(0));
+    wprod(pr1, v1, kW16(1));
+    // The stage is released only once every value read from it has been
+    // consumed: this scratch store depends on all of them (the products of the
+    // lane-0 / lane-31 halo loads included), so no shared load can still be in
+    // flight when the copy engine refills the stage.
+    rb.scratch[threadIdx.x] = __dadd_rn(__dadd_rn(__dadd_rn(pr[0].x, pr[1].x), pr[4].x),
+                                        __dadd_rn(__dadd_rn(pr1[0].x, pr1[1].x), pr1[4].x));
     __syncwarp();
     if (lane == 0) bar_arrive(&rb.empty[q]);
-    cd pr[5];
     // even row 2p: b = 4 -> A0, b = 2 -> A1, b = 0 -> A2 (w_4 = w_0)
-    wprod(pr, v0, kW16(0));
     if (p >= 2) wacc(A0, pr);
     if (p >= 1 && p - 1 < TSR) {
       cd p2[5];
@@ -307,9 +315,8 @@ __global__ void __launch_bounds__(96) k_restrict_t(const __grid_constant__ CUten
     }
     // odd row 2p+1: b = 3 -> A1, b = 1 -> A2 (w_3 = w_1); not needed in the last pair
     if (p + 1 < np) {
-      wprod(pr, v1, kW16(1));
-      if (p >= 1 && p - 1 < TSR) wacc(A1, pr);
-      if (p < TSR) wacc(A2, pr);
+      if (p >= 1 && p - 1 < TSR) wacc(A1, pr1);
+      if (p < TSR) wacc(A2, pr1);
     }
     A0 = A1;
     A1 = A2;
@@ -386,7 +393,202 @@ static bool launch_restrict_t(const cd* fine, cd* coarse, const TGeom& t, int ze
   if (variant == 4) launch_restrict_tk<4, 32>(m, coarse, t, zero_mask, st);
   else if (variant == 5) launch_restrict_tk<3, 32>(m, coarse, t, zero_mask, st);
   else if (variant == 6) launch_restrict_tk<4, 16>(m, coarse, t, zero_mask, st);
-  else launch_restrict_tk<8, 32>(m, coarse, t, zero_mask, st);
+  else launch_restrict_tk<3, 32>(m, coarse, t, zero_mask, st);  // default: 3 stages (more CTAs per SM beat deeper rings, measured)
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// TMA-staged prolongation (fine levels).  A CTA owns 62 coarse columns (two
+// consumer warps, lane = coarse column) and a strip of PSR coarse rows; the
+// producer warp's lane 0 streams coarse rows cy0-1 .. cy0+PSR (box 128
+// doubles = coarse columns cx0-1 .. cx0+62; columns / rows outside the grid
+// arrive as zeros, whose +0 terms leave every sum unchanged -- the reference
+// drops them) and, for the accumulate form, the two base rows of each output
+// pair.  Consumers keep a 3-row register window, form the fine rows 2cy and
+// 2cy+1 (E = 2cx, O = 2cx+1, (b, a) term order of k_prolong: bit-identical),
+// stage them in shared memory and one thread writes them back with a tensor
+// store (clipped at the grid edge), double-buffered against the next pair.
+constexpr int PSR = 32;                    // coarse rows per CTA
+constexpr int PST = 4;                     // ring stages
+constexpr int PCC = 62;                    // coarse columns per CTA
+constexpr int POB = 2 * PCC;               // fine points per staged output row (124)
+constexpr uint32_t kPCoarseBytes = 128u * 8u;          // one coarse row box (64 points)
+constexpr uint32_t kPBaseBytes = 2u * POB * 16u;        // two base rows
+struct PRing {
+  uint64_t full[PST], empty[PST];
+};
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(s_addr(src)) : "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+__global__ void __launch_bounds__(96) k_prolong_t(const __grid_constant__ CUtensorMap cmap,
+                                                  const __grid_constant__ CUtensorMap bmap,
+                                                  const __grid_constant__ CUtensorMap fmap, TGeom t, int cy_lo,
+                                                  int cy_cnt, int accumulate) {
+  extern __shared__ __align__(128) unsigned char psm[];
+  // layout: coarse ring (PST x 1 KB) | base ring (PST x 3968 B, accumulate) | out (2 x 3968 B) | 2 scratch | barriers
+  cd* cring = reinterpret_cast<cd*>(psm);
+  cd* bring = reinterpret_cast<cd*>(psm + PST * kPCoarseBytes);
+  cd* obuf = reinterpret_cast<cd*>(psm + PST * (kPCoarseBytes + kPBaseBytes));
+  PRing& rb = *reinterpret_cast<PRing*>(psm + PST * (kPCoarseBytes + kPBaseBytes) + 2 * kPBaseBytes + 2 * sizeof(cd));
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cx0 = blockIdx.x * PCC;
+  const int k0 = blockIdx.y * PSR;
+  const int cy0 = cy_lo + k0;                   // first coarse row (global)
+  const int nrow = min(PSR, cy_cnt - k0);       // output coarse rows of this strip
+  const int nitems = nrow + 2;                  // coarse rows cy0-1 .. cy0+nrow
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < PST; ++q) {
+      bar_init(&rb.full[q], 1);
+      bar_init(&rb.empty[q], 2);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (wid == 2) {  // producer
+    if (lane == 0) {
+      for (int k = 0; k < nitems; ++k) {
+        const int q = k % PST;
+        if (k >= PST) bar_wait(&rb.empty[q], (uint32_t)((k / PST - 1) & 1));
+        const bool wb = accumulate && k >= 2;
+        bar_arm(&rb.full[q], kPCoarseBytes + (wb ? kPBaseBytes : 0u));
+        tma_load_2d(cring + (size_t)q * 64, &cmap, 2 * (cx0 - 1), cy0 - 1 + k, &rb.full[q]);
+        if (wb) tma_load_2d(bring + (size_t)q * 2 * POB, &bmap, 4 * cx0, 2 * (cy0 + k - 2), &rb.full[q]);
+      }
+    }
+    return;
+  }
+  const int cc = min(wid * 32 + lane, PCC - 1);  // idle lanes (62, 63) mirror column 61 (never stored)
+  const bool live = wid * 32 + lane < PCC;
+  cd L0, C0, R0, L1, C1, R1;
+  // window rows cy0-1 (item 0) and cy0 (item 1).  A stage is released only
+  // after the values read from it have been consumed by arithmetic (a shared
+  // load still in flight must not race the copy engine refilling the stage),
+  // so items 0 and 1 are released after output 0.
+  for (int k = 0; k < 2; ++k) {
+    bar_wait(&rb.full[k], 0);
+    const cd* row = cring + (size_t)k * 64;
+    if (k == 0) { L0 = row[cc]; C0 = row[cc + 1]; R0 = row[cc + 2]; }
+    else { L1 = row[cc]; C1 = row[cc + 1]; R1 = row[cc + 2]; }
+  }
+  const double w0 = kW8(0), w1 = kW8(1), w2 = kW8(2), w3 = kW8(3), w4 = kW8(4);
+#pragma unroll 1
+  for (int i = 0; i < nrow; ++i) {
+    const int k = i + 2, q = k % PST;
+    bar_wait(&rb.full[q], (uint32_t)((k / PST) & 1));
+    const cd* row = cring + (size_t)q * 64;
+    const cd L2 = row[cc], C2 = row[cc + 1], R2 = row[cc + 2];  // coarse row cy+1
+    cd bE0, bO0, bE1, bO1;
+    if (accumulate) {
+      const cd* br = bring + (size_t)q * 2 * POB;
+      bE0 = br[2 * cc]; bO0 = br[2 * cc + 1]; bE1 = br[POB + 2 * cc]; bO1 = br[POB + 2 * cc + 1];
+    }
+    // fine row 2cy: b = 0 -> cy+1, b = 2 -> cy, b = 4 -> cy-1;  E: a = 0, 2, 4 (R, C, L), O: a = 1, 3 (R, C)
+    double er = 0.0, ei = 0.0, orr = 0.0, oi = 0.0;
+#define PT(wb, LL, CC_, RR)                                                                                  \
+    er = __dadd_rn(er, __dmul_rn((wb) * w0, RR.x)); ei = __dadd_rn(ei, __dmul_rn((wb) * w0, RR.y));           \
+    er = __dadd_rn(er, __dmul_rn((wb) * w2, CC_.x)); ei = __dadd_rn(ei, __dmul_rn((wb) * w2, CC_.y));         \
+    er = __dadd_rn(er, __dmul_rn((wb) * w4, LL.x)); ei = __dadd_rn(ei, __dmul_rn((wb) * w4, LL.y));           \
+    orr = __dadd_rn(orr, __dmul_rn((wb) * w1, RR.x)); oi = __dadd_rn(oi, __dmul_rn((wb) * w1, RR.y));         \
+    orr = __dadd_rn(orr, __dmul_rn((wb) * w3, CC_.x)); oi = __dadd_rn(oi, __dmul_rn((wb) * w3, CC_.y));
+    PT(w0, L2, C2, R2)
+    PT(w2, L1, C1, R1)
+    PT(w4, L0, C0, R0)
+    cd E0 = mkc(er, ei), O0 = mkc(orr, oi);
+    er = ei = orr = oi = 0.0;
+    PT(w1, L2, C2, R2)
+    PT(w3, L1, C1, R1)
+#undef PT
+    cd E1 = mkc(er, ei), O1 = mkc(orr, oi);
+    if (accumulate) {
+      E0 = mkc(__dadd_rn(bE0.x, E0.x), __dadd_rn(bE0.y, E0.y));
+      O0 = mkc(__dadd_rn(bO0.x, O0.x), __dadd_rn(bO0.y, O0.y));
+      E1 = mkc(__dadd_rn(bE1.x, E1.x), __dadd_rn(bE1.y, E1.y));
+      O1 = mkc(__dadd_rn(bO1.x, O1.x), __dadd_rn(bO1.y, O1.y));
+    }
+    // stage and store: the store that last read this buffer (pair i-2) has been
+    // waited for by thread 0 before the previous iteration's closing barrier
+    cd* ob = obuf + (size_t)(i & 1) * 2 * POB;
+    named_sync(1, 64);
+    if (live) {
+      ob[2 * cc] = E0; ob[2 * cc + 1] = O0;
+      ob[POB + 2 * cc] = E1; ob[POB + 2 * cc + 1] = O1;
+    } else {
+      obuf[4 * POB + (wid * 32 + lane - PCC)] = E0;  // idle lanes: scratch slots after both buffers
+    }
+    // Release stage q (and, at i = 0, items 0 and 1) only now: these shared
+    // stores depend on every value read from the stage, so no shared load can
+    // still be in flight when the copy engine refills it.
+    __syncwarp();
+    if (lane == 0) {
+      bar_arrive(&rb.empty[q]);
+      if (i == 0) { bar_arrive(&rb.empty[0]); bar_arrive(&rb.empty[1]); }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    named_sync(1, 64);
+    if (threadIdx.x == 0) {
+      tma_store_2d(&fmap, 4 * cx0, 2 * (cy0 + i), ob);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    }
+    L0 = L1; C0 = C1; R0 = R1;
+    L1 = L2; C1 = C2; R1 = R2;
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static bool map2d(CUtensorMap* m, const cd* base_row0, int ncols, int nrows, uint32_t box_doubles, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {2 * (cuuint64_t)ncols, (cuuint64_t)nrows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ncols * 16};
+  const cuuint32_t box[2] = {box_doubles, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base_row0, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+struct PMapEntry {
+  const cd *c, *b, *f;
+  int nfx, nfy_g, f_row0, c_row0;
+  CUtensorMap cm, bm, fm;
+};
+static bool launch_prolong_t(const cd* coarse, const cd* base, cd* fine, const TGeom& t, int accumulate,
+                             cudaStream_t st) {
+  static thread_local PMapEntry cache[32];
+  static thread_local int n = 0, next = 0;
+  PMapEntry* e = nullptr;
+  for (int i = 0; i < n && !e; ++i)
+    if (cache[i].c == coarse && cache[i].b == base && cache[i].f == fine && cache[i].nfx == t.nfx &&
+        cache[i].nfy_g == t.nfy_g && cache[i].f_row0 == t.f_row0 && cache[i].c_row0 == t.c_row0)
+      e = &cache[i];
+  if (!e) {
+    PMapEntry ne;
+    ne.c = coarse; ne.b = base; ne.f = fine; ne.nfx = t.nfx; ne.nfy_g = t.nfy_g; ne.f_row0 = t.f_row0;
+    ne.c_row0 = t.c_row0;
+    const cd* c0 = coarse - (long long)t.c_row0 * t.ncx;  // global coarse row 0
+    const cd* f0 = fine - (long long)t.f_row0 * t.nfx;
+    const cd* b0 = base ? base - (long long)t.f_row0 * t.nfx : f0;
+    if (!map2d(&ne.cm, c0, t.ncx, t.ncy_g, 128, 1) || !map2d(&ne.bm, b0, t.nfx, t.nfy_g, 2 * POB, 2) ||
+        !map2d(&ne.fm, f0, t.nfx, t.nfy_g, 2 * POB, 2))
+      return false;
+    cache[next] = ne;
+    e = &cache[next];
+    next = (next + 1) % 32;
+    if (n < 32) ++n;
+  }
+  constexpr size_t smem = PST * (kPCoarseBytes + kPBaseBytes) + 2 * kPBaseBytes + 2 * sizeof(cd) + sizeof(PRing);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_prolong_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  const int cy_lo = t.f_row0 / 2, cy_hi = (t.f_row0 + t.f_ny - 1) / 2;
+  const int cnt = cy_hi - cy_lo + 1;
+  const dim3 grd((t.ncx + PCC - 1) / PCC, (cnt + PSR - 1) / PSR);
+  k_prolong_t<<<grd, 96, smem, st>>>(e->cm, e->bm, e->fm, t, cy_lo, cnt, accumulate);
   return true;
 }
 
@@ -602,9 +804,11 @@ void launch_restrict(const cd* fine, cd* coarse, const TGeom& t, int zero_mask, 
 void launch_prolong(const cd* coarse, const cd* base, cd* fine, const TGeom& t, int accumulate, cudaStream_t st) {
   static const int pmode = [] {
     const char* e = getenv("HDB_PROLONG");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 3;
   }();
-  if (pmode >= 2 && t.ncx >= 256 && t.f_ny >= 256) {
+  // TMA-staged form on large grids (its per-strip pipeline latency does not pay on small ones)
+  if (pmode == 3 && t.ncx >= 1024 && t.f_ny >= 1024 && launch_prolong_t(coarse, base, fine, t, accumulate, st)) return;
+  if (pmode == 2 && t.ncx >= 256 && t.f_ny >= 256) {
     const int cy_lo = t.f_row0 / 2, cy_hi = (t.f_row0 + t.f_ny - 1) / 2;
     const int cnt = cy_hi - cy_lo + 1;
     const dim3 grd((t.ncx + 63) / 64, (cnt + PHB - 1) / PHB);

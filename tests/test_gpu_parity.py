@@ -147,6 +147,27 @@ def test_transfers_large_vs_oracle_and_adjoint():
     assert abs(lhs - rhs) <= 1e-12 * abs(rhs)
 
 
+@pytest.mark.parametrize("shape", [(2049, 2561), (4097, 2049)])
+def test_transfers_tma_sizes_bitexact_vs_oracle(shape):
+    """Grids large enough for the TMA-staged transfer kernels (tensor-map zero
+    fill at the edges, partial CTA column blocks and strips): bit-identical to
+    the oracle, overwrite and accumulate forms, and with coarse zero rows."""
+    rng = _rng(sum(shape))
+    ny, nx = shape
+    cy, cx = (ny - 1) // 2 + 1, (nx - 1) // 2 + 1
+    v = _rand(rng, shape)
+    c = _rand(rng, (cy, cx))
+    base = _rand(rng, shape)
+    r = oracle.restrict(v)
+    np.testing.assert_array_equal(hdb.restrict_array(v), r)
+    rz = r.copy()
+    rz[:, 0] = rz[:, -1] = rz[0, :] = rz[-1, :] = 0  # zero_mask 15: coarse Dirichlet rows
+    np.testing.assert_array_equal(hdb.restrict_array(v, zero_mask=15), rz)
+    p = oracle.prolong(c, shape)
+    np.testing.assert_array_equal(hdb.prolong_array(c, shape), p)
+    np.testing.assert_array_equal(hdb.prolong_array(c, shape, base=base), base + p)
+
+
 # ------------------------------------------------------------ jacobi / MG
 @pytest.mark.parametrize("name", ["mp1s65", "mp1d65div", "poisson65", "wedge145"])
 def test_jacobi_bitexact_and_vcycle(name):

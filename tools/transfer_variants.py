@@ -60,8 +60,8 @@ def child():
 
 
 def main():
-    modes = [("R3", {"HDB_RESTRICT": "3"}), ("R4", {"HDB_RESTRICT": "4"}), ("R5", {"HDB_RESTRICT": "5"}),
-             ("R6", {"HDB_RESTRICT": "6"})]
+    modes = [("R3P3", {"HDB_RESTRICT": "3", "HDB_PROLONG": "3"}), ("R3P1", {"HDB_RESTRICT": "3", "HDB_PROLONG": "1"}),
+             ("R0P0", {"HDB_RESTRICT": "0", "HDB_PROLONG": "0"})]
     for name, env in modes:
         e = dict(os.environ)
         e.update(env)
