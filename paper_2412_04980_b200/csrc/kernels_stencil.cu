@@ -342,6 +342,94 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
   out[p] = MODE == 0 ? acc : c_sub(b[p], acc);
 }
 
+// Vertically register-blocked form (radius 3 on large grids): each thread owns
+// the outputs (y, x) and (y+1, x).  Tile row r (r = 0 .. 2R+1) is loaded once
+// (2R+1 values of u, and of k^2 on heterogeneous levels) and feeds tap row a = r
+// of the upper output and a = r-1 of the lower one, so every output still
+// receives its taps in the reference's row-major (a, b) order (bit-identical),
+// while the shared-memory loads per output drop from (2R+1)^2 to
+// (2R+2)(2R+1)/2.  Tile: 32 x 16 outputs (256 threads).
+constexpr int VTY = 8, VROWS = 2 * VTY;
+template <int R, int MODE>
+__global__ void __launch_bounds__(TX * VTY) k_rgv(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                 const double* __restrict__ k, cd* __restrict__ out, Geom g,
+                                                 OpCoef c) {
+  if (c.skip && *c.skip) return;
+  constexpr int W = TX + 2 * R, H = VROWS + 2 * R, N = 2 * R + 1;
+  __shared__ cd su[H][W];
+  __shared__ double sk[H][W];
+  const int i0 = blockIdx.x * TX, j0 = blockIdx.y * VROWS;
+  const bool fast = c.uniform && i0 >= R && i0 + TX + R <= g.nx && g.row0 + j0 >= R &&
+                    g.row0 + j0 + VROWS + R <= g.nyg;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  for (int t = tid; t < H * W; t += TX * VTY) {
+    const int ty = t / W, tx = t % W;
+    const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+    if (fast) {
+      su[ty][tx] = U(u, g, gj, gi);
+    } else {
+      su[ty][tx] = upad(u, k, g, c, gj, gi);
+      sk[ty][tx] = kpad(k, g, c, gj, gi);
+    }
+  }
+  __syncthreads();
+  const int ly = 2 * threadIdx.y, lx = threadIdx.x;  // upper output at tile (ly, lx)
+  cd a0 = mkc(0.0, 0.0), a1 = mkc(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r <= N; ++r) {
+    cd uv[N];
+#pragma unroll
+    for (int bb = 0; bb < N; ++bb) uv[bb] = su[ly + r][lx + bb];
+    if (fast) {
+      if (r < N) {
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) a0 = c_add(a0, c_mul(c.ucoef[r * N + bb], uv[bb]));
+      }
+      if (r >= 1) {
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) a1 = c_add(a1, c_mul(c.ucoef[(r - 1) * N + bb], uv[bb]));
+      }
+    } else {
+      double kv[N];
+#pragma unroll
+      for (int bb = 0; bb < N; ++bb) kv[bb] = sk[ly + r][lx + bb];
+      if (r < N) {
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) {
+          const cd m = c.mass[r * N + bb];
+          const cd coef = mkc(__dadd_rn(c.lap[r * N + bb], __dmul_rn(m.x, kv[bb])), __dmul_rn(m.y, kv[bb]));
+          a0 = c_add(a0, c_mul(coef, uv[bb]));
+        }
+      }
+      if (r >= 1) {
+#pragma unroll
+        for (int bb = 0; bb < N; ++bb) {
+          const cd m = c.mass[(r - 1) * N + bb];
+          const cd coef =
+              mkc(__dadd_rn(c.lap[(r - 1) * N + bb], __dmul_rn(m.x, kv[bb])), __dmul_rn(m.y, kv[bb]));
+          a1 = c_add(a1, c_mul(coef, uv[bb]));
+        }
+      }
+    }
+  }
+  const int i = i0 + lx;
+  if (i >= g.nx) return;
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    const int j = j0 + ly + o;
+    if (j >= g.ny) return;
+    const int gj = j + g.row0;
+    const long long p = (long long)j * g.nx + i;
+    const cd acc = o == 0 ? a0 : a1;
+    if (pinned(g, c, gj, i)) {
+      const cd uc = su[ly + o + R][lx + R];
+      out[p] = MODE == 0 ? uc : c_sub(b[p], uc);
+    } else {
+      out[p] = MODE == 0 ? acc : c_sub(b[p], acc);
+    }
+  }
+}
+
 // Horizontally blocked radius-2 form for large grids (radius 3 keeps k_rg: its
 // 49-tap body is already FP64/shared-memory co-limited and blocking measured
 // slower): each thread owns HX
@@ -474,6 +562,16 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
   if (blocked && c.radius == 2 && g.nx >= 256 && g.ny >= 64) {
     if (mode == 0) launch_rgh<2, 0>(c, g, u, b, k, out, st);
     else launch_rgh<2, 1>(c, g, u, b, k, out, st);
+    return;
+  }
+  static const bool vblock = [] {
+    const char* e = getenv("HDB_RG_VBLOCK");
+    return !e || atoi(e) != 0;
+  }();
+  if (vblock && c.radius == 3 && g.nx >= 64 && g.ny >= 64) {
+    const dim3 blk(TX, VTY), grd((g.nx + TX - 1) / TX, (g.ny + VROWS - 1) / VROWS);
+    if (mode == 0) k_rgv<3, 0><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
+    else k_rgv<3, 1><<<grd, blk, 0, st>>>(u, b, k, out, g, c);
     return;
   }
   const dim3 blk(TX, TY), grd((g.nx + TX - 1) / TX, (g.ny + TY - 1) / TY);

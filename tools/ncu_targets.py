@@ -40,8 +40,9 @@ def main():
     _lib.check(L.hdb_op_apply(op.handle, u.data_ptr(), out.data_ptr()))                       # k_r1s<0>
     _lib.check(L.hdb_op_residual(op.handle, b.data_ptr(), u.data_ptr(), out.data_ptr()))      # k_r1s<1>
     _lib.check(L.hdb_op_jacobi(mg.levels[0].op.handle, u.data_ptr(), b.data_ptr(), out.data_ptr(), 0.8))  # k_r1s<2>
-    _lib.check(L.hdb_restrict(u.data_ptr(), lv.ny, lv.nx, c.data_ptr(), 0))                   # k_restrict_s
-    _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr()))               # k_prolong_s
+    _lib.check(L.hdb_restrict(u.data_ptr(), lv.ny, lv.nx, c.data_ptr(), 0))                   # k_restrict_t
+    _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr()))               # k_prolong_t
+    _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, b.data_ptr(), out.data_ptr()))       # k_prolong_t (+ base)
     d = (C.c_double * 2)()
     L.hdb_dot(u.data_ptr(), out.data_ptr(), lv.npoints, d)                                    # k_dot
     _lib.check(L.hdb_op_resnorm(mg.levels[0].op.handle, b.data_ptr(), u.data_ptr(), d))       # k_resnorm
