@@ -132,8 +132,8 @@ int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_ite
                  int* iterations, double* final_relres);
 
 /* telemetry: enable=1 zeroes and arms per-phase cycle counters of the
- * device-resident solver; enable=0 disarms and copies the 8 counters out     */
-int hdb_resident_profile(int enable, long long* host_out8);
+ * device-resident solver; enable=0 disarms and copies the 12 counters out    */
+int hdb_resident_profile(int enable, long long* host_out12);
 
 /* ---- MADP solver: replaces MadpSolver (madp.py:220-371) ------------------- */
 int hdb_solver_create(hdb_solver** out, int ml, double outer_tol, int outer_max);

@@ -358,16 +358,17 @@ int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_ite
 
 // telemetry: per-phase cycle counters of device-resident solves (CTA 0, thread 0)
 static long long* g_phase = nullptr;
-int hdb_resident_profile(int enable, long long* host_out8) {
+static constexpr int kPhaseSlots = 12;
+int hdb_resident_profile(int enable, long long* host_out12) {
   return guarded([&] {
     Engine& E = engine();
     if (enable) {
-      if (!g_phase) g_phase = (long long*)E.alloc_bytes(8 * sizeof(long long));
-      HDB_CUDA(cudaMemsetAsync(g_phase, 0, 8 * sizeof(long long), E.st));
+      if (!g_phase) g_phase = (long long*)E.alloc_bytes(kPhaseSlots * sizeof(long long));
+      HDB_CUDA(cudaMemsetAsync(g_phase, 0, kPhaseSlots * sizeof(long long), E.st));
       resident_set_profile(g_phase);
     } else {
-      if (host_out8 && g_phase) {
-        HDB_CUDA(cudaMemcpyAsync(host_out8, g_phase, 8 * sizeof(long long), cudaMemcpyDeviceToHost, E.st));
+      if (host_out12 && g_phase) {
+        HDB_CUDA(cudaMemcpyAsync(host_out12, g_phase, kPhaseSlots * sizeof(long long), cudaMemcpyDeviceToHost, E.st));
         E.sync();
       }
       resident_set_profile(nullptr);

@@ -69,8 +69,11 @@ constexpr int kGatherCap = 130;  // cluster all-gather vector length (DSMEM buff
 
 typedef cd GatherBuf[2][16][kGatherCap];  // [buffer][source rank][element] (cluster mode only)
 
+constexpr int kOnePhaseMax = 64;  // grid reductions of up to this many elements take one barrier
+
 struct RSmem {
   uint64_t mbar[2];
+  cd sub[kRT];                // one-barrier grid reduction: per-thread sub-sums
   cd coef[49];    // per-tap coefficients when this CTA's k^2 window is uniform
   int uniform;
   cd pv[kVecCap];             // this CTA's block partial vector
@@ -324,6 +327,32 @@ struct GridSync {
         }
         out[i] = q;
       }
+    } else if (m <= kOnePhaseMax) {
+      // one grid barrier: every CTA sums all P partials of every element itself.
+      // Thread t takes element e = t % m over ranks gi, gi + G, ... (gi = t / m,
+      // G = kRT / m groups), the G sub-sums are then added in group order --
+      // the same fixed order in every CTA, so all CTAs hold identical sums.
+      const int G = kRT / m, t = threadIdx.x, e = t % m, gi = t / m;
+      cd q = mkc(0.0, 0.0);
+      if (gi < G) {
+#pragma unroll 4
+        for (int r = gi; r < P; r += G) {
+          const cd z = __ldcg(&col[(long long)r * kVecCap + e]);
+          q.x += z.x;
+          q.y += z.y;
+        }
+      }
+      s.sub[t] = q;
+      __syncthreads();
+      for (int i = t; i < m; i += blockDim.x) {
+        cd a = mkc(0.0, 0.0);
+        for (int g2 = 0; g2 < G; ++g2) {
+          const cd z = s.sub[g2 * m + i];
+          a.x += z.x;
+          a.y += z.y;
+        }
+        out[i] = a;
+      }
     } else {
       cd* sums = gpart + 2LL * P * kVecCap + (long long)buf * kVecCap;  // published element sums
       for (int i = blockIdx.x; i < m; i += P) {
@@ -390,22 +419,40 @@ __device__ __forceinline__ cd cdiv_(cd a, cd b) {
 
 // CGS pass: out = V[0..m)^H w (warp per basis vector over this CTA's points),
 // then w -= V out.  Returns with out[] reduced cluster/grid-wide in s.hv.
-// with_norm: element m of the reduction carries <w, w> of the incoming w
-template <class Sync>
+// with_norm: element m of the reduction carries <w, w> of the incoming w.
+// `ph(k)` marks sub-phases (telemetry): 6 after the local dots, 7 after the
+// reduction, 8 after the update.
+template <class Sync, class Ph>
 __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n, long long p0, int cnt, int m,
-                         int& buf, cd* gpart, bool with_norm = false) {
+                         int& buf, cd* gpart, bool with_norm, Ph&& ph) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int mm = m + (with_norm ? 1 : 0);
-  for (int i = wid; i < mm; i += kRT / 32) {
-    const cd* vi = i < m ? basis + (long long)i * n + p0 : ws;
-    cd a = mkc(0.0, 0.0);
-#pragma unroll 8
-    for (int q = lane; q < cnt; q += 32) a = c_conjmul_acc(a, vi[q], ws[q]);
+  constexpr int NW = kRT / 32;
+  // warp w takes vectors w and w + NW together (one latency round for both);
+  // each dot keeps its lane-strided order and warp tree
+  for (int i = wid; i < mm; i += 2 * NW) {
+    const int i2 = i + NW;
+    const bool two = i2 < mm;
+    const cd* v1 = i < m ? basis + (long long)i * n + p0 : ws;
+    const cd* v2 = !two ? v1 : (i2 < m ? basis + (long long)i2 * n + p0 : ws);
+    cd a = mkc(0.0, 0.0), b2 = mkc(0.0, 0.0);
+#pragma unroll 4
+    for (int q = lane; q < cnt; q += 32) {
+      const cd wq = ws[q];
+      a = c_conjmul_acc(a, v1[q], wq);
+      b2 = c_conjmul_acc(b2, v2[q], wq);
+    }
     a = warp_sum_c(a);
-    if (lane == 0) s.pv[i] = a;
+    b2 = warp_sum_c(b2);
+    if (lane == 0) {
+      s.pv[i] = a;
+      if (two) s.pv[i2] = b2;
+    }
   }
   __syncthreads();
+  ph(6);
   sy.reduce_vec(s, mm, s.hv, buf, gpart);
+  ph(7);
   for (int q = threadIdx.x; q < cnt; q += kRT) {
     cd w = ws[q];
     const cd* vq = basis + p0 + q;
@@ -421,6 +468,7 @@ __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long 
     ws[q] = w;
   }
   __syncthreads();
+  ph(8);
 }
 
 template <class Sync, int R, int ORTHO>
@@ -492,6 +540,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   if (t == 0) s.g[0] = mkc(beta, 0.0);
   int its = 0;
   long long tprev_ = clock64();
+  auto ph = [&](int k) { PHASE(k); };
   // ws = M V_j for this CTA's points (stencil from the shared-memory windows).
   // `givens_j` >= 0: thread 0 first applies the rotations of step givens_j,
   // overlapping that serial work with everybody else's stencil points.
@@ -501,21 +550,32 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       if (cnt > 0) load_u_tile<R>(ut, T, vj, A.ksq, A.g, A.c);
       __syncthreads();
     }
-    if (givens_j >= 0 && t == 0) {
-      // rotations (krylov.py:126-151), identical in every CTA
+    PHASE(9);
+    if (givens_j >= 0 && t == kRT - 1) {
+      // rotations (krylov.py:126-151), identical in every CTA.  Run by the LAST
+      // thread: on small levels its warp owns no stencil points, so this serial
+      // work overlaps the other warps' stencil instead of delaying warp 0.  The
+      // rotated entry is carried in registers (no shared-memory round trip on
+      // the dependency chain); same operations in the same order as before.
       const int j = givens_j;
       const double hn = hn_prev;
       cd* col = s.hcol;
       col[j + 1] = mkc(hn, 0.0);
-      bool finite = true;
-      for (int i = 0; i <= j + 1; ++i) finite &= isfinite(col[i].x) && isfinite(col[i].y);
+      cd cur = col[0];
+      bool finite = isfinite(cur.x) && isfinite(cur.y) && isfinite(hn);
+#pragma unroll 4
       for (int i = 0; i < j; ++i) {
-        const cd sc = cmul_(s.sn[i], col[i + 1]);
-        const cd tt = mkc(s.cs[i] * col[i].x + sc.x, s.cs[i] * col[i].y + sc.y);
-        const cd nb = cmul_(mkc(-s.sn[i].x, s.sn[i].y), col[i]);
-        col[i + 1] = mkc(nb.x + s.cs[i] * col[i + 1].x, nb.y + s.cs[i] * col[i + 1].y);
+        const cd nxt = col[i + 1];
+        const double csi = s.cs[i];
+        const cd sni = s.sn[i];
+        finite &= isfinite(nxt.x) && isfinite(nxt.y);
+        const cd sc = cmul_(sni, nxt);
+        const cd tt = mkc(csi * cur.x + sc.x, csi * cur.y + sc.y);
+        const cd nb = cmul_(mkc(-sni.x, sni.y), cur);
+        cur = mkc(nb.x + csi * nxt.x, nb.y + csi * nxt.y);
         col[i] = tt;
       }
+      col[j] = cur;
       const cd h1 = col[j], h2 = col[j + 1];
       double c;
       cd sn;
@@ -542,6 +602,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       const double rel = cabs_(s.g[j + 1]) / bnorm;
       s.decision = !finite ? 2 : ((hn < 1e-30 || rel <= A.tol) ? 1 : 0);
     }
+    PHASE(10);
     if (jv < A.cap) {  // the stencil of step jv (skipped past the cap)
       for (int q = t; q < cnt; q += kRT) {
         const long long p = p0 + q;
@@ -571,10 +632,10 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
       // Hessenberg column in exact arithmetic, two reductions instead of j+1
       __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, false, ph);
       for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
       __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart);
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, false, ph);
       for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
       __syncthreads();
     }
@@ -587,7 +648,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       // the (tiny) corrections.  Same Hessenberg column in exact arithmetic;
       // every CTA takes the same branch (identically reduced scalars).
       __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true);
+      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true, ph);
       double nw = s.hv[j + 1].x, sh = 0.0;
       for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
       __syncthreads();
@@ -595,7 +656,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       double est = nw - sh;
       if (!(est > 0.5 * nw)) {
         __syncthreads();
-        cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true);
+        cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true, ph);
         nw = s.hv[j + 1].x;
         sh = 0.0;
         for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;

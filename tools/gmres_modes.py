@@ -55,13 +55,13 @@ def main():
                                C.byref(its), C.byref(rel))
             torch.cuda.synchronize()
             dt = (time.perf_counter() - t0) / a.reps * 1e3
-            prof = (C.c_longlong * 8)()
+            prof = (C.c_longlong * 12)()
             if mode >= 0:
                 L.hdb_resident_profile(1, None)
                 L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), a.tol, a.cap or pol.cslp_stop.max_iters, mode,
                                C.byref(its), C.byref(rel))
                 L.hdb_resident_profile(0, prof)
-            row[str(mode) + "_phase_us"] = [round(v / 1.965e3, 1) for v in prof[:6]]
+            row[str(mode) + "_phase_us"] = [round(v / 1.965e3, 1) for v in prof[:11]]
             row[str(mode)] = {"its": its.value, "ms": round(dt, 3), "us_per_it": round(dt * 1e3 / max(1, its.value), 1),
                               "relres": rel.value}
         out[l] = row
