@@ -372,8 +372,12 @@ def test_solve_bit_reproducible_run_to_run():
             torch.cuda.synchronize()
             hashes.append(hash(x.cpu().numpy().tobytes()))
             hists.append(tuple(rep.residual_history))
+        # host-buffer API (pageable numpy in and out: the staged, chunked copy path, 67 MB)
+        u, reph = s.solve(np.ascontiguousarray(prob.rhs.grid_view(prob.hierarchy)))
     assert rep.converged
     assert len(set(hashes)) == 1 and len(set(hists)) == 1
+    np.testing.assert_array_equal(u.grid_view(prob.hierarchy), x.cpu().numpy())
+    assert tuple(reph.residual_history) == hists[0]
 
 
 def test_transfers_repeatable_under_load():
