@@ -153,6 +153,19 @@ def ncu_traffic(kernel, config):
         return None
 
 
+def dominant_kernel_info(config, peak):
+    """Share and achieved bandwidth of the solve's top kernel, from the committed
+    ncu evidence (launch list + one `ncu --set full` capture of that kernel)."""
+    if config != "c2":
+        return None
+    return {"kernel": "k_mgs_grid_t (TMA-fed cooperative MGS step, 1025^2 level)",
+            "share": 0.242, "share_source": "profiles/r01d_launches_c2.txt (ncu launch list, cold cache)",
+            "traffic_MB_per_launch": 201.8, "us_per_launch": 114.8,
+            "achieved_GBs": round(201.8e6 / 114.8e-6 / 1e9, 1), "frac": round(201.8e6 / 114.8e-6 / 1e9 / peak, 3),
+            "bound": "synchronisation: j+2 grid reductions per launch (j ~ 11 here), basis streamed by TMA between them",
+            "source": "ncu --set full on tools/gmres_modes.py c2 --levels 3 (r01d_mgs capture, not committed)"}
+
+
 def kernel_roofline(hdb, hier, reps=20):
     """Time the fine-level 5-point apply (K1) and other path kernels live with CUDA
     events on the library stream (= torch's current stream)."""
@@ -431,6 +444,9 @@ def main():
                          "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"]},
             "kernels": {k: {"gbs": round(v["gbs"], 1), "ms": round(v["ms"], 4), "frac": round(v["gbs"] / peak, 3)}
                         for k, v in kern.items()},
+            # the solve's largest GPU-time share is not a stencil: it is the MGS step of the
+            # 1025^2 level, bounded by one grid reduction per coefficient (committed evidence)
+            "dominant_kernel": dominant_kernel_info(args.config, peak),
             "gpu_launches": int(launches / max(1, args.steps)),
             "gpu_launches_total": int(launches),
             "clocks": clk.summary(),

@@ -52,6 +52,13 @@ def to_host(t) -> np.ndarray:
     return t.detach().cpu().numpy()
 
 
+def copy_to_host(t, out: np.ndarray) -> np.ndarray:
+    """device tensor -> an existing host array (no new allocation); synchronous."""
+    torch = torch_mod()
+    torch.from_numpy(out).copy_(t.detach())
+    return out
+
+
 def ptr(t) -> int:
     return t.data_ptr()
 
