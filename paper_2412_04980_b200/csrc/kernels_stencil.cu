@@ -4,6 +4,7 @@
 // Reference: _kernels.py:14-68, operators.py:130-178, mg.py:88-102.
 // Memory-bound: 40 B/pt algorithmic for an apply (u 16 + k^2 8 + out 16),
 // 56 B/pt for the residual / A-DEF1 form (+ b 16), 56 B/pt per Jacobi sweep.
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -76,61 +77,55 @@ __device__ __forceinline__ cd interior_dinv(const OpCoef& c, double kc) {
 
 constexpr int SX = 32, SY = 4, RB = 16;  // block 32x4 threads, 16 rows per thread
 
+// one output by the per-point closure path (boundaries, ragged edges, pinned rows)
 template <int MODE>
-__global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
-                                                 const double* __restrict__ k, cd* __restrict__ out, Geom g,
-                                                 OpCoef c, double omega) {
-  if (c.skip && *c.skip) return;
-  const int i = blockIdx.x * SX + threadIdx.x;
-  const int jbeg = (blockIdx.y * SY + threadIdx.y) * RB;  // local row
-  const int gi0 = blockIdx.x * SX, gj0 = g.row0 + blockIdx.y * SY * RB;
-  const int gj1 = gj0 + SY * RB;  // exclusive
-  const bool interior = gi0 >= 1 && gi0 + SX <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
-                        blockIdx.y * SY * RB + SY * RB <= g.ny;
-  if (!interior) {
-    // generic per-point path (boundaries, ragged edges)
-    if (i >= g.nx) return;
-    for (int r = 0; r < RB; ++r) {
-      const int j = jbeg + r;
-      if (j >= g.ny) return;
-      const int gj = j + g.row0;
-      const long long p = (long long)j * g.nx + i;
-      if (MODE == 3) {
-        const cd bb = b[p];
-        if (pinned(g, c, gj, i)) { out[p] = c_scale(omega, bb); continue; }
-        out[p] = c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), bb);
-        continue;
-      }
-      const cd uc = u[p];
-      if (pinned(g, c, gj, i)) {
-        if (MODE == 0) out[p] = uc;
-        else if (MODE == 1) out[p] = c_sub(b[p], uc);
-        else out[p] = c_add(uc, c_scale(omega, c_sub(b[p], uc)));
-        continue;
-      }
-      const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
-                               upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
-      if (MODE == 0) { out[p] = Au; continue; }
-      const cd r1 = c_sub(b[p], Au);
-      if (MODE == 1) { out[p] = r1; continue; }
-      out[p] = c_add(uc, c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), r1));
-    }
+__device__ __forceinline__ void r1_point(const cd* __restrict__ u, const cd* __restrict__ b,
+                                         const double* __restrict__ k, cd* __restrict__ out, const Geom& g,
+                                         const OpCoef& c, double omega, int i, int j) {
+  const int gj = j + g.row0;
+  const long long p = (long long)j * g.nx + i;
+  if (MODE == 3) {
+    const cd bb = b[p];
+    if (pinned(g, c, gj, i)) { out[p] = c_scale(omega, bb); return; }
+    out[p] = c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), bb);
     return;
   }
-  // interior fast path: no closure, no pinning; every (i, j) and its neighbours exist
+  const cd uc = u[p];
+  if (pinned(g, c, gj, i)) {
+    if (MODE == 0) out[p] = uc;
+    else if (MODE == 1) out[p] = c_sub(b[p], uc);
+    else out[p] = c_add(uc, c_scale(omega, c_sub(b[p], uc)));
+    return;
+  }
+  const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
+                           upad(u, k, g, c, gj - 1, i), upad(u, k, g, c, gj + 1, i));
+  if (MODE == 0) { out[p] = Au; return; }
+  const cd r1 = c_sub(b[p], Au);
+  if (MODE == 1) { out[p] = r1; return; }
+  out[p] = c_add(uc, c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), r1));
+}
+
+// rows [j0, j0 + n) of column i by the sliding window: no closure, no pinning
+// (the caller guarantees every point and its neighbours exist).  The whole
+// warp runs the same rows (E/W come from lane shuffles).
+template <int MODE, int UNR>
+__device__ __forceinline__ void r1_run(const cd* __restrict__ u, const cd* __restrict__ b,
+                                       const double* __restrict__ k, cd* __restrict__ out, const Geom& g,
+                                       const OpCoef& c, double omega, int i, int j0, int n) {
+  if (n <= 0) return;
   const int lane = threadIdx.x;
   const long long nx = g.nx;
-  const cd* up = u + (long long)jbeg * nx + i;
+  const cd* up = u + (long long)j0 * nx + i;
   if (MODE == 3) {
-    const double* kp = k + (long long)jbeg * nx + i;
-    const cd* bp = b + (long long)jbeg * nx + i;
-    cd* op = out + (long long)jbeg * nx + i;
+    const double* kp = k + (long long)j0 * nx + i;
+    const cd* bp = b + (long long)j0 * nx + i;
+    cd* op = out + (long long)j0 * nx + i;
     // the reciprocal depends on k^2 only: reuse it while k^2 repeats down the
     // column (constant and layered models), bit-identical either way
     double klast = kp[0];
     cd dlast = interior_dinv(c, klast);
 #pragma unroll 4
-    for (int r = 0; r < RB; ++r) {
+    for (int r = 0; r < n; ++r) {
       const double kc = kp[r * nx];
       if (kc != klast) { klast = kc; dlast = interior_dinv(c, kc); }
       op[r * nx] = c_mul(c_scale(omega, dlast), bp[r * nx]);
@@ -138,9 +133,9 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
     return;
   }
   // software pipeline: row r+1's loads are issued before row r is computed
-  const double* kp = k + (long long)jbeg * nx + i;
-  const cd* bp = b ? b + (long long)jbeg * nx + i : nullptr;
-  cd* op = out + (long long)jbeg * nx + i;
+  const double* kp = k + (long long)j0 * nx + i;
+  const cd* bp = b ? b + (long long)j0 * nx + i : nullptr;
+  cd* op = out + (long long)j0 * nx + i;
   cd s_ = up[-nx], c_ = up[0], n_ = up[nx];
   double kc = kp[0];
   cd bc = (MODE != 0) ? bp[0] : mkc(0.0, 0.0);
@@ -148,11 +143,11 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
   double klast = 0.0;
   cd dlast = mkc(0.0, 0.0);
   if (MODE == 2) { klast = kc; dlast = interior_dinv(c, kc); }
-#pragma unroll (MODE == 2 ? 2 : 4)
-  for (int r = 0; r < RB; ++r) {
+#pragma unroll (UNR)
+  for (int r = 0; r < n; ++r) {
     const long long o = (long long)r * nx;
     // prefetch row r+1 (its north row r+2, k, b, warp-edge neighbours)
-    const bool more = r + 1 < RB;
+    const bool more = r + 1 < n;
     cd n2 = mkc(0.0, 0.0), b2 = mkc(0.0, 0.0), wl2 = mkc(0.0, 0.0), el2 = mkc(0.0, 0.0);
     double k2 = 0.0;
     if (more) {
@@ -191,15 +186,67 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
   }
 }
 
+template <int MODE>
+__global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) k_r1s(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                 const double* __restrict__ k, cd* __restrict__ out, Geom g,
+                                                 OpCoef c, double omega) {
+  if (c.skip && *c.skip) return;
+  const int i = blockIdx.x * SX + threadIdx.x;
+  const int jbeg = (blockIdx.y * SY + threadIdx.y) * RB;  // local row
+  const int gi0 = blockIdx.x * SX, gj0 = g.row0 + blockIdx.y * SY * RB;
+  const int gj1 = gj0 + SY * RB;  // exclusive
+  const bool interior = gi0 >= 1 && gi0 + SX <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
+                        blockIdx.y * SY * RB + SY * RB <= g.ny;
+  if (!interior) {
+    // generic per-point path (boundaries, ragged edges)
+    if (i >= g.nx) return;
+    for (int r = 0; r < RB; ++r) {
+      const int j = jbeg + r;
+      if (j >= g.ny) return;
+      r1_point<MODE>(u, b, k, out, g, c, omega, i, j);
+    }
+    return;
+  }
+  r1_run<MODE, (MODE == 2 ? 2 : 4)>(u, b, k, out, g, c, omega, i, jbeg, RB);
+}
+
+// Same tiles as k_r1s with a run-time row count per thread (rb).  Shorter
+// column runs are faster on the fine grids although each run re-reads its
+// two halo rows (they hit L2: the block's other warps own them): measured
+// (HDB_R1_RB sweep, profiles/r01e_r1_rows_sweep.txt) 4097^2 apply / residual
+// 93.7 / 99.7 % of the copy peak at rb = 4 vs 83 / 91 % at rb = 16, 73.7 /
+// 83 % at rb = 32; the Jacobi sweep (more registers, 5 CTAs/SM) peaks at rb = 8
+// on 4097^2 and rb = 16 on 8193^2.
+template <int MODE, int UNR>
+__global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) k_r1w(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                 const double* __restrict__ k, cd* __restrict__ out, Geom g,
+                                                 OpCoef c, double omega, int rb) {
+  if (c.skip && *c.skip) return;
+  const int i = blockIdx.x * SX + threadIdx.x;
+  const int jbeg = (blockIdx.y * SY + threadIdx.y) * rb;  // local row
+  const int gi0 = blockIdx.x * SX, gj0 = g.row0 + blockIdx.y * SY * rb;
+  const int gj1 = gj0 + SY * rb;  // exclusive
+  const bool interior = gi0 >= 1 && gi0 + SX <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
+                        blockIdx.y * SY * rb + SY * rb <= g.ny;
+  if (!interior) {
+    if (i >= g.nx) return;
+    const int je = min(jbeg + rb, g.ny);
+    for (int j = jbeg; j < je; ++j) r1_point<MODE>(u, b, k, out, g, c, omega, i, j);
+    return;
+  }
+  r1_run<MODE, UNR>(u, b, k, out, g, c, omega, i, jbeg, rb);
+}
+
 // ------------------------------------------------------------------------
 // Fused residual norm (the MG divergence guard, mg.py:131-138, and any
 // ||b - A u|| that only needs the norm): dst = (||b - A u||^2, ||b||^2) as one
 // complex slot (re, im), read in one pass over u, b, k^2 (40 B/pt); the
-// residual itself is never stored.  One block per 32 x (NRW*RB) strip tile
+// residual itself is never stored.  One block per 32 x (NRW*RBN) strip tile
 // (interior tiles with the k_r1s sliding window, boundary tiles per point),
 // per-tile partials in tile order, then one ordered sum (k_sum_partials):
 // deterministic for a given grid.
-constexpr int NRW = 4;  // warps per block (tile rows = NRW * RB)
+constexpr int NRW = 4;  // warps per block (tile rows = NRW * RBN)
+constexpr int RBN = 8;  // rows per warp (shorter runs stream faster, see k_r1w)
 __global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, const cd* __restrict__ b,
                                                       const double* __restrict__ k, Geom g, OpCoef c, cd* partials) {
   const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
@@ -207,13 +254,13 @@ __global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, 
   const long long nx = g.nx;
   const int bx = blockIdx.x, by = blockIdx.y;
   const int i = bx * 32 + lane;
-  const int jbeg = (by * NRW + wy) * RB;
-  const int gi0 = bx * 32, gj0 = g.row0 + by * NRW * RB, gj1 = gj0 + NRW * RB;
+  const int jbeg = (by * NRW + wy) * RBN;
+  const int gi0 = bx * 32, gj0 = g.row0 + by * NRW * RBN, gj1 = gj0 + NRW * RBN;
   const bool interior = gi0 >= 1 && gi0 + 32 <= g.nx - 1 && gj0 >= 1 && gj1 <= g.nyg - 1 &&
-                        by * NRW * RB + NRW * RB <= g.ny;
+                        by * NRW * RBN + NRW * RBN <= g.ny;
   if (!interior) {
     if (i < g.nx)
-      for (int r = 0; r < RB; ++r) {
+      for (int r = 0; r < RBN; ++r) {
         const int j = jbeg + r;
         if (j >= g.ny) break;
         const int gj = j + g.row0;
@@ -239,9 +286,9 @@ __global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, 
     cd bc = bp[0];
     cd wl = (lane == 0) ? up[-1] : mkc(0.0, 0.0), el = (lane == 31) ? up[1] : mkc(0.0, 0.0);
 #pragma unroll 4
-    for (int r = 0; r < RB; ++r) {
+    for (int r = 0; r < RBN; ++r) {
       const long long o = (long long)r * nx;
-      const bool more = r + 1 < RB;
+      const bool more = r + 1 < RBN;
       cd n2 = mkc(0.0, 0.0), b2 = mkc(0.0, 0.0), wl2 = mkc(0.0, 0.0), el2 = mkc(0.0, 0.0);
       double k2 = 0.0;
       if (more) {
@@ -541,13 +588,42 @@ static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny 
 static inline dim3 grid_r1s(const Geom& g) { return dim3((g.nx + SX - 1) / SX, (g.ny + SY * RB - 1) / (SY * RB)); }
 static inline bool use_strip(const Geom& g) { return g.nx >= 512 && g.ny >= 512; }  // small grids: all blocks are boundary blocks
 
+// HDB_R1_WAVE=0 selects the fixed 16-row k_r1s; HDB_R1_RB=n forces rb
+static int r1_rows(int mode, const Geom& g) {
+  static const int forced = [] {
+    const char* e = getenv("HDB_R1_RB");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  if (forced) return forced;
+  if (mode == 0 || mode == 1) return 4;
+  return (long long)g.nx * g.ny >= (32LL << 20) ? 16 : 8;
+}
+static bool r1_wave() {
+  static const bool v = [] {
+    const char* e = getenv("HDB_R1_WAVE");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+template <int MODE>
+static void launch_r1_strip(const Geom& g, const cd* u, const cd* b, const double* k, cd* out, const OpCoef& c,
+                            double omega, cudaStream_t st) {
+  const dim3 blk(SX, SY);
+  if (!r1_wave()) {
+    k_r1s<MODE><<<grid_r1s(g), blk, 0, st>>>(u, b, k, out, g, c, omega);
+    return;
+  }
+  const int rb = r1_rows(MODE, g);
+  const dim3 grd((g.nx + SX - 1) / SX, (g.ny + SY * rb - 1) / (SY * rb));
+  k_r1w<MODE, (MODE == 2 ? 2 : 4)><<<grd, blk, 0, st>>>(u, b, k, out, g, c, omega, rb);
+}
+
 void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
                   int mode, cudaStream_t st) {
   if (c.radius == 1) {
     if (use_strip(g)) {
-      const dim3 blk(SX, SY), grd = grid_r1s(g);
-      if (mode == 0) k_r1s<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
-      else k_r1s<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+      if (mode == 0) launch_r1_strip<0>(g, u, b, k, out, c, 0.0, st);
+      else launch_r1_strip<1>(g, u, b, k, out, c, 0.0, st);
       return;
     }
     const dim3 blk(32, 8), grd = grid_r1(g);
@@ -587,9 +663,8 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
 void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out,
                    double omega, bool from_zero, cudaStream_t st) {
   if (use_strip(g)) {
-    const dim3 blk(SX, SY), grd = grid_r1s(g);
-    if (from_zero) k_r1s<3><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
-    else k_r1s<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+    if (from_zero) launch_r1_strip<3>(g, x, b, k, out, c, omega, st);
+    else launch_r1_strip<2>(g, x, b, k, out, c, omega, st);
     return;
   }
   const dim3 blk(32, 8), grd = grid_r1(g);
@@ -598,11 +673,11 @@ void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, con
 }
 
 long long resnorm_partials(const Geom& g) {
-  return (long long)((g.nx + 31) / 32) * ((g.ny + NRW * RB - 1) / (NRW * RB));
+  return (long long)((g.nx + 31) / 32) * ((g.ny + NRW * RBN - 1) / (NRW * RBN));
 }
 void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* partials,
                     cd* dst, cudaStream_t st) {
-  const dim3 grd((g.nx + 31) / 32, (g.ny + NRW * RB - 1) / (NRW * RB));
+  const dim3 grd((g.nx + 31) / 32, (g.ny + NRW * RBN - 1) / (NRW * RBN));
   k_resnorm<<<grd, 32 * NRW, 0, st>>>(u, b, k, g, c, partials);
   k_sum_partials<<<1, kSumThreads, 0, st>>>(partials, (long long)grd.x * grd.y, dst);
 }

@@ -99,6 +99,27 @@ def test_operator_uniform_k_large_bitexact(level, bnd):
     np.testing.assert_array_equal(op.residual(b, u), b - ref.apply(u))
 
 
+@pytest.mark.parametrize("shape", [(1025, 1025), (600, 2050), (2049, 517), (777, 1111)])
+@pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
+def test_strip_kernels_bitexact_vs_oracle(shape, bnd):
+    """5-point apply, residual and both Jacobi forms on grids >= 512^2 (the
+    column-strip kernels: balanced one-wave row ranges, ragged last strip,
+    global first/last rows on the closure path) against the oracle, bit for bit."""
+    rng = _rng(shape[0] + 3 * shape[1])
+    ny, nx = shape
+    ksq = 900.0 + 500.0 * rng.random((ny, nx))
+    ksq[ny // 2: ny // 2 + 40] = 700.0  # constant band: Jacobi reciprocal reuse
+    op = hdb.radius1_operator(nx, ny, 1.0 / 256, ksq, bnd, complex(1.0, 0.5))
+    ref = oracle.CpuLevelOp(nx, ny, 1.0 / 256, ksq, bnd, *oracle.level_kernels(1)[:4], shift=complex(1.0, 0.5),
+                            level_scale=1.0)
+    u, b = _rand(rng, shape), _rand(rng, shape)
+    au = ref.apply(u)
+    np.testing.assert_array_equal(op.apply(u), au)
+    np.testing.assert_array_equal(op.residual(b, u), b - au)
+    np.testing.assert_array_equal(op.jacobi(u, b, 0.8), ref.jacobi(u, b, 0.8))
+    np.testing.assert_array_equal(op.jacobi(None, b, 0.8), ref.jacobi(np.zeros(shape, complex), b, 0.8))
+
+
 @pytest.mark.parametrize("shape", [(129, 129), (600, 300), (1025, 1025)])
 @pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
 def test_fused_residual_norms_vs_oracle(shape, bnd):

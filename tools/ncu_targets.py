@@ -4,7 +4,7 @@ for one `ncu --set full` capture of all of them:
     ncu --set full --clock-control none --import-source on -k regex:'^k_' \
         -o gpurun_out/targets python tools/ncu_targets.py
 
-Fine level (4097^2): 5-point apply / residual / Jacobi (K1-K3), restriction,
+Fine level (4097^2): 5-point apply (k_r1w) / residual / Jacobi (K1-K3), restriction,
 prolongation, dot, fused residual norm (MG guard).  Coarse levels: radius-3 apply on level 3 (1025^2),
 radius-2 apply on level 2 (2049^2).
 """
@@ -37,9 +37,9 @@ def main():
     mg = hdb.CslpMultigrid(lv.nx, lv.ny, lv.h, hier.ksq_at(1), hier.boundary, beta2=0.5)
     c = torch.empty(hier.level(2).shape, dtype=torch.complex128, device="cuda")
     torch.cuda.synchronize()
-    _lib.check(L.hdb_op_apply(op.handle, u.data_ptr(), out.data_ptr()))                       # k_r1s<0>
-    _lib.check(L.hdb_op_residual(op.handle, b.data_ptr(), u.data_ptr(), out.data_ptr()))      # k_r1s<1>
-    _lib.check(L.hdb_op_jacobi(mg.levels[0].op.handle, u.data_ptr(), b.data_ptr(), out.data_ptr(), 0.8))  # k_r1s<2>
+    _lib.check(L.hdb_op_apply(op.handle, u.data_ptr(), out.data_ptr()))                       # k_r1w<0> (k_r1s<0> with HDB_R1_WAVE=0)
+    _lib.check(L.hdb_op_residual(op.handle, b.data_ptr(), u.data_ptr(), out.data_ptr()))      # k_r1w<1>
+    _lib.check(L.hdb_op_jacobi(mg.levels[0].op.handle, u.data_ptr(), b.data_ptr(), out.data_ptr(), 0.8))  # k_r1w<2>
     _lib.check(L.hdb_restrict(u.data_ptr(), lv.ny, lv.nx, c.data_ptr(), 0))                   # k_restrict_t
     _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, None, out.data_ptr()))               # k_prolong_t
     _lib.check(L.hdb_prolong(c.data_ptr(), lv.ny, lv.nx, b.data_ptr(), out.data_ptr()))       # k_prolong_t (+ base)
