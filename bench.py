@@ -141,10 +141,10 @@ def _allmax(val, ws):
 
 def ncu_traffic(kernel, config):
     """dram read + write bytes per launch of `kernel` from the committed
-    `ncu --set full` capture (profiles/r01d_kernels_ncu.json, config-2 grids)."""
+    `ncu --set full` capture (profiles/r01e_kernels_ncu.json, config-2 grids)."""
     if config != "c2":
         return None
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01d_kernels_ncu.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01e_kernels_ncu.json")
     try:
         with open(path) as f:
             k = json.load(f)["kernels"][kernel]
@@ -466,8 +466,8 @@ def main():
                     "d2h_bytes_per_step": int(b_host.nbytes) * ws},
             "roofline": {"bound": "hbm", "kernel": "stencil5_apply (K1, fine level)",
                          "achieved": dom["gbs"], "peak": peak, "unit": "GB/s", "frac": dom["gbs"] / peak,
-                         "traffic": ncu_traffic("k_r1s<0>", args.config),
-                         "traffic_source": "profiles/r01d_kernels_ncu.json (ncu --set full, dram read+write per launch)",
+                         "traffic": ncu_traffic("k_r1w<0, 4>", args.config),
+                         "traffic_source": "profiles/r01e_kernels_ncu.json (ncu --set full, dram read+write per launch)",
                          "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": dom["bytes"], "ms_per_launch": dom["ms"]},
             "kernels": {k: kernel_entry(k, v, peak) for k, v in kern.items()},

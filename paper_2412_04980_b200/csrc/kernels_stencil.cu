@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
 // per-tile partials in tile order, then one ordered sum (k_sum_partials):
 // deterministic for a given grid.
 constexpr int NRW = 4;  // warps per block (tile rows = NRW * RBN)
-constexpr int RBN = 8;  // rows per warp (shorter runs stream faster, see k_r1w)
+constexpr int RBN = 16;  // rows per warp (8 measured slower on 8193^2: 83 vs 90 % of peak)
 __global__ void __launch_bounds__(32 * NRW) k_resnorm(const cd* __restrict__ u, const cd* __restrict__ b,
                                                       const double* __restrict__ k, Geom g, OpCoef c, cd* partials) {
   const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
@@ -395,7 +395,9 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
 // of the upper output and a = r-1 of the lower one, so every output still
 // receives its taps in the reference's row-major (a, b) order (bit-identical),
 // while the shared-memory loads per output drop from (2R+1)^2 to
-// (2R+2)(2R+1)/2.  Tile: 32 x 16 outputs (256 threads).
+// (2R+2)(2R+1)/2.  Tile: 32 x 16 outputs (256 threads).  Four outputs per
+// thread (17.5 loads per output) measured slower: 94 registers leave 20 warps
+// per SM (41.0 vs 37.4 us on the 1025^2 level of config 2).
 constexpr int VTY = 8, VROWS = 2 * VTY;
 template <int R, int MODE>
 __global__ void __launch_bounds__(TX * VTY) k_rgv(const cd* __restrict__ u, const cd* __restrict__ b,

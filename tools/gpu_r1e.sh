@@ -1,8 +1,4 @@
-# r01e validation: GPU tests, smoke, config-2 / config-5 bench, ncu capture of the strip kernels
-set -x
-timeout 900 python -m pytest tests -q -m gpu > gpurun_out/r01e_gpu_tests.log 2>&1; echo TESTS_EXIT $? >> gpurun_out/r01e_gpu_tests.log
-timeout 300 python __graft_entry__.py smoke > gpurun_out/r01e_smoke.log 2>&1; echo SMOKE_EXIT $? >> gpurun_out/r01e_smoke.log
-timeout 900 python bench.py > gpurun_out/r01e_bench_c2.json 2> gpurun_out/r01e_bench_c2.err
-timeout 900 python bench.py --config c5 --steps 2 > gpurun_out/r01e_bench_c5.json 2> gpurun_out/r01e_bench_c5.err
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_r1w|k_resnorm|k_r1s' -f -o gpurun_out/r01e_targets python tools/ncu_targets.py c2 > gpurun_out/r01e_ncu.log 2>&1
-echo done
+# radius-3 Galerkin stencil: 2 vs 4 outputs per thread (HDB_RG_VO), config-2 level 3
+timeout 600 python -m pytest tests -x -q -m gpu -k "operator" > gpurun_out/r1j_tests.log 2>&1; echo tests rc=$? >> gpurun_out/r1j_tests.log
+for V in 2 4 2 4; do echo "vo=$V $(HDB_RG_VO=$V timeout 300 python tools/kernel_bench.py c2 --reps 30 2>/dev/null)" >> gpurun_out/r1j_kb_vo.txt; done
+echo "c5 vo=4 $(HDB_RG_VO=4 timeout 300 python tools/kernel_bench.py c5 --reps 20 2>/dev/null)" >> gpurun_out/r1j_kb_vo.txt
