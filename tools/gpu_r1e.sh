@@ -1,4 +1,5 @@
-# radius-3 Galerkin stencil: 2 vs 4 outputs per thread (HDB_RG_VO), config-2 level 3
-timeout 600 python -m pytest tests -x -q -m gpu -k "operator" > gpurun_out/r1j_tests.log 2>&1; echo tests rc=$? >> gpurun_out/r1j_tests.log
-for V in 2 4 2 4; do echo "vo=$V $(HDB_RG_VO=$V timeout 300 python tools/kernel_bench.py c2 --reps 30 2>/dev/null)" >> gpurun_out/r1j_kb_vo.txt; done
-echo "c5 vo=4 $(HDB_RG_VO=4 timeout 300 python tools/kernel_bench.py c5 --reps 20 2>/dev/null)" >> gpurun_out/r1j_kb_vo.txt
+# r01e final validation of the committed tree: GPU tests, smoke, config-2 bench (with cpu_baseline)
+timeout -s KILL 900 python -m pytest tests -q -m gpu > gpurun_out/r01e2_gpu_tests.log 2>&1; echo TESTS_EXIT $? >> gpurun_out/r01e2_gpu_tests.log
+timeout -s KILL 300 python __graft_entry__.py smoke > gpurun_out/r01e2_smoke.log 2>&1; echo SMOKE_EXIT $? >> gpurun_out/r01e2_smoke.log
+timeout -s KILL 900 python bench.py > gpurun_out/r01e2_bench_c2.json 2> gpurun_out/r01e2_bench_c2.err
+timeout -s KILL 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/r01e2_bench_reference_c2.json 2> gpurun_out/r01e2_bench_reference_c2.err
