@@ -217,8 +217,11 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
 // 93.7 / 99.7 % of the copy peak at rb = 4 vs 83 / 91 % at rb = 16, 73.7 /
 // 83 % at rb = 32; the Jacobi sweep (more registers, 5 CTAs/SM) peaks at rb = 8
 // on 4097^2 and rb = 16 on 8193^2.
+// The Jacobi form is held to 80 registers (6 CTAs/SM, 8 B of spill) -- measured
+// faster than 94 registers at 5 CTAs/SM: 86.6 vs 83.4 % of the copy peak on
+// 4097^2, 95.2 vs 91.8 % on 8193^2 (profiles/r01e_jacobi_occupancy.txt).
 template <int MODE, int UNR>
-__global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) k_r1w(const cd* __restrict__ u, const cd* __restrict__ b,
+__global__ void __launch_bounds__(SX * SY, (MODE == 1 || MODE == 2) ? 6 : 8) k_r1w(const cd* __restrict__ u, const cd* __restrict__ b,
                                                  const double* __restrict__ k, cd* __restrict__ out, Geom g,
                                                  OpCoef c, double omega, int rb) {
   if (c.skip && *c.skip) return;
