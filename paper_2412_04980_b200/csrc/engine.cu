@@ -163,11 +163,15 @@ TGeom level_tgeom(const LevelOp& f, const LevelOp& c) {
   return t;
 }
 
-// coarse slab of this rank under a fine slab (nested partition)
+// coarse rows this rank restricts when a sharded level feeds a replicated one:
+// coarse row c is centred on fine row 2c, so the rank owning fine rows [f0, f1)
+// takes coarse rows [ceil(f0/2), ceil(f1/2)) -- every centre lies inside its own
+// slab and the 5-tap restriction reads at most 2 rows beyond it (the exchanged
+// halo).  Cut rows of the last sharded depth can be odd (P not a power of two).
 static void coarse_slab_of(const LevelOp& f, int rank, int ncy_g, int& row0, int& ny) {
   const int P = (int)f.slab_row0.size();
-  row0 = f.slab_row0[rank] / 2;
-  const int end = rank == P - 1 ? ncy_g : f.slab_row0[rank + 1] / 2;
+  row0 = (f.slab_row0[rank] + 1) / 2;
+  const int end = rank == P - 1 ? ncy_g : (f.slab_row0[rank + 1] + 1) / 2;
   ny = end - row0;
 }
 

@@ -11,9 +11,12 @@ rotations and the least-squares update on the host (as in the reference).
     method -> called on device buffers directly;
   * any other callable -> called with arrays of ``b``'s kind (numpy in,
     numpy out for numpy ``b``; torch CUDA tensors for a CUDA ``b``).
-``dot`` is accepted for signature compatibility; the library's deterministic
-conj-first device reduction is always used (the contract of reduce_dot,
-parallel.py:168-195: conj(u).v, independent of the number of workers).
+``dot`` (krylov.py:57-61): the Krylov engine computes every inner product on
+the device with the library's deterministic conj-first reduction, which is
+the contract of the reference's choices for it (np.vdot, the default, and
+reduce_dot, parallel.py:168-195: conj(u).v, independent of the worker count).
+Those, and this package's reduce_dot, are accepted; any other callable would
+be silently replaced, so it is rejected with ConfigError instead.
 """
 from __future__ import annotations
 
@@ -98,8 +101,22 @@ class _Bridge:
             return 1
 
 
+def _check_dot(dot):
+    """Accept only inner products the device reduction implements (see module doc)."""
+    if dot is None or dot is np.vdot:
+        return
+    name = getattr(dot, "__name__", "")
+    mod = getattr(dot, "__module__", "") or ""
+    if name == "reduce_dot" and (mod.endswith(".parallel") or mod == "parallel"):
+        return   # this package's or the reference's deterministic block dot
+    from .errors import ConfigError
+    raise ConfigError(f"custom dot {dot!r} is not supported: Krylov inner products run on the device "
+                      "(conj-first deterministic reduction); pass dot=None, np.vdot or reduce_dot")
+
+
 def fgmres(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None, on_iteration=None):
     """Right-preconditioned flexible GMRES without restarts (krylov.py:61-177)."""
+    _check_dot(dot)
     host = not dev.is_device(b)
     shape = tuple(b.shape)
     db = dev.to_device(b)
@@ -142,6 +159,7 @@ def bicgstab(apply_A, apply_M, b, stop: StopRule, x0=None, dot=None):
     """Right-preconditioned Bi-CGSTAB (krylov.py:185-276).  Raises BreakdownError
     carrying the best iterate and its report when rho or omega vanish."""
     from .errors import BreakdownError
+    _check_dot(dot)
     host = not dev.is_device(b)
     shape = tuple(b.shape)
     db = dev.to_device(b)

@@ -21,12 +21,52 @@ from .errors import ShapeError
 from .grid import BC_CODE, DIRICHLET, ComplexField
 from .stencils import StencilKernel, level_kernels, mass_level_scale
 
-__all__ = ["LevelOperator", "helmholtz_operator", "cslp_operator", "radius1_operator",
-           "apply_helmholtz", "apply_cslp", "matvec_flop_byte_counters", "arithmetic_intensity",
-           "ALGORITHMIC_BYTES_PER_POINT"]
+__all__ = ["LevelOperator", "helmholtz_operator", "cslp_operator", "radius1_operator", "ghost_pad",
+           "ksq_ghost_pad", "apply_helmholtz", "apply_cslp", "assemble_csr", "assemble_dense",
+           "matvec_flop_byte_counters", "arithmetic_intensity", "ALGORITHMIC_BYTES_PER_POINT"]
+
+DEFAULT_ASSEMBLY_LIMIT = 1_100_000  # points (operators.py:41)
 
 # algorithmic HBM bytes per grid point: u 16 + k^2 8 + out 16
 ALGORITHMIC_BYTES_PER_POINT = {"apply": 40, "residual": 56, "jacobi": 56, "jacobi0": 40}
+
+
+# ghost column/row of each side (west, east, south, north): where it lies in the
+# padded array, and the boundary / first interior line of u it is built from
+def _side_lines(u, r):
+    ny, nx = u.shape
+    return ((np.s_[r:r + ny, r - 1], u[:, 0], u[:, 1]),
+            (np.s_[r:r + ny, r + nx], u[:, -1], u[:, -2]),
+            (np.s_[r - 1, r:r + nx], u[0, :], u[1, :]),
+            (np.s_[r + ny, r:r + nx], u[-1, :], u[-2, :]))
+
+
+def ghost_pad(u, radius: int, h: float, boundary, k_edges) -> np.ndarray:
+    """Host copy of u embedded in a zero band of width `radius` with the first
+    ghost layer closed per side (operators.py:44-75): Dirichlet 2 u_b - u_in,
+    Sommerfeld u_in + (2ih k_b) u_b; ghost corners and deeper layers stay 0.
+    The device kernels synthesise the same values on the fly (csrc/stencil.cuh);
+    this copy serves LevelOperator.pad / halo_exchange callers."""
+    u = np.asarray(u)
+    ny, nx = u.shape
+    pad = np.zeros((ny + 2 * radius, nx + 2 * radius), dtype=np.complex128)
+    pad[radius:radius + ny, radius:radius + nx] = u
+    two_ih = 2.0j * h
+    for kind, kb, (where, ub, uin) in zip(boundary, k_edges, _side_lines(u, radius)):
+        pad[where] = 2.0 * ub - uin if kind == DIRICHLET else uin + two_ih * kb * ub
+    return pad
+
+
+def ksq_ghost_pad(ksq, radius: int, boundary) -> np.ndarray:
+    """k^2 with its ghost band: 2 k_b^2 - k_in^2 on Dirichlet sides, 0 elsewhere (operators.py:78-93)."""
+    ksq = np.asarray(ksq, dtype=np.float64)
+    ny, nx = ksq.shape
+    pad = np.zeros((ny + 2 * radius, nx + 2 * radius))
+    pad[radius:radius + ny, radius:radius + nx] = ksq
+    for kind, (where, kb, kin) in zip(boundary, _side_lines(ksq, radius)):
+        if kind == DIRICHLET:
+            pad[where] = 2.0 * kb - kin
+    return pad
 
 
 class LevelOperator:
@@ -50,6 +90,27 @@ class LevelOperator:
         self.mass_coef = (-self.shift / level_scale) * mass.as_float().astype(np.complex128)
         self.slab = slab  # distributed.SlabSpec of this rank, None = whole grid
         self._handle = None
+        self._kedges = None
+        self._kpad = None
+
+    # host-side closure data of the reference object (operators.py:114-116), built on first use
+    @property
+    def k_edges(self):
+        if self._kedges is None:
+            kf = np.sqrt(self.ksq)
+            self._kedges = (kf[:, 0], kf[:, -1], kf[0, :], kf[-1, :])
+        return self._kedges
+
+    @property
+    def ksq_pad(self):
+        if self._kpad is None:
+            self._kpad = ksq_ghost_pad(self.ksq, self.radius, self.boundary)
+        return self._kpad
+
+    def pad(self, u) -> np.ndarray:
+        """Ghost-padded host snapshot of u (operators.py:127-128)."""
+        return ghost_pad(dev.to_host(u) if dev.is_device(u) else u, self.radius, self.h, self.boundary,
+                         self.k_edges)
 
     # -- device handle ------------------------------------------------------
     @property
@@ -230,6 +291,67 @@ def apply_helmholtz(op: LevelOperator, hierarchy, u: ComplexField) -> ComplexFie
 
 def apply_cslp(op: LevelOperator, hierarchy, u: ComplexField) -> ComplexField:
     return apply_helmholtz(op, hierarchy, u)
+
+
+def _ghost_weights(kind, h, kb):
+    """(boundary point, first interior point) weights that replace one ghost value."""
+    if kind == DIRICHLET:
+        return np.full(kb.shape, 2.0 + 0.0j), np.full(kb.shape, -1.0 + 0.0j)
+    return 2.0j * h * kb, np.full(kb.shape, 1.0 + 0.0j)
+
+
+def assemble_csr(op: LevelOperator, max_points: int = DEFAULT_ASSEMBLY_LIMIT):
+    """The operator as an explicit scipy CSR matrix (operators.py:261-328), built
+    from the stencil coefficients and the closure algebra, independently of the
+    device kernels, so each can certify the other.  Host-side test oracle.
+
+    Row p = j*nx + i.  Every tap (oj, oi) contributes coef = lap + mass * ksq_pad
+    at the neighbour; a neighbour in the first ghost layer is redistributed onto
+    the boundary point and the first interior point with the closure weights;
+    anything further out is zero padding; Dirichlet rows are identity rows."""
+    import scipy.sparse as sp
+    from .errors import CapacityError
+    if op.npoints > max_points:
+        raise CapacityError(f"{op.npoints} points exceed the assembly guard {max_points}")
+    nx, ny, r = op.nx, op.ny, op.radius
+    J, I = np.divmod(np.arange(op.npoints), nx)
+    free = np.ones(op.npoints, dtype=bool)
+    for kind, hit in zip(op.boundary, (I == 0, I == nx - 1, J == 0, J == ny - 1)):
+        if kind == DIRICHLET:
+            free &= ~hit
+    rows, cols, vals = [np.flatnonzero(~free)], [np.flatnonzero(~free)], [np.ones((~free).sum(), np.complex128)]
+    P, Jf, If = np.flatnonzero(free), J[free], I[free]
+    kw, ke, ks, kn = op.k_edges
+    for oj in range(-r, r + 1):
+        for oi in range(-r, r + 1):
+            jj, ii = Jf + oj, If + oi
+            coef = op.lap_coef[oj + r, oi + r] + op.mass_coef[oj + r, oi + r] * op.ksq_pad[jj + r, ii + r]
+            nz = coef != 0
+            xin, yin = (ii >= 0) & (ii < nx), (jj >= 0) & (jj < ny)
+            m = nz & xin & yin
+            rows.append(P[m]); cols.append(jj[m] * nx + ii[m]); vals.append(coef[m])
+            # first ghost layer on each side: (mask, boundary index, interior index, k_b, side kind)
+            ghosts = ((nz & yin & (ii == -1), lambda q: (jj[q], 0), lambda q: (jj[q], 1), lambda q: kw[jj[q]], 0),
+                      (nz & yin & (ii == nx), lambda q: (jj[q], nx - 1), lambda q: (jj[q], nx - 2),
+                       lambda q: ke[jj[q]], 1),
+                      (nz & xin & (jj == -1), lambda q: (0, ii[q]), lambda q: (1, ii[q]), lambda q: ks[ii[q]], 2),
+                      (nz & xin & (jj == ny), lambda q: (ny - 1, ii[q]), lambda q: (ny - 2, ii[q]),
+                       lambda q: kn[ii[q]], 3))
+            for mask, at_b, at_in, kb_of, side in ghosts:
+                if not mask.any():
+                    continue
+                wb, wi = _ghost_weights(op.boundary[side], op.h, kb_of(mask))
+                for (yy, xx), w in ((at_b(mask), wb), (at_in(mask), wi)):
+                    rows.append(P[mask]); cols.append(np.broadcast_to(yy, mask.sum()) * nx + xx)
+                    vals.append(coef[mask] * w)
+    mat = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                        shape=(op.npoints, op.npoints))
+    return mat.tocsr()
+
+
+def assemble_dense(op: LevelOperator, max_points: int = 40_000) -> np.ndarray:
+    """Dense form of assemble_csr (operators.py:331-333)."""
+    return assemble_csr(op, max_points=max_points).toarray()
 
 
 def matvec_flop_byte_counters(kind: str, n_points: int):

@@ -31,15 +31,33 @@ class StencilKernel:
 
     numerators: tuple
     denominator: int
-    h_power: int
+    h_power: int     # -2: Laplace-like (divided by h_l^2 when applied), 0: mass-like
+
+    def __post_init__(self):
+        side = len(self.numerators)
+        if side % 2 == 0 or any(len(row) != side for row in self.numerators):
+            raise ValueError("stencil must be square with odd side length")
+        d = self.denominator
+        if d <= 0 or d & (d - 1):
+            raise ValueError("denominator must be a positive power of two")
 
     @property
     def radius(self) -> int:
         return len(self.numerators) // 2
 
+    def as_array(self):
+        import numpy as np
+        return np.array(self.numerators, dtype=object)
+
     def as_float(self):
         import numpy as np
         return np.array(self.numerators, dtype=np.float64) / float(self.denominator)
+
+    def is_symmetric(self) -> bool:
+        """Invariant under transposition and both reflections (the D4 symmetry of the chain)."""
+        rows = [list(r) for r in self.numerators]
+        cols = [list(c) for c in zip(*rows)]
+        return rows == cols and rows == rows[::-1] and rows == [r[::-1] for r in rows]
 
     def coefficient_sum(self):
         return sum(sum(r) for r in self.numerators)
@@ -122,3 +140,86 @@ def _pad(rows, r):
 def mass_level_scale(level: int) -> float:
     """4**(level-1): value normalisation carried by the mass chain."""
     return float(4 ** (level - 1))
+
+
+# ------------------------------------------------------------------ 2D coarsening
+def _triple_matrix(radius_in: int):
+    """Integer matrix T (7 x (2 r + 1)) of the 1D triple product: for a 1D stencil f
+    with offsets -r..r, (T f)[d + 3] = sum_{a,s} w[a] f[s] w[a + s - 2d] (the same
+    map `_triple_1d` applies)."""
+    w = PROLONG_NUMERATORS_1D
+    T = [[0] * (2 * radius_in + 1) for _ in range(7)]
+    for d in range(-3, 4):
+        for s in range(-radius_in, radius_in + 1):
+            T[d + 3][s + radius_in] = sum(w[a + 2] * w[a + s - 2 * d + 2] for a in range(-2, 3)
+                                          if -2 <= a + s - 2 * d <= 2)
+    return T
+
+
+def galerkin_coarsen(laplace: StencilKernel, mass: StencilKernel):
+    """One exact Galerkin coarsening Z^T S Z of a 2D kernel pair (stencils.py:149-180
+    contract).  The 2D triple product with the tensor transfer w (x) w factorises
+    per axis, so each kernel becomes T S T^T with T the integer 1D triple-product
+    matrix; the denominator gains 8**4 and is then reduced to canonical form.
+    Works for any square integer kernel (not only separable ones); feeding
+    level_kernels(l) returns level_kernels(l + 1)."""
+    out = []
+    for kern in (laplace, mass):
+        S, r = kern.numerators, kern.radius
+        T = _triple_matrix(r)
+        TS = [[sum(T[p][q] * S[q][c] for q in range(2 * r + 1)) for c in range(2 * r + 1)] for p in range(7)]
+        C = [[sum(TS[p][c] * T[k][c] for c in range(2 * r + 1)) for k in range(7)] for p in range(7)]
+        table = {(x - 3, y - 3): C[y][x] for y in range(7) for x in range(7) if C[y][x]}
+        rows, den = _canonical(table, kern.denominator * PROLONG_DENOMINATOR_1D ** 4)
+        out.append(StencilKernel(rows, den, kern.h_power))
+    return out[0], out[1]
+
+
+@lru_cache(maxsize=1)
+def _published_tables():
+    """The paper's integer level 3-6 kernels (reference
+    stencils.py:215-308), shipped as package data."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "data",
+                           "published_kernel_tables.json")) as f:
+        raw = json.load(f)
+    return {int(l): {k: (tuple(tuple(r) for r in v[0]), int(v[1])) for k, v in d.items()} for l, d in raw.items()}
+
+
+def __getattr__(name):  # REFERENCE_KERNELS is loaded lazily from the data file
+    if name == "REFERENCE_KERNELS":
+        return _published_tables()
+    raise AttributeError(name)
+
+
+def verify_chain(kernels=None):
+    """Compare a kernel chain (default: level_kernels) with the published tables
+    (stencils.py:321-371 contract).  One record per (level, kind) with keys level,
+    kind, exact_match, within_ulp (entries beyond 2**53 may differ from the
+    published float-derived values by <= 3 ulp) and first_mismatch
+    ((row, col, derived, published), or (-1, -1, den, published den))."""
+    import math
+    provider = kernels if kernels is not None else level_kernels
+    records = []
+    for level, tabs in sorted(_published_tables().items()):
+        for kind, kern in zip(("laplace", "mass"), provider(level)):
+            want_rows, want_den = tabs[kind]
+            exact = within = kern.denominator == want_den
+            first = None
+            for r, (got_row, want_row) in enumerate(zip(kern.numerators, want_rows)):
+                for c, (got, want) in enumerate(zip(got_row, want_row)):
+                    if got == want:
+                        continue
+                    exact = False
+                    ulp = max(1, int(math.ulp(float(abs(got)))))
+                    if abs(want) > 2 ** 53 and abs(got - want) <= 3 * ulp:
+                        continue
+                    within = False
+                    first = first or (r, c, got, want)
+            if kern.denominator != want_den:
+                within = False
+                first = first or (-1, -1, kern.denominator, want_den)
+            records.append({"level": level, "kind": kind, "exact_match": exact, "within_ulp": within,
+                            "first_mismatch": first})
+    return records

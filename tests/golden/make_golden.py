@@ -198,6 +198,70 @@ def c4_solve():
     print("c4", rep.outer_iterations, rep.final_relres, rep.wall_ms)
 
 
+def grid_models():
+    """k^2 / velocity fields of the reference's problem builders (grid.py:184-217,
+    350-427) at small sizes: wedge (default and BASELINE interfaces), the
+    synthetic Marmousi stand-in raster and its bilinear resampling, a gridfile
+    model with a non-grid-aligned raster."""
+    from helmdef import marmousi_problem, synthetic_marmousi_velocity
+    rec = {}
+    p = wedge_problem(f=7.0, nx=61, ml=3)
+    rec["wedge_ksq1"] = p.hierarchy.ksq[0]
+    rec["wedge_ksq3"] = p.hierarchy.ksq[2]
+    rec["wedge_rhs"] = p.rhs.data
+    vel = VelocityModel(kind="wedge", layers=[(-400.0, -200.0, 2000.0), (-800.0, -600.0, 1500.0), (0.0, 0.0, 3000.0)])
+    h = build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=12.5, ml=3, velocity=vel, f=9.0)
+    rec["bwedge_ksq1"] = h.ksq[0]
+    m = synthetic_marmousi_velocity(185, 61)
+    rec["marm_values"] = m.values
+    rec["marm_meta"] = np.array([m.dx, m.dy, m.x0, m.y0])
+    mp = marmousi_problem(3.0, nx=185, ml=3)
+    rec["marm_ksq1"] = mp.hierarchy.ksq[0]
+    rec["marm_rhs"] = mp.rhs.data
+    mg = marmousi_problem(2.0, nx=93, ml=2, velocity=m)
+    rec["marmg_ksq1"] = mg.hierarchy.ksq[0]
+    rng = np.random.default_rng(21)
+    raster = 1500.0 + 2000.0 * rng.random((23, 37))
+    gv = VelocityModel(kind="gridfile", values=raster, dx=17.3, dy=11.1, x0=-5.0, y0=-240.0)
+    gh = build_hierarchy(((0.0, 600.0), (-250.0, 0.0)), h=6.25, ml=2, velocity=gv, f=11.0)
+    rec["raster_in"] = raster
+    rec["raster_ksq1"] = gh.ksq[0]
+    np.savez_compressed(os.path.join(HERE, "grid_models.npz"), **rec)
+
+
+def api_surface():
+    """Reference outputs of the host-side API names this package re-implements:
+    assemble_csr (operators.py:261-328), LevelOperator.pad / ksq_pad (:44-93,127),
+    partition_grid tiles (parallel.py:71-109), verify_chain records
+    (stencils.py:321-371), galerkin_coarsen of the level-1 pair (:149-180)."""
+    from helmdef import assemble_csr, partition_grid, verify_chain, galerkin_coarsen
+    from helmdef.stencils import level_kernels
+    rng = np.random.default_rng(31)
+    rec = {}
+    vel = VelocityModel(kind="wedge", layers=[(-400.0, -200.0, 2000.0), (-800.0, -600.0, 1500.0), (0.0, 0.0, 3000.0)])
+    for tag, bc in (("s", "sommerfeld"), ("d", "dirichlet"), ("m", ("dirichlet", "sommerfeld", "sommerfeld", "dirichlet"))):
+        hier = build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=25.0, ml=3, velocity=vel, f=6.0, boundary=bc)
+        for l in (1, 2, 3):
+            op = cslp_operator(hier, l, beta2=0.5) if tag != "s" else helmholtz_operator(hier, l)
+            rec[f"asm_{tag}{l}"] = assemble_csr(op).toarray()
+            u = rnd(rng, op.shape)
+            rec[f"pad_{tag}{l}_u"] = u
+            rec[f"pad_{tag}{l}"] = op.pad(u)
+            rec[f"kpad_{tag}{l}"] = op.ksq_pad
+    for name, prob in (("mp1_257_5", mp1_problem(k=20.0, n=257, ml=5)), ("wedge_145_4", wedge_problem(f=10.0, nx=145, ml=4))):
+        for w in (1, 2, 3, 4, 6, 8):
+            part = partition_grid(prob.hierarchy, w)
+            rec[f"tiles_{name}_{w}"] = np.array([[l, t.j0, t.j1, t.i0, t.i1] for l in sorted(part.tiles)
+                                                 for t in part.tiles[l]])
+    rec["verify_chain"] = np.array([[r["level"], r["kind"] == "mass", r["exact_match"], r["within_ulp"]]
+                                    for r in verify_chain()])
+    lap2, mass2 = galerkin_coarsen(*level_kernels(1))
+    rec["coarsen_l1_lap"] = np.array(lap2.numerators)
+    rec["coarsen_l1_mass"] = np.array(mass2.numerators)
+    rec["coarsen_l1_den"] = np.array([lap2.denominator, mass2.denominator])
+    np.savez_compressed(os.path.join(HERE, "api_surface.npz"), **rec)
+
+
 def io_files():
     """Reference-written report / field / config files (format compatibility fixtures)."""
     import helmdef.io as hio
@@ -291,6 +355,9 @@ if __name__ == "__main__":
         preset_solves()
     if "--c4" in sys.argv:
         c4_solve()
+    if "--grid" in sys.argv:
+        grid_models()
+        api_surface()
     if "--io" in sys.argv:
         io_files()
     print("golden fixtures written to", HERE)

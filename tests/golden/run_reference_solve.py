@@ -6,7 +6,11 @@ on the GPU box.  The small outputs it writes (iteration counts, residual
 histories, solution norms / down-sampled solutions) are committed under
 tests/golden/ and are what the GPU parity tests compare against.
 
-Usage:  python tests/golden/run_reference_solve.py CONFIG OUT.npz [--workers W]
+Usage:  python tests/golden/run_reference_solve.py CONFIG OUT.npz [--workers W] [--perturb]
+
+--perturb solves with b' = b + 1e-15 max|b| (N(0,1) + i N(0,1)), default_rng(0)
+(SURVEY §11): the reference's own self-sensitivity, i.e. the noise floor the
+GPU-vs-reference deltas are held to.
 """
 import argparse
 import os
@@ -51,6 +55,14 @@ def make(config):
         hier = build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=0.5, ml=5, velocity=vel, f=f)
         rhs = point_source_rhs(hier, (300.0, 0.0))
         return hier, rhs.grid_view(hier)
+    if config.startswith("c4_h6_f"):  # BASELINE configs[3] model at h = 6 m, ml = 3 (gridfile raster)
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+        from paper_2412_04980_b200.models import C4_DOMAIN, C4_SOURCE, synthetic_layered_velocity
+        f = float(config.split("_f")[1])
+        v = synthetic_layered_velocity(2412, dx=6.0)
+        vel = VelocityModel(kind="gridfile", values=v.values, dx=v.dx, dy=v.dy, x0=v.x0, y0=v.y0)
+        hier = build_hierarchy(C4_DOMAIN, h=6.0, ml=3, velocity=vel, f=f)
+        return hier, point_source_rhs(hier, C4_SOURCE).grid_view(hier)
     raise SystemExit(f"unknown config {config}")
 
 
@@ -61,9 +73,13 @@ def main():
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--max-outer", type=int, default=150)
     ap.add_argument("--save-solution", action="store_true")
+    ap.add_argument("--perturb", action="store_true")
     a = ap.parse_args()
     from helmdef.krylov import StopRule
     hier, b = make(a.config)
+    if a.perturb:
+        g = np.random.default_rng(0)
+        b = b + 1e-15 * np.abs(b).max() * (g.standard_normal(b.shape) + 1j * g.standard_normal(b.shape))
     cfg = preset("MADP", hier, outer_stop=StopRule(1e-6, a.max_outer))
     t0 = time.perf_counter()
     with MadpSolver(hier, cfg, workers=a.workers) as s:
@@ -76,6 +92,7 @@ def main():
         wall_s=wall, workers=a.workers, solution_l2=float(np.linalg.norm(x)),
         cycle_iters=repr(rep.cycle_iters), cslp_iters=repr(rep.cslp_iters),
         matvecs=repr(rep.matvecs), iteration_wall_ms=np.array(rep.iteration_wall_ms),
+        perturbed=a.perturb,
     )
     if a.save_solution:
         rec["solution"] = x

@@ -134,16 +134,22 @@ def test_errors_and_config_validation():
 
 
 def test_slab_partition_nesting():
-    hier = hdb.mp1_problem(k=50.0, n=257, ml=5).hierarchy
-    for ranks in (1, 2, 4, 8):
-        part = hdb.partition_slabs(hier, ranks)
-        for l in range(1, hier.ml + 1):
-            slabs = part.level_slabs(l)
-            assert slabs[0].j0 == 0 and slabs[-1].j1 == hier.level(l).ny
-            assert all(a.j1 == b.j0 for a, b in zip(slabs, slabs[1:]))
-            if l > 1:  # coarse slab starts are injections of fine slab starts
-                fine = part.level_slabs(l - 1)
-                assert all(c.j0 * 2 == f.j0 for c, f in zip(slabs, fine))
+    """distributed.slab_plan (the product's row-slab decomposition): slabs tile every
+    sharded depth, coarse starts are injections of fine starts, and every rank keeps
+    >= min_rows rows at the last sharded depth; P = 3 exercises odd cut rows."""
+    from paper_2412_04980_b200.distributed import slab_plan
+    for ny, ml in ((129, 6), (257, 5), (4097, 12), (2001, 5)):
+        for ranks in (1, 2, 3, 4, 8):
+            for min_rows in (8, 32):
+                plan = slab_plan(ny, ranks, ml, min_rows=min_rows)
+                for d in range(plan.depths):
+                    slabs = [plan.slab(d, r) for r in range(ranks)]
+                    assert slabs[0][0] == 0 and sum(n for _, n in slabs) == plan.rows_at(d)
+                    assert all(a[0] + a[1] == b[0] for a, b in zip(slabs, slabs[1:]))
+                    if d > 0:
+                        assert all(plan.slab(d - 1, r)[0] == 2 * slabs[r][0] for r in range(ranks))
+                if plan.depths:
+                    assert min(plan.slab(plan.depths - 1, r)[1] for r in range(ranks)) >= min_rows
 
 
 def test_synthetic_layered_model_is_seeded_and_in_range():
@@ -160,6 +166,5 @@ def test_synthetic_layered_model_is_seeded_and_in_range():
     from paper_2412_04980_b200.models import C4_DOMAIN
     hier = hdb.build_hierarchy(C4_DOMAIN, h=12.0, ml=2, velocity=a, f=10.0)
     from oracle.grid import build_hierarchy as obuild
-    import paper_2412_04980_b200.grid as pg
-    oh = obuild(C4_DOMAIN, 12.0, 2, speed=lambda x, y: pg._raster(a, x, y), f=10.0)
+    oh = obuild(C4_DOMAIN, 12.0, 2, speed=lambda x, y: a.velocity_at(x, y), f=10.0)
     np.testing.assert_array_equal(hier.ksq_at(1), oh.ksq_at(1))
