@@ -156,7 +156,34 @@ int hdb_solver_precond(hdb_solver* s, int level, const void* v, void* out);
  * host synchronisations and kernel launches                                   */
 int hdb_solver_profile(hdb_solver* s, double* ms_host, long long* calls_host, int cap,
                        long long* syncs, long long* launches);
+/* algorithmic HBM bytes of the last solve's launches (SURVEY §8(d) per-point
+ * figures x points, counted by the host driver; device-resident solves from
+ * their iteration counts) -> solve-level achieved bandwidth = bytes / time      */
+int hdb_solver_bytes(hdb_solver* s, double* alg_bytes);
 int hdb_solver_destroy(hdb_solver* s);
+
+/* separable form of a radius-2/3 Galerkin operator (host-verified factors,
+ * 2r+1 entries each): lap = lsc (sa (x) sm + sm (x) sa), mass = msc (sm (x) sm);
+ * the level then applies as 1D passes (K2) unless "rg_exact" is set          */
+int hdb_op_set_separable(hdb_op* op, const double* sa, const double* sm, double lsc, double msc_re,
+                         double msc_im);
+
+/* ---- engine options (not on the reference API) ----------------------------- */
+/* "mgs_ls": 1 (default) one-launch MGS steps of large levels use the
+ * low-synchronisation form (two grid reductions per Arnoldi step), 0 the
+ * reference's coefficient-by-coefficient MGS order (HDB_MGS_LS=0 likewise).
+ * "rg_exact": 1 radius-2/3 operators use the reference's row-major tap order
+ * (bit-identical to contract_general; HDB_RG_EXACT=1), 0 (default) the
+ * separable 1D passes where the operator has them                            */
+int hdb_option(const char* name, int value);
+
+/* ---- launch accounting / timing (measurement, not on the reference API) ---- */
+/* enable = 1: zero the per-family counters and record a CUDA-event pair on the
+ * library stream around every launch; 0: counters only (always on)           */
+int hdb_kprof(int enable);
+/* family fam (0..count-1; fam < 0 returns the count in *launches): name,
+ * launches, algorithmic bytes and summed event time (ms) since hdb_kprof      */
+int hdb_kprof_read(int fam, char* name_out32, long long* launches, double* alg_bytes, double* device_ms);
 
 #ifdef __cplusplus
 }

@@ -64,7 +64,12 @@ SIGNATURES = {
     "hdb_solver_matvecs": [vp, P(i64), i32],
     "hdb_solver_precond": [vp, i32, vp, vp],
     "hdb_solver_profile": [vp, P(f64), P(i64), i32, P(i64), P(i64)],
+    "hdb_solver_bytes": [vp, P(f64)],
     "hdb_solver_destroy": [vp],
+    "hdb_option": [C.c_char_p, i32],
+    "hdb_op_set_separable": [vp, P(f64), P(f64), f64, f64, f64],
+    "hdb_kprof": [i32],
+    "hdb_kprof_read": [i32, C.c_char_p, P(i64), P(f64), P(f64)],
 }
 _RESTYPE = {"hdb_last_error": C.c_char_p}
 
@@ -136,6 +141,25 @@ def check(status: int):
     if status == 1 and ("preset" in msg or "config" in msg.lower()):
         cls = ConfigError
     raise cls(msg)
+
+
+def kprof(enable: bool):
+    """Arm (zero + per-launch CUDA events) or disarm the library's launch accounting."""
+    check(lib().hdb_kprof(1 if enable else 0))
+
+
+def kprof_read() -> dict:
+    """{family: {"launches", "alg_bytes", "device_ms"}} since the last kprof(...)."""
+    L = lib()
+    cnt = C.c_longlong()
+    check(L.hdb_kprof_read(-1, None, C.byref(cnt), C.byref(C.c_double()), C.byref(C.c_double())))
+    out = {}
+    for f in range(cnt.value):
+        name = C.create_string_buffer(32)
+        n, b, ms = C.c_longlong(), C.c_double(), C.c_double()
+        check(L.hdb_kprof_read(f, name, C.byref(n), C.byref(b), C.byref(ms)))
+        out[name.value.decode()] = {"launches": n.value, "alg_bytes": b.value, "device_ms": ms.value}
+    return out
 
 
 def device_index() -> int:

@@ -509,6 +509,61 @@ int hdb_solver_profile(hdb_solver* s, double* ms_host, long long* calls_host, in
     *launches = r.launches;
   });
 }
+int hdb_solver_bytes(hdb_solver* s, double* alg_bytes) {
+  return guarded([&] { *alg_bytes = s->s.rep.alg_bytes; });
+}
+
+int hdb_op_set_separable(hdb_op* op, const double* sa, const double* sm, double lsc, double msc_re, double msc_im) {
+  return guarded([&] {
+    OpCoef& c = op->op.c;
+    if (c.radius < 2) throw Error(E_ARG, "the separable form applies to radius-2/3 Galerkin levels");
+    const int n = 2 * c.radius + 1;
+    for (int q = 0; q < 7; ++q) {
+      c.sa[q] = q < n ? sa[q] : 0.0;
+      c.sm[q] = q < n ? sm[q] : 0.0;
+    }
+    c.lsc = lsc;
+    c.msc = mkc(msc_re, msc_im);
+    c.sep = 1;
+  });
+}
+
+int hdb_option(const char* name, int value) {
+  return guarded([&] {
+    const std::string k = name ? name : "";
+    if (k == "mgs_ls") set_mgs_ls(value);
+    else if (k == "rg_exact") set_rg_exact(value);
+    else throw Error(E_ARG, "unknown option " + k);
+  });
+}
+
+int hdb_kprof(int enable) {
+  return guarded([&] {
+    Engine& E = engine();
+    E.kp.reset();
+    E.kp.on = enable != 0;
+  });
+}
+
+int hdb_kprof_read(int fam, char* name_out32, long long* launches, double* alg_bytes, double* device_ms) {
+  return guarded([&] {
+    Engine& E = engine();
+    if (fam < 0) {
+      *launches = KF_COUNT;
+      return;
+    }
+    if (fam >= KF_COUNT) throw Error(E_ARG, "kernel family out of range");
+    E.kp.resolve();
+    if (name_out32) {
+      std::strncpy(name_out32, kfam_name(fam), 31);
+      name_out32[31] = 0;
+    }
+    *launches = E.kp.n[fam];
+    *alg_bytes = E.kp.bytes[fam];
+    *device_ms = E.kp.ms[fam];
+  });
+}
+
 int hdb_solver_destroy(hdb_solver* s) {
   return guarded([&] {
     if (engine_ready()) engine().sync();

@@ -15,6 +15,45 @@
 
 namespace hdb {
 
+// ------------------------------------------------------------- launch accounting
+const char* kfam_name(int f) {
+  static const char* names[KF_COUNT] = {"apply5", "residual5", "jacobi5", "resnorm5", "galerkin", "restrict",
+                                        "prolong", "mgs_coop", "mgs_chain", "blas1", "resident_gmres", "control",
+                                        "gemv"};
+  return f >= 0 && f < KF_COUNT ? names[f] : "?";
+}
+
+double gmres_alg_bytes(long long n, int m) {
+  double per = 48.0 + 16.0 * (m + 1) + 72.0;
+  for (int j = 0; j < m; ++j) per += 72.0 + 16.0 * (j + 1);
+  return per * (double)n;
+}
+
+cudaEvent_t KProf::get() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    HDB_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void KProf::resolve() {
+  if (recs.empty()) return;
+  HDB_CUDA(cudaEventSynchronize(recs.back().b));
+  for (const Rec& r : recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.fam] += t;
+  }
+  recs.clear();
+  used = 0;
+}
+
+void KProf::reset() {
+  if (!recs.empty()) resolve();
+  for (int f = 0; f < KF_COUNT; ++f) { bytes[f] = 0; n[f] = 0; ms[f] = 0; }
+}
+
 // ------------------------------------------------------------------ engine
 static std::unique_ptr<Engine> g_engine;
 
@@ -33,6 +72,7 @@ Engine::Engine(int dev) : device(dev) {
 
 Engine::~Engine() {
   cudaStreamSynchronize(st);
+  for (cudaEvent_t e : kp.pool) cudaEventDestroy(e);
   if (own_st) st = own_st;
   delete comm;
   cudaFree(red.partials);
@@ -118,14 +158,12 @@ void LevelOp::reduce(cd* slot) const {
 void LevelOp::apply(const cd* u, cd* out) const {
   Engine& E = engine();
   exchange(u, c.radius);
-  launch_apply(c, g, u, nullptr, ksq, out, 0, E.st);
-  E.launches++;
+  E.kl(c.radius == 1 ? KF_APPLY5 : KF_GALERKIN, 40.0 * n, [&] { launch_apply(c, g, u, nullptr, ksq, out, 0, E.st); });
 }
 void LevelOp::residual(const cd* b, const cd* u, cd* out) const {
   Engine& E = engine();
   exchange(u, c.radius);
-  launch_apply(c, g, u, b, ksq, out, 1, E.st);
-  E.launches++;
+  E.kl(c.radius == 1 ? KF_RESID5 : KF_GALERKIN, 56.0 * n, [&] { launch_apply(c, g, u, b, ksq, out, 1, E.st); });
 }
 void LevelOp::resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const {
   Engine& E = engine();
@@ -137,22 +175,21 @@ void LevelOp::resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const {
       E.red.big = (cd*)E.alloc_bytes(sizeof(cd) * (size_t)G);
       E.red.big_cap = G;
     }
-    launch_resnorm(c, g, u, b, ksq, E.red.big, slot, E.st);
-    E.launches += 2;
+    E.kl(KF_RESNORM, 40.0 * n, [&] { launch_resnorm(c, g, u, b, ksq, E.red.big, slot, E.st); }, 2);
   } else {
-    launch_apply(c, g, u, b, ksq, scratch, 1, E.st);
-    launch_dot(scratch, scratch, n, E.red, slot, E.st);
-    launch_dot(b, b, n, E.red, E.dscal + kSlotMgB, E.st);
-    launch_pack_im(slot, E.dscal + kSlotMgB, E.st);
-    E.launches += 4;
+    E.kl(KF_GALERKIN, 56.0 * n, [&] { launch_apply(c, g, u, b, ksq, scratch, 1, E.st); });
+    E.kl(KF_BLAS, 32.0 * n, [&] {
+      launch_dot(scratch, scratch, n, E.red, slot, E.st);
+      launch_dot(b, b, n, E.red, E.dscal + kSlotMgB, E.st);
+      launch_pack_im(slot, E.dscal + kSlotMgB, E.st);
+    }, 3);
   }
   reduce(slot);
 }
 void LevelOp::jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const {
   Engine& E = engine();
   if (!from_zero) exchange(x, 1);
-  launch_jacobi(c, g, x, b, ksq, out, omega, from_zero, E.st);
-  E.launches++;
+  E.kl(KF_JACOBI, (from_zero ? 40.0 : 56.0) * n, [&] { launch_jacobi(c, g, x, b, ksq, out, omega, from_zero, E.st); });
 }
 
 // ----------------------------------------------------------- level transfers
@@ -186,8 +223,7 @@ void restrict_levels(const LevelOp& f, const LevelOp& c, const cd* fine, cd* out
     coarse_slab_of(f, E.comm->rank, c.g.nyg, r0, rn);
     t.c_row0 = r0;
     t.c_ny = rn;
-    launch_restrict(fine, slab, t, zero_mask, E.st);
-    E.launches++;
+    E.kl(KF_RESTRICT, 20.0 * f.n, [&] { launch_restrict(fine, slab, t, zero_mask, E.st); });
     std::vector<size_t> off(P), bytes(P);
     for (int r = 0; r < P; ++r) {
       int a, n;
@@ -198,15 +234,14 @@ void restrict_levels(const LevelOp& f, const LevelOp& c, const cd* fine, cd* out
     E.comm->allgatherv(slab, out, off, bytes, E.st);
     return;
   }
-  launch_restrict(fine, out, level_tgeom(f, c), zero_mask, E.st);
-  E.launches++;
+  E.kl(KF_RESTRICT, 20.0 * f.n, [&] { launch_restrict(fine, out, level_tgeom(f, c), zero_mask, E.st); });
 }
 
 void prolong_levels(const LevelOp& c, const LevelOp& f, const cd* coarse, const cd* base, cd* fine) {
   Engine& E = engine();
   c.exchange(coarse, 1);
-  launch_prolong(coarse, base, fine, level_tgeom(f, c), base != nullptr, E.st);
-  E.launches++;
+  E.kl(KF_PROLONG, (base ? 36.0 : 20.0) * f.n,
+       [&] { launch_prolong(coarse, base, fine, level_tgeom(f, c), base != nullptr, E.st); });
 }
 
 // ------------------------------------------------------------------- KWS
@@ -242,6 +277,7 @@ KWS::~KWS() {
   if (hflags) cudaFreeHost(hflags);
   E.free(dV);
   E.free(gpart);
+  E.free(tg);
   for (auto p : V) E.free_h(p, halo);
   for (auto p : Z) E.free_h(p, halo);
   E.free_h(tmp, halo);
@@ -308,13 +344,18 @@ bool SmallSolve::try_run(const cd* b, cd* x, Stop stop, int* its_dev, double* re
   Engine& E = engine();
   const int mode = resident_mode(op->n, stop.max_iters);
   if (mode < 0) return false;
-  if (launch_resident_gmres(mode, resident_ortho(), op->c, op->g, op->ksq, b, x, basis, Rg, gpart, op->n,
-                            stop.rel_tol, stop.max_iters, its_dev, rel_dev, E.dscal + kSlotFlag, E.st) != 0) {
+  int rc = 0;
+  E.kl(KF_RESIDENT, 0.0, [&] {
+    rc = launch_resident_gmres(mode, resident_ortho(), op->c, op->g, op->ksq, b, x, basis, Rg, gpart, op->n,
+                               stop.rel_tol, stop.max_iters, its_dev, rel_dev, E.dscal + kSlotFlag, E.st);
+  });
+  if (rc != 0) {
+    E.launches--;
+    E.kp.n[KF_RESIDENT]--;
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) throw Error(E_CUDA, std::string("device-resident GMRES launch: ") + cudaGetErrorString(err));
     return false;  // does not fit the resident working set: caller uses the launch path
   }
-  E.launches++;
   return true;
 }
 
@@ -343,8 +384,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   ws.ensure(n, stop.max_iters, M != nullptr);
   KReport rep;
 
-  launch_dot(b, b, n, E.red, E.dscal + kSlotH, E.st);
-  E.launches++;
+  E.kl(KF_BLAS, 16.0 * n, [&] { launch_dot(b, b, n, E.red, E.dscal + kSlotH, E.st); });
   red(E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   const double bnorm = E.fetch_norm(kSlotH);
@@ -357,9 +397,10 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   double beta = bnorm;
   if (x0) {
     A(x0, ws.tmp);
-    launch_add(b, ws.tmp, ws.tmp, n, 1, E.st);
-    launch_dot(ws.tmp, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
-    E.launches += 2;
+    E.kl(KF_BLAS, 64.0 * n, [&] {
+      launch_add(b, ws.tmp, ws.tmp, n, 1, E.st);
+      launch_dot(ws.tmp, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
+    }, 2);
     red(E.dscal + kSlotH);
     r0 = ws.tmp;
   }
@@ -383,8 +424,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   }
   if (!std::isfinite(beta)) throw Error(E_NONFINITE, "initial residual is not finite");
 
-  launch_scale(r0, ws.v(0), 1.0 / beta, n, E.st);  // V0 = r0 / beta
-  E.launches++;
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_scale(r0, ws.v(0), 1.0 / beta, n, E.st); });  // V0 = r0 / beta
 
   std::vector<std::vector<cplx>> R;
   std::vector<double> cs;
@@ -392,6 +432,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   g.push_back(cplx(beta, 0.0));
   int its = 0;
   bool conv = false;
+  bool ls_ok = true;
   for (int j = 0; j < stop.max_iters; ++j) {
     const cd* z = ws.v(j);
     if (M) {
@@ -418,20 +459,37 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     };
     if (!shard && n >= coop_mgs_min()) {
       if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
+      if (!ws.tg) ws.tg = E.alloc(mgs_ls_tg_elems());
       ensure_dv();
-      coop = launch_mgs_grid(w, (const cd* const*)ws.dV, j, n, ws.gpart, E.dscal + kSlotH, E.st) == 0;
-      if (coop) E.launches++;
+      // the low-synchronisation step needs every earlier step of this Arnoldi process in it
+      if (j == 0) ls_ok = true;
+      const bool use_ls = ls_ok && mgs_ls_fits(n, j);
+      ls_ok = use_ls;
+      E.kl(KF_MGS_COOP, (16.0 * (j + 1) + 32.0) * n, [&] {
+        coop = launch_mgs_grid(w, (const cd* const*)ws.dV, j, n, ws.gpart, E.dscal + kSlotH, E.st, nullptr,
+                               use_ls ? ws.tg : nullptr) == 0;
+      });
+      if (!coop) {  // did not fit or could not be co-scheduled: clear the error, use the chain
+        cudaGetLastError();
+        ls_ok = false;
+        E.launches--;
+        E.kp.n[KF_MGS_COOP]--;
+        E.kp.bytes[KF_MGS_COOP] -= (16.0 * (j + 1) + 32.0) * n;
+      }
     }
     if (!coop) {
-      launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st);
+      E.kl(KF_MGS_CHAIN, 32.0 * n, [&] { launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st); });
       red(E.dscal + kSlotH);
       for (int i = 0; i < j; ++i) {
-        launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
+        E.kl(KF_MGS_CHAIN, 64.0 * n, [&] {
+          launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
+        });
         red(E.dscal + kSlotH + i + 1);
       }
-      launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
+      E.kl(KF_MGS_CHAIN, 48.0 * n, [&] {
+        launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
+      });
       red(E.dscal + kSlotH + j + 1);
-      E.launches += j + 2;
     }
     E.fetch(kSlotH + j + 2);
     std::vector<cplx> col(j + 2);
@@ -473,10 +531,8 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
       conv = true;
       break;
     }
-    if (!coop) {  // the cooperative MGS already wrote V_{j+1} = w / hnext
-      launch_scale(w, w, 1.0 / hn, n, E.st);
-      E.launches++;
-    }
+    if (!coop)  // the cooperative MGS already wrote V_{j+1} = w / hnext
+      E.kl(KF_BLAS, 32.0 * n, [&] { launch_scale(w, w, 1.0 / hn, n, E.st); });
   }
   // least squares R y = g (krylov.py:161-168), solution update (169-172)
   const int m = its;
@@ -492,12 +548,10 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   }
   HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*) * m, cudaMemcpyHostToDevice, E.st));
   HDB_CUDA(cudaMemcpyAsync(ws.dy, ws.hy, sizeof(cd) * m, cudaMemcpyHostToDevice, E.st));
-  launch_lincomb(ws.dbasis, ws.dy, m, x0, x, n, E.st);
-  E.launches++;
+  E.kl(KF_BLAS, 16.0 * (m + 1 + (x0 ? 1 : 0)) * n, [&] { launch_lincomb(ws.dbasis, ws.dy, m, x0, x, n, E.st); });
   // explicit true residual (krylov.py:174)
   A(x, ws.tmp);
-  launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
-  E.launches++;
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st); });
   red(E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   const double fin = E.fetch_norm(kSlotH) / bnorm;
@@ -542,6 +596,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
   Engine& E = engine();
   ws.ensure(n, cap, false);
   if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
+  if (!ws.tg) ws.tg = E.alloc(mgs_ls_tg_elems());
   if (ws.gst_cap < cap) {
     E.free(ws.gst);
     ws.gst = E.alloc(gm_state_elems(cap));
@@ -554,10 +609,9 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
   cd* hcol = E.dscal + kSlotH;
   cd* flag = E.dscal + kSlotFlag;
   ensure_vtab(ws, 0);
-  launch_dot(b, b, n, E.red, hcol, E.st);
-  launch_gm_init(hcol, st, lay, flag, E.st);
-  launch_gm_scale(b, ws.v(0), st, n, E.st);  // krylov.py:92-115 with x0 = 0
-  E.launches += 3;
+  E.kl(KF_BLAS, 16.0 * n, [&] { launch_dot(b, b, n, E.red, hcol, E.st); });
+  E.kl(KF_CONTROL, 0.0, [&] { launch_gm_init(hcol, st, lay, flag, E.st); });
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_gm_scale(b, ws.v(0), st, n, E.st); });  // krylov.py:92-115 with x0 = 0
   OpCoef cs = op->c;
   cs.skip = skip;
   // first batch: one short of the previous solve's count (the counts of one
@@ -568,13 +622,17 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
     const int jend = std::min(cap, j + batch);
     ensure_vtab(ws, jend);
     for (; j < jend; ++j) {
-      launch_apply(cs, op->g, ws.v(j), nullptr, op->ksq, ws.v(j + 1), 0, E.st);  // krylov.py:119
-      if (launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip) != 0) {
+      // bytes are booked after the loop for the steps that ran (later ones return at once)
+      E.kl(op->c.radius == 1 ? KF_APPLY5 : KF_GALERKIN, 0.0,
+           [&] { launch_apply(cs, op->g, ws.v(j), nullptr, op->ksq, ws.v(j + 1), 0, E.st); });  // krylov.py:119
+      int rc = 0;
+      E.kl(KF_MGS_COOP, 0.0,
+           [&] { rc = launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip, ws.tg); });
+      if (rc != 0) {
         const cudaError_t err = cudaGetLastError();
         throw Error(E_CUDA, std::string("cooperative MGS launch: ") + cudaGetErrorString(err));
       }
-      launch_gm_givens(j, hcol, st, lay, cap, stop.rel_tol, flag, E.st);
-      E.launches += 3;
+      E.kl(KF_CONTROL, 0.0, [&] { launch_gm_givens(j, hcol, st, lay, cap, stop.rel_tol, flag, E.st); });
     }
     HDB_CUDA(cudaMemcpyAsync(ws.hflags, skip, 2 * sizeof(int), cudaMemcpyDeviceToHost, E.st));
     HDB_CUDA(cudaStreamSynchronize(E.st));
@@ -583,17 +641,20 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
     batch = 3;
   }
   const int its = ws.hflags[1];
+  for (int q = 0; q < its; ++q) {
+    E.kp.bytes[op->c.radius == 1 ? KF_APPLY5 : KF_GALERKIN] += 40.0 * n;
+    E.kp.bytes[KF_MGS_COOP] += (16.0 * (q + 1) + 32.0) * n;
+  }
   if (its == 0) {
     HDB_CUDA(cudaMemsetAsync(x, 0, sizeof(cd) * n, E.st));  // b = 0 (or non-finite ||b||: flag raised)
   } else {
-    launch_gm_solve(st, lay, E.st);  // krylov.py:161-168
-    launch_lincomb((const cd* const*)ws.dV, gm_y(st, lay), its, nullptr, x, n, E.st);  // 169-172
-    op->apply(x, ws.tmp);                                                               // 174
-    launch_subnorm(b, ws.tmp, n, E.red, hcol, E.st);
-    E.launches += 3;
+    E.kl(KF_CONTROL, 0.0, [&] { launch_gm_solve(st, lay, E.st); });  // krylov.py:161-168
+    E.kl(KF_BLAS, 16.0 * (its + 1) * n,
+         [&] { launch_lincomb((const cd* const*)ws.dV, gm_y(st, lay), its, nullptr, x, n, E.st); });  // 169-172
+    op->apply(x, ws.tmp);                                                                           // 174
+    E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, hcol, E.st); });
   }
-  launch_gm_final(hcol, st, lay, its_dev, rel_dev, flag, E.st);
-  E.launches++;
+  E.kl(KF_CONTROL, 0.0, [&] { launch_gm_final(hcol, st, lay, its_dev, rel_dev, flag, E.st); });
   ws.last_its = its;
   return true;
 }
@@ -614,26 +675,25 @@ void fgmres_step1(long long n, const LinOp& A, const LinOp& M, const cd* b, cd* 
     if (shard) dist->reduce(E.dscal + slot);
   };
   cd* S = E.dscal;
-  launch_dot(b, b, n, E.red, S + kS1B, E.st);  // ||b||^2 (krylov.py:92)
+  E.kl(KF_BLAS, 16.0 * n, [&] { launch_dot(b, b, n, E.red, S + kS1B, E.st); });  // ||b||^2 (krylov.py:92)
   red(kS1B);
-  launch_scale_dev(b, ws.v(0), S + kS1B, n, E.st);  // V0 = r0 / beta
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_scale_dev(b, ws.v(0), S + kS1B, n, E.st); });  // V0 = r0 / beta
   M(ws.v(0), ws.z(0));
   cd* w = ws.v(1);
   A(ws.z(0), w);
-  launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, S + kS1H0, E.st);  // h0 = <V0, w>
+  E.kl(KF_MGS_CHAIN, 32.0 * n, [&] { launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, S + kS1H0, E.st); });
   red(kS1H0);
-  launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st);  // w -= h0 V0; ||w||^2
+  E.kl(KF_MGS_CHAIN, 48.0 * n, [&] { launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st); });
   red(kS1HN);
-  launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st);
+  E.kl(KF_CONTROL, 0.0, [&] { launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st); });
   ws.hbasis[0] = ws.z(0);
   HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*), cudaMemcpyHostToDevice, E.st));
-  launch_lincomb(ws.dbasis, S + kS1Y, 1, nullptr, x, n, E.st);  // x = y0 Z0
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_lincomb(ws.dbasis, S + kS1Y, 1, nullptr, x, n, E.st); });  // x = y0 Z0
   // explicit true residual: only its finiteness matters to the caller (krylov.py:174-176)
   A(x, ws.tmp);
-  launch_subnorm(b, ws.tmp, n, E.red, S + kS1F, E.st);
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, S + kS1F, E.st); });
   red(kS1F);
-  launch_finite_guard(S + kS1F, S + kSlotFlag, E.st);
-  E.launches += 9;
+  E.kl(KF_CONTROL, 0.0, [&] { launch_finite_guard(S + kS1F, S + kSlotFlag, E.st); });
 }
 
 // --------------------------------------------------------------- Bi-CGSTAB
@@ -657,8 +717,7 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
   *breakdown = false;
   const bool shard = dist && dist->sharded;
   auto dotv = [&](const cd* u, const cd* w) {  // conj-dot to the host (one sync)
-    launch_dot(u, w, n, E.red, E.dscal + kSlotH, E.st);
-    E.launches++;
+    E.kl(KF_BLAS, (u == w ? 16.0 : 32.0) * n, [&] { launch_dot(u, w, n, E.red, E.dscal + kSlotH, E.st); });
     if (shard) dist->reduce(E.dscal + kSlotH);
     E.fetch(kSlotH + 1);
     return cplx(E.hscal[kSlotH].x, E.hscal[kSlotH].y);
@@ -670,7 +729,7 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
   if (x0) {
     HDB_CUDA(cudaMemcpyAsync(x, x0, bytes, cudaMemcpyDeviceToDevice, E.st));
     A(x0, ws.tmp);
-    launch_add(b, ws.tmp, ws.r, n, 1, E.st);
+    E.kl(KF_BLAS, 48.0 * n, [&] { launch_add(b, ws.tmp, ws.r, n, 1, E.st); });
   } else {
     HDB_CUDA(cudaMemsetAsync(x, 0, bytes, E.st));
     HDB_CUDA(cudaMemcpyAsync(ws.r, b, bytes, cudaMemcpyDeviceToDevice, E.st));
@@ -705,16 +764,19 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
     const cplx rho_new = dotv(ws.rhat, ws.r);
     if (std::abs(rho_new) < eps * bnorm * bnorm) { brk("rho vanished in Bi-CGSTAB"); return rep; }
     const cplx beta = (rho_new / rho) * (alpha / omega);
-    launch_bicg_p(ws.r, ws.p, ws.v, mkc(beta.real(), beta.imag()), mkc(omega.real(), omega.imag()), n, E.st);
+    E.kl(KF_BLAS, 64.0 * n, [&] {
+      launch_bicg_p(ws.r, ws.p, ws.v, mkc(beta.real(), beta.imag()), mkc(omega.real(), omega.imag()), n, E.st);
+    });
     const cd* phat = ws.p;
     if (M) { (*M)(ws.p, ws.ph); phat = ws.ph; }
     A(phat, ws.v);
     const cplx denom = dotv(ws.rhat, ws.v);
     if (std::abs(denom) < eps * bnorm * bnorm) { brk("alpha denominator vanished in Bi-CGSTAB"); return rep; }
     alpha = rho_new / denom;
-    launch_axpy(ws.r, mkc(alpha.real(), alpha.imag()), ws.v, ws.s, n, 1, E.st);  // s = r - alpha v
-    launch_axpy(x, mkc(alpha.real(), alpha.imag()), phat, x, n, 0, E.st);        // x = x + alpha phat
-    E.launches += 3;
+    E.kl(KF_BLAS, 96.0 * n, [&] {
+      launch_axpy(ws.r, mkc(alpha.real(), alpha.imag()), ws.v, ws.s, n, 1, E.st);  // s = r - alpha v
+      launch_axpy(x, mkc(alpha.real(), alpha.imag()), phat, x, n, 0, E.st);        // x = x + alpha phat
+    }, 2);
     its = it;
     const double srel = nrm(ws.s) / bnorm;
     if (srel <= stop.rel_tol) {
@@ -729,9 +791,10 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
     if (std::abs(tt) < eps) { brk("omega denominator vanished in Bi-CGSTAB"); return rep; }
     omega = dotv(ws.t, ws.s) / tt;
     if (std::abs(omega) < eps) { brk("omega vanished in Bi-CGSTAB"); return rep; }
-    launch_axpy(x, mkc(omega.real(), omega.imag()), shat, x, n, 0, E.st);     // x = x + omega shat
-    launch_axpy(ws.s, mkc(omega.real(), omega.imag()), ws.t, ws.r, n, 1, E.st);  // r = s - omega t
-    E.launches += 2;
+    E.kl(KF_BLAS, 96.0 * n, [&] {
+      launch_axpy(x, mkc(omega.real(), omega.imag()), shat, x, n, 0, E.st);     // x = x + omega shat
+      launch_axpy(ws.s, mkc(omega.real(), omega.imag()), ws.t, ws.r, n, 1, E.st);  // r = s - omega t
+    }, 2);
     rel = nrm(ws.r) / bnorm;
     rep.history.push_back(rel);
     if (!std::isfinite(rel)) throw Error(E_NONFINITE, "non-finite residual in Bi-CGSTAB");
@@ -742,8 +805,7 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
     rho = rho_new;
   }
   A(x, ws.tmp);  // final true residual (krylov.py:275)
-  launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
-  E.launches++;
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st); });
   if (shard) dist->reduce(E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   rep.iterations = its;
@@ -795,8 +857,7 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
   const int L = (int)ops.size();
   if (i == L - 1) {  // mg.py:104-109
     if (Ainv) {
-      launch_gemv(Ainv, b, x, ninv, E.st);
-      E.launches++;
+      E.kl(KF_GEMV, 16.0 * ninv * (double)ninv + 32.0 * ninv, [&] { launch_gemv(Ainv, b, x, ninv, E.st); });
     } else {
       const LevelOp* op = ops[i];
       Engine& E2 = engine();
@@ -850,17 +911,16 @@ void Multigrid::vcycle(const cd* b, cd* x, const cd* x0) {
   // r0 (mg.py:131): ||b|| from zero, ||b - M x0|| otherwise
   if (x0) {
     op->residual(b, x0, R[0]);
-    launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgR0, E.st);
-    E.launches++;
+    E.kl(KF_BLAS, 16.0 * op->n, [&] { launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgR0, E.st); });
     op->reduce(E.dscal + kSlotMgR0);
   }
   cycle(0, b, x, x0);
   // divergence guard (mg.py:133-138), evaluated on device; raised at the next host sync.
   // One fused pass: (||b - M x||^2, ||b||^2) without storing the residual.
   op->resnorm(b, x, E.dscal + kSlotMgPost, R[0]);
-  launch_guard(E.dscal + kSlotMgPost, nullptr, x0 ? E.dscal + kSlotMgR0 : nullptr, guard, E.dscal + kSlotFlag,
-               E.st);
-  E.launches += 1;
+  E.kl(KF_CONTROL, 0.0, [&] {
+    launch_guard(E.dscal + kSlotMgPost, nullptr, x0 ? E.dscal + kSlotMgR0 : nullptr, guard, E.dscal + kSlotFlag, E.st);
+  });
 }
 
 }  // namespace hdb
@@ -1011,6 +1071,7 @@ void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
   if (!M->sharded && resident_mode(M->n, L.cslp_stop.max_iters) >= 0) {
     L.small_cslp.ensure(M, L.cslp_stop.max_iters);
     const int slot = reserve_count(l);
+    slot_npts[slot] = M->n;
     if (L.small_cslp.try_run(rhs, out, L.cslp_stop, dcounts + slot, drel + slot)) return;
     unreserve_count(l);  // did not fit: the launch path below reports its own count
   }
@@ -1031,6 +1092,7 @@ int MadpSolver::reserve_count(int level) {
   auto& lst = level < 0 ? rep.cycle_iters[-level] : rep.cslp_iters[level];
   lst.push_back(-1);
   pending.emplace_back(level, (int)lst.size() - 1);
+  slot_npts.push_back(0);
   return dused++;
 }
 
@@ -1038,6 +1100,7 @@ void MadpSolver::unreserve_count(int level) {
   auto& lst = level < 0 ? rep.cycle_iters[-level] : rep.cslp_iters[level];
   lst.pop_back();
   pending.pop_back();
+  slot_npts.pop_back();
   dused--;
 }
 
@@ -1052,10 +1115,12 @@ void MadpSolver::flush_counts() {
       const int lvl = pending[k].first;
       if (lvl < 0) rep.cycle_iters[-lvl][pending[k].second] = h[k];
       else rep.cslp_iters[lvl][pending[k].second] = h[k];
+      if (slot_npts[k] > 0) E.kp.bytes[KF_RESIDENT] += gmres_alg_bytes(slot_npts[k], h[k]);
     }
   }
   dused = 0;
   pending.clear();
+  slot_npts.clear();
 }
 
 // madp.py:301-327  (A-DEF1, lambda = 1)
@@ -1085,14 +1150,14 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   rep.matvecs[l] += 1;
   L.A->residual(v, L.t, L.rhs);  // v - A t
   cslp_apply(l, L.rhs, L.r);
-  launch_add(L.r, L.t, out, L.A->n, 0, E.st);  // r + t
-  E.launches++;
+  E.kl(KF_BLAS, 48.0 * L.A->n, [&] { launch_add(L.r, L.t, out, L.A->n, 0, E.st); });  // r + t
 }
 
 void MadpSolver::solve(const cd* b, cd* x) {
   Engine& E = engine();
   setup();
   reset_report();
+  const double bytes0 = E.kp.total_bytes();
   HDB_CUDA(cudaMemsetAsync(E.dscal + kSlotFlag, 0, sizeof(cd), E.st));
   cudaEvent_t e0, e1;
   HDB_CUDA(cudaEventCreate(&e0));
@@ -1130,6 +1195,7 @@ void MadpSolver::solve(const cd* b, cd* x) {
   rep.wall_ms = ms;
   rep.syncs = E.syncs - s0;
   rep.launches = E.launches - l0;
+  rep.alg_bytes = E.kp.total_bytes() - bytes0;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
 }

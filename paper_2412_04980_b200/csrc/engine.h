@@ -38,6 +38,52 @@ constexpr int kSlotMgPost = 1020;
 constexpr int kSlotMgB = 1021;
 constexpr int kSlotMisc = 1022;
 
+// Kernel families for the launch accounting (algorithmic HBM bytes per launch,
+// SURVEY §8(d) per-point figures x the points the launch covers) and, when
+// armed, per-launch CUDA-event timing on the engine stream (hdb_kprof).
+enum KFam {
+  KF_APPLY5 = 0,   // radius-1 apply, 40 B/pt
+  KF_RESID5,       // radius-1 residual b - A u, 56 B/pt
+  KF_JACOBI,       // damped Jacobi sweep, 56 B/pt (40 from zero)
+  KF_RESNORM,      // fused residual + norms, 40 B/pt
+  KF_GALERKIN,     // radius-2/3 apply or residual, 40 / 56 B/pt
+  KF_RESTRICT,     // Z^T, 20 B per fine pt
+  KF_PROLONG,      // Z, 20 (36 with base) B per fine pt
+  KF_MGS_COOP,     // one-launch MGS step, 16 (j + 1) + 32 B/pt
+  KF_MGS_CHAIN,    // fused MGS launches of the chain, 32-64 B/pt each
+  KF_BLAS,         // dot / norm / scale / add / axpy / lincomb
+  KF_RESIDENT,     // device-resident GMRES solves (bytes from their iteration counts)
+  KF_CONTROL,      // Givens, least squares, guards, flags (no field traffic)
+  KF_GEMV,         // dense inverse at the multigrid bottom, 16 n^2 B
+  KF_COUNT
+};
+const char* kfam_name(int f);
+
+struct KProf {
+  bool on = false;                 // record an event pair around every launch
+  double bytes[KF_COUNT] = {};     // always accumulated
+  long long n[KF_COUNT] = {};
+  double ms[KF_COUNT] = {};        // resolved event time (armed only)
+  struct Rec { int fam; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  cudaEvent_t get();
+  void resolve();                  // wait for the recorded pairs, add their times
+  void reset();
+  double total_bytes() const {
+    double t = 0;
+    for (double b : bytes) t += b;
+    return t;
+  }
+};
+
+// algorithmic bytes of one GMRES solve of m iterations on n points, counted the
+// way the reference's algorithm streams its vectors (krylov.py:92-176): ||b||
+// and V0 (48), per iteration a stencil (40) and the MGS chain 16 (j + 1) + 32,
+// the solution update 16 (m + 1) and the true residual (40 + 32)
+double gmres_alg_bytes(long long n, int m);
+
 struct Engine {
   int device = 0;
   cudaStream_t st = nullptr;      // stream all work is ordered on (may be external)
@@ -49,6 +95,27 @@ struct Engine {
   long long launches = 0;  // kernels launched through the engine (telemetry)
   long long syncs = 0;     // host synchronisations (Hessenberg reads etc.)
   Comm* comm = nullptr;    // row-slab communicator of this rank (owned), null on one rank
+  KProf kp;                // launch accounting / optional per-launch timing
+  // run `f` (which enqueues `nl` kernels of family `fam` moving `bytes`
+  // algorithmic bytes) with optional event timing around it
+  template <class F>
+  void kl(int fam, double bytes, F&& f, int nl = 1) {
+    cudaEvent_t a = nullptr;
+    if (kp.on) {
+      a = kp.get();
+      cudaEventRecord(a, st);
+    }
+    f();
+    launches += nl;
+    kp.bytes[fam] += bytes;
+    kp.n[fam] += nl;
+    if (a) {
+      cudaEvent_t b = kp.get();
+      cudaEventRecord(b, st);
+      kp.recs.push_back({fam, a, b});
+      if (kp.recs.size() > 40000) kp.resolve();
+    }
+  }
 
   explicit Engine(int dev);
   ~Engine();
@@ -115,6 +182,7 @@ struct KWS {
   cd** dV = nullptr;       // device table of V pointers (cooperative MGS)
   int dV_cap = 0, dV_n = 0;
   cd* gpart = nullptr;     // grid-reduction partials
+  cd* tg = nullptr;        // T = (I + L)^{-1} rows of the low-synchronisation MGS (mgs_ls_tg_elems())
   cd* tmp = nullptr;
   cd** dbasis = nullptr;   // device pointer table for the solution update
   cd* dy = nullptr;
@@ -240,6 +308,7 @@ struct SolveReport {
   std::vector<long long> matvecs;
   std::vector<double> iter_wall_ms;
   double wall_ms = 0.0;
+  double alg_bytes = 0.0;  // algorithmic HBM bytes of the solve's launches (KProf counters)
 };
 
 struct MadpSolver {
@@ -248,6 +317,7 @@ struct MadpSolver {
   double* drel = nullptr;
   int dcap = 0, dused = 0;
   std::vector<std::pair<int, int>> pending;  // (level, index into cslp_iters[level]) per slot
+  std::vector<long long> slot_npts;          // points of a device-resident solve's level (bytes at flush), else 0
   void flush_counts();
   // device timing (HDB_PROFILE=1): event pairs per (level, kind), resolved at the end of a solve
   struct EvRec { int slot; cudaEvent_t a, b; };

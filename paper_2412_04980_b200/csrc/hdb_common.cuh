@@ -67,6 +67,13 @@ struct OpCoef {
   double ku;             // that constant
   cd ucoef[49];          // lap + mass * ku per tap, same rounded operations as the per-point form
   const int* skip = nullptr;  // device flag: nonzero -> the launch does nothing (device-driven loops)
+  // separable form of a radius-2/3 Galerkin level:
+  //   lap[a][b] = lsc * (sa[a] sm[b] + sm[a] sa[b]),  mass[a][b] = msc * sm[a] sm[b]
+  // (host-verified reconstruction); used unless the exact tap order is requested
+  int sep = 0;
+  double sa[7], sm[7];
+  double lsc;
+  cd msc;
 };
 
 constexpr int kReduceThreads = 256;

@@ -55,8 +55,15 @@ int resident_grid_ctas();
 int resident_vec_cap();
 void resident_set_profile(long long* dev_counters);
 // one Arnoldi step's MGS chain in a cooperative launch (large levels); 1 = does not fit
+// tg != null: the low-synchronisation form (two grid reductions per step) where the
+// level fits it; tg holds the T = (I + L)^{-1} rows of the Arnoldi process so far
+// (mgs_ls_tg_elems() elements; every step j of the process must go through it)
 int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
-                    const int* skip = nullptr);
+                    const int* skip = nullptr, cd* tg = nullptr);
+bool mgs_ls_fits(long long n, int j);
+void set_mgs_ls(int on);
+void set_rg_exact(int on);  // 1: radius-2/3 levels use the reference's exact tap order (HDB_RG_EXACT=1)  // runtime switch (HDB_MGS_LS=0 at start-up does the same)
+long long mgs_ls_tg_elems();
 bool mgs_grid_fits(long long n);
 // device-driven GMRES control (launch path; kernels_resident.cu)
 long long gm_state_elems(int cap);

@@ -1212,6 +1212,194 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid_t(cd* w, const cd* const* V, i
   }
 }
 
+// ---------------------------------------------------------------------------
+// Low-synchronisation MGS step (one-reduce MGS in the compact-WY form of
+// Swirydowicz, Langou, Ananthan, Yang & Thomas, "Low synchronization
+// Gram-Schmidt and GMRES algorithms", NLAA 2020).  MGS computes
+//     h_i = <V_i, w - sum_{k<i} h_k V_k> = g_i - sum_{k<i} <V_i, V_k> h_k,
+// i.e. h = (I + L)^{-1} g with g = V^H w and L the strictly lower part of
+// V^H V.  One streaming pass over V_0..V_{j-1} yields g and the new row of L
+// (<V_j, V_k>, k < j) together; ONE grid reduction combines them; the new row
+// of T = (I + L)^{-1} (t_jk = -sum_{m=k}^{j-1} <V_j, V_m> T_mk, rows < j kept
+// in Tg from the earlier steps) and h = T g follow redundantly in every CTA; a
+// second pass subtracts h_k V_k (V_j from shared memory, then V_{j-1}..V_0,
+// the recently streamed vectors first so they are still in L2); one more
+// reduction gives ||w||^2.  Two grid barriers per Arnoldi step instead of
+// j + 2, at the price of re-reading the basis (partly from L2).  Same
+// coefficients as MGS in exact arithmetic (krylov.py:121-124); the rounding
+// differs like the reference's own worker-count-dependent zdotc rounding does.
+// w and V_j slices both live in shared memory: levels with <= kLsMaxChunk
+// points per CTA (the 1025^2 level of config 2: 7099).
+constexpr int kLsSlot = 14;                // slice elements per thread (kRT * 14 >= chunk)
+constexpr int kLsMaxJ = 63;                // 4 j + 2 scalars fit the staging area
+constexpr int kLsStage = 16;               // reduced elements per warp-partial staging round
+struct LsSmem {
+  MgsSmem red;
+  cd stage[kRT / 32][kLsStage];            // warp partials; reused for g, l, t-row and h
+};
+constexpr size_t kLsHead = ((sizeof(LsSmem) + 127) / 128) * 128;
+
+__global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, int j, long long n, cd* gpart,
+                                                   cd* hout, cd* Tg, const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  LsSmem& s = *reinterpret_cast<LsSmem*>(smem_raw);
+  cg::grid_group gr = cg::this_grid();
+  const int P = gridDim.x, rank = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
+  const int cnt = (int)(p1 - p0);
+  const int cap = (int)((n + P - 1) / P);
+  cd* ws = reinterpret_cast<cd*>(smem_raw + kLsHead);
+  cd* vj = ws + ((cap + 7) / 8) * 8;
+  load_slice_smem(ws, w + p0, cnt);
+  load_slice_smem(vj, V[j] + p0, cnt);
+  __syncthreads();
+  const int ne = 2 * j + 1;  // g_0..g_j, then l_0..l_{j-1}
+  cd pw[4];                   // this warp's partial of element e sits in lane e % 32, slot e / 32
+#pragma unroll
+  for (int k = 0; k < 4; ++k) pw[k] = mkc(0.0, 0.0);
+  auto stash = [&](int e, cd v) {
+    v = warp_sum_c(v);
+    v.x = __shfl_sync(0xffffffffu, v.x, 0);
+    v.y = __shfl_sync(0xffffffffu, v.y, 0);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (e == 32 * k + lane) pw[k] = v;
+  };
+  // pass A: g_k = <V_k, w>, l_k = <V_j, V_k> for k < j, one read of each V_k
+  for (int k = 0; k < j; ++k) {
+    const cd* vk = V[k] + p0;
+    cd r[kLsSlot];
+#pragma unroll
+    for (int m = 0; m < kLsSlot; ++m) {
+      const int q = t + m * kRT;
+      r[m] = q < cnt ? __ldcg(vk + q) : mkc(0.0, 0.0);
+    }
+    cd ag = mkc(0.0, 0.0), al = mkc(0.0, 0.0);
+#pragma unroll
+    for (int m = 0; m < kLsSlot; ++m) {
+      const int q = t + m * kRT;
+      if (q < cnt) {
+        ag = c_conjmul_acc(ag, r[m], ws[q]);
+        al = c_conjmul_acc(al, vj[q], r[m]);
+      }
+    }
+    stash(k, ag);
+    stash(j + 1 + k, al);
+  }
+  {
+    cd ag = mkc(0.0, 0.0);
+    for (int q = t; q < cnt; q += kRT) ag = c_conjmul_acc(ag, vj[q], ws[q]);
+    stash(j, ag);
+  }
+  // block partials (16 warps in order) -> gpart region 0, one grid barrier
+  for (int e0 = 0; e0 < ne; e0 += kLsStage) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = 32 * k + lane;
+      if (e >= e0 && e < e0 + kLsStage && e < ne) s.stage[wid][e - e0] = pw[k];
+    }
+    __syncthreads();
+    if (t < kLsStage && e0 + t < ne) {
+      cd a = mkc(0.0, 0.0);
+#pragma unroll
+      for (int ww = 0; ww < kRT / 32; ++ww) {
+        a.x += s.stage[ww][t].x;
+        a.y += s.stage[ww][t].y;
+      }
+      __stcg(&gpart[(long long)rank * kVecCap + e0 + t], a);
+    }
+    __syncthreads();
+  }
+  gr.sync();
+  cd* tot = &s.stage[0][0];  // [0, 2j]: g then l; [2j+1, 3j]: new T row; [3j+1, 4j+1]: h
+  for (int e = wid; e < ne; e += kRT / 32) {  // rank-ordered per lane, then a fixed warp tree
+    cd a = mkc(0.0, 0.0);
+    for (int r = lane; r < P; r += 32) {
+      const cd z = __ldcg(&gpart[(long long)r * kVecCap + e]);
+      a.x += z.x;
+      a.y += z.y;
+    }
+    a = warp_sum_c(a);
+    if (lane == 0) tot[e] = a;
+  }
+  __syncthreads();
+  cd* trow = tot + ne;
+  cd* hs = trow + j;
+  const long long rj = (long long)j * (j + 1) / 2;
+  if (t < j) {  // t_jk = -sum_{m=k}^{j-1} l_m T_mk
+    cd a = mkc(0.0, 0.0);
+    for (int m = t; m < j; ++m) {
+      const cd tm = __ldcg(&Tg[(long long)m * (m + 1) / 2 + t]);
+      const cd lm = tot[j + 1 + m];
+      a.x = __fma_rn(lm.x, tm.x, a.x); a.x = __fma_rn(-lm.y, tm.y, a.x);
+      a.y = __fma_rn(lm.x, tm.y, a.y); a.y = __fma_rn(lm.y, tm.x, a.y);
+    }
+    trow[t] = mkc(-a.x, -a.y);
+    if (rank == 0) Tg[rj + t] = mkc(-a.x, -a.y);
+  }
+  if (rank == 0 && t == 0) Tg[rj + j] = mkc(1.0, 0.0);
+  __syncthreads();
+  if (t <= j) {  // h_i = sum_{k <= i} T_ik g_k
+    cd a = mkc(0.0, 0.0);
+    const long long ri = (long long)t * (t + 1) / 2;
+    for (int k = 0; k <= t; ++k) {
+      const cd tk = t < j ? (k < t ? __ldcg(&Tg[ri + k]) : mkc(1.0, 0.0)) : (k < j ? trow[k] : mkc(1.0, 0.0));
+      const cd gk = tot[k];
+      a.x = __fma_rn(tk.x, gk.x, a.x); a.x = __fma_rn(-tk.y, gk.y, a.x);
+      a.y = __fma_rn(tk.x, gk.y, a.y); a.y = __fma_rn(tk.y, gk.x, a.y);
+    }
+    hs[t] = a;
+    if (rank == 0) hout[t] = a;
+  }
+  __syncthreads();
+  // pass B: w -= h_j V_j (shared), then h_k V_k for k = j-1 .. 0 (L2-recent first)
+  {
+    const cd hj = hs[j];
+    for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(hj, vj[q]));
+  }
+  for (int k = j - 1; k >= 0; --k) {
+    const cd* vk = V[k] + p0;
+    const cd hk = hs[k];
+    cd r[kLsSlot];
+#pragma unroll
+    for (int m = 0; m < kLsSlot; ++m) {
+      const int q = t + m * kRT;
+      r[m] = q < cnt ? __ldcg(vk + q) : mkc(0.0, 0.0);
+    }
+#pragma unroll
+    for (int m = 0; m < kLsSlot; ++m) {
+      const int q = t + m * kRT;
+      if (q < cnt) ws[q] = c_sub(ws[q], c_mul_np(hk, r[m]));
+    }
+  }
+  cd a = mkc(0.0, 0.0);
+  for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+  int buf = 1;  // gpart region 1 (region 0 holds the coefficient partials)
+  const cd nn = grid_reduce_small(a, s.red, buf, gpart, gr);
+  if (rank == 0 && t == 0) hout[j + 1] = nn;
+  const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
+  const double inv = 1.0 / hn;
+  for (int q = t; q < cnt; q += kRT) {
+    const cd v = ws[q];
+    w[p0 + q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+  }
+}
+
+static size_t mgs_ls_smem(long long chunk) { return kLsHead + 2 * (size_t)((chunk + 7) / 8) * 8 * sizeof(cd); }
+
+long long mgs_ls_tg_elems() { return (long long)(kLsMaxJ + 1) * (kLsMaxJ + 2) / 2; }
+
+static int g_mgs_ls = -1;  // -1: from HDB_MGS_LS (default on)
+void set_mgs_ls(int on) { g_mgs_ls = on ? 1 : 0; }
+static bool mgs_ls_enabled() {
+  if (g_mgs_ls < 0) {
+    const char* e = getenv("HDB_MGS_LS");
+    g_mgs_ls = e ? (atoi(e) != 0) : 1;
+  }
+  return g_mgs_ls != 0;
+}
+
 static size_t mgs_t_smem(long long chunk) {
   const size_t head = ((sizeof(MgsTSmem) + 127) / 128) * 128;
   return head + 2 * (size_t)((chunk + 7) / 8) * 8 * sizeof(cd);
@@ -1246,9 +1434,25 @@ bool mgs_grid_fits(long long n) {
   return mgs_grid_plan(n, ks) != 0;
 }
 
+bool mgs_ls_fits(long long n, int j) {
+  init_limits();
+  const long long chunk = (n + g_grid - 1) / g_grid;
+  return mgs_ls_enabled() && j <= kLsMaxJ && chunk <= (long long)kLsSlot * kRT && mgs_ls_smem(chunk) <= g_smem_optin;
+}
+
 // returns 0 when launched, 1 when the level does not fit (caller: launch chain)
 int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
-                    const int* skip) {
+                    const int* skip, cd* tg) {
+  if (tg && mgs_ls_fits(n, j)) {
+    const size_t sm = mgs_ls_smem((n + g_grid - 1) / g_grid);
+    static size_t configured_ls = 0;
+    if (sm > configured_ls) {
+      if (cudaFuncSetAttribute(k_mgs_ls, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 1;
+      configured_ls = sm;
+    }
+    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip};
+    return cudaLaunchCooperativeKernel((void*)k_mgs_ls, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
+  }
   long long ks = 0;
   const int plan = mgs_grid_plan(n, ks);
   if (plan == 0) return 1;

@@ -588,6 +588,193 @@ static void launch_rgh(const OpCoef& c, const Geom& g, const cd* u, const cd* b,
   k_rgh<R, MODE><<<grd, blk, HTile<R>::bytes, st>>>(u, b, k, out, g, c);
 }
 
+// ---------------------------------------------------------------------------
+// Separable Galerkin stencil (K2).  Every level kernel factorises exactly
+// (SURVEY §0): lap = lsc (a (x) m + m (x) a), mass = msc (m (x) m), so
+//   A u = lsc [ sum_r a_r (M u)_r + sum_r m_r (A u)_r ] + msc sum_r m_r (M (k u))_r
+// with row-wise 1D passes  (M u)(y, x) = sum_c m_c u(y, x + c)  etc. over the
+// SAME ghost-closed u and k^2 samples as the tap form (upad / kpad), then the
+// Dirichlet identity rows.  ~100 FP64 operations per output instead of 392-539:
+// the kernel becomes memory-bound.  Not bit-identical to the reference's
+// row-major 49-tap sum (a different association of the same products):
+// within a few ulp of it (tests hold it to 4e-15 of the field's max).
+// CTA: 32 x 32 outputs, 256 threads.  Horizontal pass: a thread forms the three
+// row sums of 4 adjacent columns from one register window of 4 + 2R samples
+// (tile columns skewed by one element every 4 so a quarter-warp's 16-byte window
+// loads hit distinct banks); vertical pass: a thread forms 4 vertically adjacent
+// outputs of one column from a window of 4 + 2R row sums.
+constexpr int GS_T = 32;          // outputs per tile side
+__device__ __forceinline__ int gskew(int col) { return col + (col >> 2); }
+template <int R>
+struct GSTile {
+  static constexpr int TR = GS_T + 2 * R, TC = GS_T + 2 * R, PC = TC + TC / 4 + 1;
+  static constexpr size_t u_bytes = (size_t)TR * PC * sizeof(cd);
+  static constexpr size_t k_bytes = (size_t)TR * PC * sizeof(double);
+  static constexpr size_t h_bytes = (size_t)3 * TR * GS_T * sizeof(cd);
+  static constexpr size_t bytes = u_bytes + k_bytes + h_bytes;
+};
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(256, 2) k_rgs(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                const double* __restrict__ k, cd* __restrict__ out, Geom g,
+                                                OpCoef c) {
+  if (c.skip && *c.skip) return;
+  using T = GSTile<R>;
+  constexpr int N = 2 * R + 1, TR = T::TR, TC = T::TC, PC = T::PC, W = 4 + 2 * R;
+  extern __shared__ __align__(16) unsigned char gsm[];
+  cd* su = reinterpret_cast<cd*>(gsm);
+  double* sk = reinterpret_cast<double*>(gsm + T::u_bytes);
+  cd* hm = reinterpret_cast<cd*>(gsm + T::u_bytes + T::k_bytes);  // (M u) rows
+  cd* ha = hm + TR * GS_T;                                        // (A u) rows
+  cd* hk = ha + TR * GS_T;                                        // (M (k u)) rows
+  const int i0 = blockIdx.x * GS_T, j0 = blockIdx.y * GS_T;
+  const bool fast = c.uniform && i0 >= R && i0 + GS_T + R <= g.nx && g.row0 + j0 >= R &&
+                    g.row0 + j0 + GS_T + R <= g.nyg;
+  const int tid = threadIdx.x;
+  for (int t = tid; t < TR * TC; t += 256) {
+    const int ty = t / TC, tx = t - ty * TC;
+    const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+    const int si = ty * PC + gskew(tx);
+    if (fast) {
+      su[si] = (gi < g.nx && gj < g.nyg) ? U(u, g, gj, gi) : mkc(0.0, 0.0);
+    } else {
+      su[si] = upad(u, k, g, c, gj, gi);
+      sk[si] = kpad(k, g, c, gj, gi);
+    }
+  }
+  __syncthreads();
+  // horizontal pass: item = (tile row r, column group xg of 4)
+  for (int it = tid; it < TR * (GS_T / 4); it += 256) {
+    const int r = it >> 3, x0 = (it & 7) * 4;
+    const cd* row = su + r * PC;
+    cd uv[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) uv[q] = row[gskew(x0 + q)];
+    cd am[4], aa[4];
+#pragma unroll
+    for (int o = 0; o < 4; ++o) { am[o] = mkc(0.0, 0.0); aa[o] = mkc(0.0, 0.0); }
+#pragma unroll
+    for (int bb = 0; bb < N; ++bb) {
+      const double mb = c.sm[bb], ab = c.sa[bb];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const cd v = uv[o + bb];
+        am[o].x = fma(mb, v.x, am[o].x); am[o].y = fma(mb, v.y, am[o].y);
+        aa[o].x = fma(ab, v.x, aa[o].x); aa[o].y = fma(ab, v.y, aa[o].y);
+      }
+    }
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      hm[r * GS_T + x0 + o] = am[o];
+      ha[r * GS_T + x0 + o] = aa[o];
+    }
+    if (!fast) {
+      const double* krow = sk + r * PC;
+      cd ak[4];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) ak[o] = mkc(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const double kq = krow[gskew(x0 + q)];
+        const cd ku = mkc(kq * uv[q].x, kq * uv[q].y);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+          const int bb = q - o;
+          if (bb >= 0 && bb < N) {
+            ak[o].x = fma(c.sm[bb], ku.x, ak[o].x);
+            ak[o].y = fma(c.sm[bb], ku.y, ak[o].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o) hk[r * GS_T + x0 + o] = ak[o];
+    }
+  }
+  __syncthreads();
+  // vertical pass: thread = (column x, row group y0 of 4)
+  const int x = tid & 31, y0 = (tid >> 5) * 4;
+  cd lm[4], lk[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) { lm[o] = mkc(0.0, 0.0); lk[o] = mkc(0.0, 0.0); }
+  {
+    cd w[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = hm[(y0 + q) * GS_T + x];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const double aa = c.sa[a], ma = c.sm[a];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        lm[o].x = fma(aa, w[o + a].x, lm[o].x); lm[o].y = fma(aa, w[o + a].y, lm[o].y);
+        lk[o].x = fma(ma, w[o + a].x, lk[o].x); lk[o].y = fma(ma, w[o + a].y, lk[o].y);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = ha[(y0 + q) * GS_T + x];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const double ma = c.sm[a];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) { lm[o].x = fma(ma, w[o + a].x, lm[o].x); lm[o].y = fma(ma, w[o + a].y, lm[o].y); }
+    }
+    if (!fast) {  // lk = sum_a m_a (M (k u))_a; the uniform form scales sum_a m_a (M u)_a by k
+#pragma unroll
+      for (int q = 0; q < W; ++q) w[q] = hk[(y0 + q) * GS_T + x];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) lk[o] = mkc(0.0, 0.0);
+#pragma unroll
+      for (int a = 0; a < N; ++a) {
+        const double ma = c.sm[a];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) { lk[o].x = fma(ma, w[o + a].x, lk[o].x); lk[o].y = fma(ma, w[o + a].y, lk[o].y); }
+      }
+    } else {
+#pragma unroll
+      for (int o = 0; o < 4; ++o) lk[o] = mkc(c.ku * lk[o].x, c.ku * lk[o].y);
+    }
+  }
+  const int i = i0 + x;
+  if (i >= g.nx) return;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int j = j0 + y0 + o;
+    if (j >= g.ny) return;
+    const int gj = j + g.row0;
+    const long long p = (long long)j * g.nx + i;
+    cd v;
+    if (pinned(g, c, gj, i)) {
+      v = su[(y0 + o + R) * PC + gskew(x + R)];
+    } else {
+      // lsc * lap sums + msc * mass sum (complex msc)
+      v.x = fma(c.lsc, lm[o].x, fma(c.msc.x, lk[o].x, -c.msc.y * lk[o].y));
+      v.y = fma(c.lsc, lm[o].y, fma(c.msc.x, lk[o].y, c.msc.y * lk[o].x));
+    }
+    out[p] = MODE == 0 ? v : c_sub(b[p], v);
+  }
+}
+
+template <int R, int MODE>
+static void launch_rgs(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
+                       cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_rgs<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GSTile<R>::bytes);
+    configured = true;
+  }
+  const dim3 grd((g.nx + GS_T - 1) / GS_T, (g.ny + GS_T - 1) / GS_T);
+  k_rgs<R, MODE><<<grd, 256, GSTile<R>::bytes, st>>>(u, b, k, out, g, c);
+}
+
+static int g_rg_exact = -1;  // -1: from HDB_RG_EXACT (default 0 = separable form where available)
+void set_rg_exact(int on) { g_rg_exact = on ? 1 : 0; }
+static bool rg_exact() {
+  if (g_rg_exact < 0) {
+    const char* e = getenv("HDB_RG_EXACT");
+    g_rg_exact = e ? (atoi(e) != 0) : 0;
+  }
+  return g_rg_exact != 0;
+}
+
 // ------------------------------------------------------------------------
 static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny + 7) / 8); }
 static inline dim3 grid_r1s(const Geom& g) { return dim3((g.nx + SX - 1) / SX, (g.ny + SY * RB - 1) / (SY * RB)); }
@@ -634,6 +821,16 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
     const dim3 blk(32, 8), grd = grid_r1(g);
     if (mode == 0) k_r1<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
     else k_r1<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
+    return;
+  }
+  if (c.sep && !rg_exact()) {
+    if (c.radius == 2) {
+      if (mode == 0) launch_rgs<2, 0>(c, g, u, b, k, out, st);
+      else launch_rgs<2, 1>(c, g, u, b, k, out, st);
+    } else {
+      if (mode == 0) launch_rgs<3, 0>(c, g, u, b, k, out, st);
+      else launch_rgs<3, 1>(c, g, u, b, k, out, st);
+    }
     return;
   }
   static const bool blocked = [] {

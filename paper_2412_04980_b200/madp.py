@@ -146,6 +146,7 @@ class ConvergenceReport:
     model_flops: float
     model_bytes: float
     device_ms: float = 0.0
+    alg_bytes: float = 0.0   # algorithmic HBM bytes of the solve's kernels (device solver telemetry)
 
     def cycle_max(self, level: int) -> int:
         v = self.cycle_iters.get(level, [])
@@ -343,13 +344,15 @@ class MadpSolver:
         flops = sum(matvecs[l] * _model_flops_per_point(self.A[l].radius) * self.A[l].npoints for l in matvecs)
         nbytes = sum(matvecs[l] * _model_bytes_per_point(self.A[l].radius) * self.A[l].npoints for l in matvecs)
         n_it = its.value
+        ab = C.c_double()
+        check(L.hdb_solver_bytes(h, C.byref(ab)))
         return ConvergenceReport(
             outer_iterations=n_it, converged=bool(conv.value), final_relres=fin.value,
             residual_history=list(hist[: hl.value]),
             wall_ms=dms.value if wall_ms is None else wall_ms,
             iteration_wall_ms=[0.0] + list(iw[:n_it]), preset_name=self.config.preset_name,
             levels=ml, workers=self.workers, cycle_iters=cyc, cslp_iters=csl, matvecs=matvecs,
-            model_flops=float(flops), model_bytes=float(nbytes), device_ms=dms.value)
+            model_flops=float(flops), model_bytes=float(nbytes), device_ms=dms.value, alg_bytes=ab.value)
 
 
 def solve(problem, config: SolverConfig, workers: int = 1) -> tuple:

@@ -134,7 +134,42 @@ class LevelOperator:
                 check(L.hdb_op_create_slab(C.byref(h), self.nx, self.ny, self.radius, self.h, bc, f(lap), f(mre),
                                            f(mim), f(self.ksq), sl.row0, sl.ny, sl.halo, P, r0s, nys))
             self._handle = h
+            sep = self.separable_factors()
+            if sep is not None:
+                sa, sm, lsc, msc = sep
+                check(L.hdb_op_set_separable(h, f(sa), f(sm), lsc, msc.real, msc.imag))
         return self._handle
+
+    def separable_factors(self):
+        """(sa, sm, lsc, msc) with lap_coef = lsc (sa (x) sm + sm (x) sa) and
+        mass_coef = msc (sm (x) sm), derived EXACTLY from the integer numerator
+        tables (the Galerkin chain is a sum of tensor products),
+        then checked in floating point to 2 ulp of the largest coefficient; None
+        for radius 1 or a kernel pair without that structure (the device then
+        uses the tap form)."""
+        from fractions import Fraction
+        if self.radius < 2:
+            return None
+        R, n = self.radius, 2 * self.radius + 1
+        Mt, Lt = self.mass.numerators, self.laplace.numerators
+        mu = [Mt[R][b] for b in range(n)]
+        if mu[R] == 0 or any(Mt[a][b] * mu[R] != mu[a] * mu[b] for a in range(n) for b in range(n)):
+            return None
+        aR = Fraction(Lt[R][R], 2 * mu[R])
+        al = [(Fraction(Lt[a][R]) - mu[a] * aR) / mu[R] for a in range(n)]
+        if any(Lt[a][b] != al[a] * mu[b] + mu[a] * al[b] for a in range(n) for b in range(n)):
+            return None
+        sa = np.array([float(v) for v in al])
+        sm = np.array([float(v) for v in mu])
+        lsc = 1.0 / float(self.laplace.denominator) / self.h ** 2
+        msc = complex(self.mass_coef[R, R]) / (sm[R] * sm[R])
+        lap_r = lsc * (np.outer(sa, sm) + np.outer(sm, sa))
+        mass_r = msc * np.outer(sm, sm)
+        tol = 2.0 * np.finfo(float).eps
+        if (np.abs(lap_r - self.lap_coef).max() > tol * np.abs(self.lap_coef).max()
+                or np.abs(mass_r - self.mass_coef).max() > tol * np.abs(self.mass_coef).max()):
+            return None
+        return sa, sm, lsc, msc
 
     def close(self):
         if self._handle is not None:

@@ -24,6 +24,15 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
+@pytest.fixture
+def exact_taps():
+    """Radius-2/3 operators in the reference's row-major tap order (bit-exact path)."""
+    from paper_2412_04980_b200 import _lib
+    _lib.check(_lib.lib().hdb_option(b"rg_exact", 1))
+    yield
+    _lib.check(_lib.lib().hdb_option(b"rg_exact", 0))
+
+
 def _rng(seed=7):
     return np.random.default_rng(seed)
 
@@ -36,7 +45,7 @@ def _rand(rng, shape):
 @pytest.mark.parametrize("bc", ["sommerfeld", "dirichlet"])
 @pytest.mark.parametrize("level", [1, 2, 3, 4])
 @pytest.mark.parametrize("kind", ["A", "M"])
-def test_operator_bitexact_vs_reference(bc, level, kind):
+def test_operator_bitexact_vs_reference(bc, level, kind, exact_taps):
     g = golden("operators.npz")
     hier = hdb.mp1_problem(k=25.0, n=33, ml=4, boundary=bc).hierarchy
     op = hdb.helmholtz_operator(hier, level) if kind == "A" else hdb.cslp_operator(hier, level, beta2=0.35)
@@ -44,7 +53,7 @@ def test_operator_bitexact_vs_reference(bc, level, kind):
     np.testing.assert_array_equal(got, g[f"mp1_{bc}_L{level}_{kind}_v"])
 
 
-def test_operator_heterogeneous_and_mixed_bc_bitexact():
+def test_operator_heterogeneous_and_mixed_bc_bitexact(exact_taps):
     g = golden("operators.npz")
     hier = hdb.wedge_problem(f=4.0, nx=25, ml=3).hierarchy
     for l in (1, 2, 3):
@@ -62,7 +71,7 @@ def test_operator_heterogeneous_and_mixed_bc_bitexact():
 
 @pytest.mark.parametrize("shape", [(129, 129), (65, 257), (257, 33), (300, 270), (289, 513)])
 @pytest.mark.parametrize("level", [1, 2, 3])
-def test_operator_bitexact_vs_oracle_larger(shape, level):
+def test_operator_bitexact_vs_oracle_larger(shape, level, exact_taps):
     rng = _rng(level)
     ny, nx = shape
     ksq = 400.0 + 300.0 * rng.random((ny, nx))
@@ -81,7 +90,7 @@ def test_operator_bitexact_vs_oracle_larger(shape, level):
 
 @pytest.mark.parametrize("level", [2, 3])
 @pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
-def test_operator_uniform_k_large_bitexact(level, bnd):
+def test_operator_uniform_k_large_bitexact(level, bnd, exact_taps):
     """Constant-k^2 level on a grid large enough for the register-blocked tile
     kernel (interior tiles take the precomputed-coefficient fast path)."""
     rng = _rng(40 + level)
@@ -97,6 +106,37 @@ def test_operator_uniform_k_large_bitexact(level, bnd):
     np.testing.assert_array_equal(op.apply(u), ref.apply(u))
     b = _rand(rng, (ny, nx))
     np.testing.assert_array_equal(op.residual(b, u), b - ref.apply(u))
+
+
+@pytest.mark.parametrize("shape", [(129, 129), (300, 270), (289, 513), (1025, 1025), (65, 257)])
+@pytest.mark.parametrize("level", [2, 3, 5])
+@pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
+@pytest.mark.parametrize("uniform", [False, True])
+def test_separable_galerkin_vs_exact_taps(shape, level, bnd, uniform):
+    """K2: the separable 1D-pass form of the radius-2/3 level operators (the
+    default) against the reference's exact row-major tap sum (oracle, bit-exact
+    with contract_general) on heterogeneous and constant k^2, both closures:
+    a different association of the same products, held to 4 ulp of the field's
+    max (measured ~5e-16).  Dirichlet identity rows are exact."""
+    rng = _rng(7 * level + shape[0])
+    ny, nx = shape
+    ksq = np.full((ny, nx), 611.5) if uniform else 400.0 + 300.0 * rng.random((ny, nx))
+    lv = hdb.level_kernels(level)
+    op = hdb.LevelOperator(level, nx, ny, 1.0 / 128, ksq, bnd, lv[0], lv[1], shift=complex(1.0, 0.5),
+                           level_scale=4.0 ** (level - 1))
+    assert op.separable_factors() is not None
+    lt, ld, mt, md, _ = oracle.level_kernels(level)
+    ref = oracle.CpuLevelOp(nx, ny, 1.0 / 128, ksq, bnd, lt, ld, mt, md, shift=complex(1.0, 0.5),
+                            level_scale=4.0 ** (level - 1))
+    u, b = _rand(rng, shape), _rand(rng, shape)
+    au = ref.apply(u)
+    got = op.apply(u)
+    assert np.abs(got - au).max() <= 4 * np.finfo(float).eps * np.abs(au).max()
+    res = op.residual(b, u)
+    assert np.abs(res - (b - au)).max() <= 4 * np.finfo(float).eps * np.abs(b - au).max()
+    if bnd[0] == "dirichlet":
+        np.testing.assert_array_equal(got[:, 0], u[:, 0])
+        np.testing.assert_array_equal(got[0, :], u[0, :])
 
 
 @pytest.mark.parametrize("shape", [(1025, 1025), (600, 2050), (2049, 517), (777, 1111)])
@@ -442,6 +482,42 @@ def test_device_resident_and_launch_paths_agree():
     for i1, h1, c1 in outs[1:]:
         assert i0 == i1 and c0 == c1
         assert np.abs(np.array(h0) - np.array(h1)).max() <= 1e-12
+
+
+def test_lowsync_mgs_step_matches_mgs_order():
+    """The one-launch MGS step of large levels in its low-synchronisation form
+    (h = (I + L)^{-1} V^H w, two grid reductions per Arnoldi step) against the
+    reference's coefficient-by-coefficient order (hdb_option("mgs_ls", 0)) and
+    the oracle's fgmres, on a 1025^2 CSLP level (7099 points per CTA: the form
+    applies) with GMRES(0.1, 40) and a tighter GMRES(1e-6, 60)."""
+    import ctypes as C
+    import torch
+    from paper_2412_04980_b200 import _lib
+    L = _lib.lib()
+    prob = hdb.mp1_problem(k=100.0, n=1025, ml=3)
+    op = hdb.cslp_operator(prob.hierarchy, 1, 0.5)
+    rng = _rng(5)
+    bh = _rand(rng, op.shape)
+    b = torch.from_numpy(bh).cuda()
+    res = {}
+    for ls in (1, 0):
+        _lib.check(L.hdb_option(b"mgs_ls", ls))
+        for tol, cap in ((0.1, 40), (1e-6, 60)):
+            x = torch.empty_like(b)
+            its, rel = C.c_int(), C.c_double()
+            _lib.check(L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), tol, cap, -1, C.byref(its), C.byref(rel)))
+            res[(ls, tol)] = (its.value, rel.value, x.cpu().numpy())
+    _lib.check(L.hdb_option(b"mgs_ls", 1))
+    for tol in (0.1, 1e-6):
+        (i1, r1, x1), (i0, r0, x0) = res[(1, tol)], res[(0, tol)]
+        assert i1 == i0
+        assert abs(r1 - r0) <= 1e-9 * max(r0, 1e-300) + 1e-14
+        assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0)
+    oop = oracle.cslp_op(oracle.mp1_problem(100.0, 1025, 3)[0], 1, 0.5)
+    xo, repo = oracle.fgmres(oop.apply, None, bh, oracle.Stop(0.1, 40), dot=oracle.reduce_dot)
+    i1, r1, x1 = res[(1, 0.1)]
+    assert i1 == repo.iterations
+    assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
 
 
 ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))

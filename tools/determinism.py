@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--repeat", type=int, default=3)
     a = ap.parse_args()
     import torch
-    prob = bench.CONFIGS[a.case][1](hdb)
+    prob = bench.CONFIGS[a.case][1](hdb, 1)
     hier = prob.hierarchy
     cfg = hdb.preset("MADP", hier)
     s = hdb.MadpSolver(hier, cfg)

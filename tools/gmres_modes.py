@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--cap", type=int, default=0)
     a = ap.parse_args()
     import torch
-    prob = bench.CONFIGS[a.case][1](hdb)
+    prob = bench.CONFIGS[a.case][1](hdb, 1)
     hier = prob.hierarchy
     cfg = hdb.preset("MADP", hier)
     L = _lib.lib()

@@ -19,7 +19,7 @@ def main():
     ap.add_argument("case", nargs="?", default="c2")
     ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
-    prob = bench.CONFIGS[a.case][1](hdb)
+    prob = bench.CONFIGS[a.case][1](hdb, 1)
     res = bench.kernel_roofline(hdb, prob.hierarchy, reps=a.reps)
     peak, _ = bench._peaks()
     print(json.dumps({k: {"gbs": round(v["gbs"], 1), "ms": round(v["ms"], 4), "frac": round(v["gbs"] / peak, 3)}

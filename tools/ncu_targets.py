@@ -24,7 +24,7 @@ from paper_2412_04980_b200 import _lib  # noqa: E402
 def main():
     import torch
     case = sys.argv[1] if len(sys.argv) > 1 else "c2"
-    hier = bench.CONFIGS[case][1](hdb).hierarchy
+    hier = bench.CONFIGS[case][1](hdb, 1).hierarchy
     L = _lib.lib()
     rng = np.random.default_rng(7)
 
