@@ -1228,34 +1228,97 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid_t(cd* w, const cd* const* V, i
 // j + 2, at the price of re-reading the basis (partly from L2).  Same
 // coefficients as MGS in exact arithmetic (krylov.py:121-124); the rounding
 // differs like the reference's own worker-count-dependent zdotc rounding does.
-// w and V_j slices both live in shared memory: levels with <= kLsMaxChunk
+// The w slice lives in registers (14 points per thread), the V_j slice in
+// shared memory, and the other basis vectors stream HBM -> shared memory
+// through a TMA ring (cp.async.bulk, mbarrier full/empty pairs) that runs ahead
+// across both passes -- pass B's first chunks are already in flight while the
+// coefficient reduction and the small triangular work run.  Levels with <= 7168
 // points per CTA (the 1025^2 level of config 2: 7099).
-constexpr int kLsSlot = 14;                // slice elements per thread (kRT * 14 >= chunk)
+constexpr int kLsSlot = 14;                // w points per thread (kRT * 14 = 7168)
 constexpr int kLsMaxJ = 63;                // 4 j + 2 scalars fit the staging area
 constexpr int kLsStage = 16;               // reduced elements per warp-partial staging round
+constexpr int kLsChunk = 2 * kRT;          // ring chunk: 1024 points (16 KB) = 2 per thread
+constexpr int kLsChunks = kLsSlot / 2;     // chunks per slice (7)
+constexpr int kLsRing = 6;                 // ring stages
 struct LsSmem {
   MgsSmem red;
   cd stage[kRT / 32][kLsStage];            // warp partials; reused for g, l, t-row and h
+  uint64_t full[kLsRing], empty[kLsRing];
 };
 constexpr size_t kLsHead = ((sizeof(LsSmem) + 127) / 128) * 128;
+
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 
 __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, int j, long long n, cd* gpart,
                                                    cd* hout, cd* Tg, const int* skip) {
   if (skip && *skip) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   LsSmem& s = *reinterpret_cast<LsSmem*>(smem_raw);
   cg::grid_group gr = cg::this_grid();
   const int P = gridDim.x, rank = blockIdx.x, t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
   const int cnt = (int)(p1 - p0);
-  const int cap = (int)((n + P - 1) / P);
-  cd* ws = reinterpret_cast<cd*>(smem_raw + kLsHead);
-  cd* vj = ws + ((cap + 7) / 8) * 8;
-  load_slice_smem(ws, w + p0, cnt);
+  cd* ring = reinterpret_cast<cd*>(smem_raw + kLsHead);                 // kLsRing x kLsChunk
+  cd* vj = ring + (size_t)kLsRing * kLsChunk;                           // V_j slice
+  // chunk sequence: pass A streams V_0..V_{j-1}, pass B V_{j-1}..V_0, kLsChunks chunks each
+  const int nchunks = 2 * j * kLsChunks;
+  auto chunk_src = [&](int q, int& bytes) -> const cd* {
+    const int v = q / kLsChunks, c = q - v * kLsChunks;
+    const int k = v < j ? v : 2 * j - 1 - v;
+    const int e0 = c * kLsChunk;
+    const int ne = cnt - e0 < kLsChunk ? cnt - e0 : kLsChunk;
+    bytes = ne > 0 ? ne * (int)sizeof(cd) : 0;
+    return V[k] + p0 + e0;
+  };
+  auto issue = [&](int q) {  // thread 0
+    const int st = q % kLsRing;
+    int bytes = 0;
+    const cd* src = chunk_src(q, bytes);
+    if (bytes > 0) {
+      mbar_arm(&s.full[st], (uint32_t)bytes);
+      bulk_g2s(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st]);
+    } else {
+      mbar_arrive1(&s.full[st]);  // empty tail chunk: complete the phase without data
+    }
+  };
+  if (t == 0) {
+    for (int st = 0; st < kLsRing; ++st) {
+      mbar_init(&s.full[st], 1);
+      mbar_init(&s.empty[st], kRT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int q = 0; q < kLsRing && q < nchunks; ++q) issue(q);
+  cd wr[kLsSlot];
+#pragma unroll
+  for (int m = 0; m < kLsSlot; ++m) {
+    const int q = t + m * kRT;
+    wr[m] = q < cnt ? w[p0 + q] : mkc(0.0, 0.0);
+  }
   load_slice_smem(vj, V[j] + p0, cnt);
   __syncthreads();
+  int qn = 0;  // next chunk to consume
+  // consume one chunk: f(m, v) for this thread's two points (m = slot index)
+  auto consume = [&](auto&& f) {
+    const int st = qn % kLsRing;
+    mbar_wait(&s.full[st], (uint32_t)((qn / kLsRing) & 1));
+    const cd* rb = ring + (size_t)st * kLsChunk;
+    f(rb);
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&s.empty[st]);
+    if (t == 0 && qn + kLsRing < nchunks) {  // refill this stage once every warp has released it
+      mbar_wait(&s.empty[st], (uint32_t)((qn / kLsRing) & 1));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(qn + kLsRing);
+    }
+    ++qn;
+  };
   const int ne = 2 * j + 1;  // g_0..g_j, then l_0..l_{j-1}
-  cd pw[4];                   // this warp's partial of element e sits in lane e % 32, slot e / 32
+  cd pw[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) pw[k] = mkc(0.0, 0.0);
   auto stash = [&](int e, cd v) {
@@ -1266,30 +1329,33 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     for (int k = 0; k < 4; ++k)
       if (e == 32 * k + lane) pw[k] = v;
   };
-  // pass A: g_k = <V_k, w>, l_k = <V_j, V_k> for k < j, one read of each V_k
+  // pass A: g_k = <V_k, w>, l_k = <V_j, V_k> for k < j
   for (int k = 0; k < j; ++k) {
-    const cd* vk = V[k] + p0;
-    cd r[kLsSlot];
-#pragma unroll
-    for (int m = 0; m < kLsSlot; ++m) {
-      const int q = t + m * kRT;
-      r[m] = q < cnt ? __ldcg(vk + q) : mkc(0.0, 0.0);
-    }
     cd ag = mkc(0.0, 0.0), al = mkc(0.0, 0.0);
 #pragma unroll
-    for (int m = 0; m < kLsSlot; ++m) {
-      const int q = t + m * kRT;
-      if (q < cnt) {
-        ag = c_conjmul_acc(ag, r[m], ws[q]);
-        al = c_conjmul_acc(al, vj[q], r[m]);
-      }
+    for (int c = 0; c < kLsChunks; ++c) {
+      consume([&](const cd* rb) {
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int q = c * kLsChunk + h2 * kRT + t;
+          if (q < cnt) {
+            const cd v = rb[h2 * kRT + t];
+            ag = c_conjmul_acc(ag, v, wr[2 * c + h2]);
+            al = c_conjmul_acc(al, vj[q], v);
+          }
+        }
+      });
     }
     stash(k, ag);
     stash(j + 1 + k, al);
   }
   {
     cd ag = mkc(0.0, 0.0);
-    for (int q = t; q < cnt; q += kRT) ag = c_conjmul_acc(ag, vj[q], ws[q]);
+#pragma unroll
+    for (int m = 0; m < kLsSlot; ++m) {
+      const int q = t + m * kRT;
+      if (q < cnt) ag = c_conjmul_acc(ag, vj[q], wr[m]);
+    }
     stash(j, ag);
   }
   // block partials (16 warps in order) -> gpart region 0, one grid barrier
@@ -1353,40 +1419,52 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     if (rank == 0) hout[t] = a;
   }
   __syncthreads();
-  // pass B: w -= h_j V_j (shared), then h_k V_k for k = j-1 .. 0 (L2-recent first)
+  // pass B: w -= h_j V_j (shared), then h_k V_k for k = j-1 .. 0 (ring)
   {
     const cd hj = hs[j];
-    for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(hj, vj[q]));
+#pragma unroll
+    for (int m = 0; m < kLsSlot; ++m) {
+      const int q = t + m * kRT;
+      if (q < cnt) wr[m] = c_sub(wr[m], c_mul_np(hj, vj[q]));
+    }
   }
   for (int k = j - 1; k >= 0; --k) {
-    const cd* vk = V[k] + p0;
     const cd hk = hs[k];
-    cd r[kLsSlot];
 #pragma unroll
-    for (int m = 0; m < kLsSlot; ++m) {
-      const int q = t + m * kRT;
-      r[m] = q < cnt ? __ldcg(vk + q) : mkc(0.0, 0.0);
-    }
+    for (int c = 0; c < kLsChunks; ++c) {
+      consume([&](const cd* rb) {
 #pragma unroll
-    for (int m = 0; m < kLsSlot; ++m) {
-      const int q = t + m * kRT;
-      if (q < cnt) ws[q] = c_sub(ws[q], c_mul_np(hk, r[m]));
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int q = c * kLsChunk + h2 * kRT + t;
+          if (q < cnt) wr[2 * c + h2] = c_sub(wr[2 * c + h2], c_mul_np(hk, rb[h2 * kRT + t]));
+        }
+      });
     }
   }
   cd a = mkc(0.0, 0.0);
-  for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, ws[q], ws[q]);
+#pragma unroll
+  for (int m = 0; m < kLsSlot; ++m) {
+    const int q = t + m * kRT;
+    if (q < cnt) a = c_conjmul_acc(a, wr[m], wr[m]);
+  }
   int buf = 1;  // gpart region 1 (region 0 holds the coefficient partials)
   const cd nn = grid_reduce_small(a, s.red, buf, gpart, gr);
   if (rank == 0 && t == 0) hout[j + 1] = nn;
   const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
   const double inv = 1.0 / hn;
-  for (int q = t; q < cnt; q += kRT) {
-    const cd v = ws[q];
-    w[p0 + q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+#pragma unroll
+  for (int m = 0; m < kLsSlot; ++m) {
+    const int q = t + m * kRT;
+    if (q < cnt) {
+      const cd v = wr[m];
+      w[p0 + q] = hn > 0.0 ? mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv)) : v;
+    }
   }
 }
 
-static size_t mgs_ls_smem(long long chunk) { return kLsHead + 2 * (size_t)((chunk + 7) / 8) * 8 * sizeof(cd); }
+static size_t mgs_ls_smem(long long chunk) {
+  return kLsHead + (size_t)kLsRing * kLsChunk * sizeof(cd) + (size_t)((chunk + 7) / 8) * 8 * sizeof(cd);
+}
 
 long long mgs_ls_tg_elems() { return (long long)(kLsMaxJ + 1) * (kLsMaxJ + 2) / 2; }
 

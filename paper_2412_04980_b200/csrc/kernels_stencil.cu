@@ -631,13 +631,26 @@ __global__ void __launch_bounds__(256, 2) k_rgs(const cd* __restrict__ u, const 
   const bool fast = c.uniform && i0 >= R && i0 + GS_T + R <= g.nx && g.row0 + j0 >= R &&
                     g.row0 + j0 + GS_T + R <= g.nyg;
   const int tid = threadIdx.x;
-  for (int t = tid; t < TR * TC; t += 256) {
-    const int ty = t / TC, tx = t - ty * TC;
-    const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
-    const int si = ty * PC + gskew(tx);
-    if (fast) {
-      su[si] = (gi < g.nx && gj < g.nyg) ? U(u, g, gj, gi) : mkc(0.0, 0.0);
-    } else {
+  constexpr int NL = (TR * TC + 255) / 256;
+  if (fast) {  // interior tile: every sample in range, all NL loads in flight before the stores
+    cd v[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int t = tid + l * 256;
+      const int ty = t / TC, tx = t - ty * TC;
+      v[l] = t < TR * TC ? U(u, g, g.row0 + j0 + ty - R, i0 + tx - R) : mkc(0.0, 0.0);
+    }
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      const int t = tid + l * 256;
+      const int ty = t / TC, tx = t - ty * TC;
+      if (t < TR * TC) su[ty * PC + gskew(tx)] = v[l];
+    }
+  } else {
+    for (int t = tid; t < TR * TC; t += 256) {
+      const int ty = t / TC, tx = t - ty * TC;
+      const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+      const int si = ty * PC + gskew(tx);
       su[si] = upad(u, k, g, c, gj, gi);
       sk[si] = kpad(k, g, c, gj, gi);
     }

@@ -1,0 +1,7 @@
+# r02d: TMA-ring low-sync MGS + unrolled K2 tile loads: microbench, focused tests, bench
+mkdir -p gpurun_out
+python -c "from paper_2412_04980_b200 import _build; _build.build()" > gpurun_out/r02d_build.log 2>&1
+timeout -s KILL 300 python tools/galerkin_bench.py c2 > gpurun_out/r02d_galerkin.log 2>&1
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "separable or lowsync or exact or bitexact or config2_analogue or full_solve or device_resident" > gpurun_out/r02d_focus.log 2>&1; echo FOCUS_EXIT $? >> gpurun_out/r02d_focus.log
+timeout -s KILL 900 python bench.py --steps 3 --warmup 2 --no-cpu > gpurun_out/r02d_bench.json 2> gpurun_out/r02d_bench.err
+echo DONE

@@ -13,7 +13,8 @@ import json
 import subprocess
 import sys
 
-UNITS = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "byte": 1.0, "Kbyte": 1e3,
+UNITS = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0,
+         "s": 1.0, "byte": 1.0, "Kbyte": 1e3,
          "Mbyte": 1e6, "Gbyte": 1e9}
 
 
