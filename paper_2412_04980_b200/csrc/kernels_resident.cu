@@ -52,6 +52,7 @@ struct ResidentArgs {
   long long* prof;    // optional: per-phase cycles of CTA 0 thread 0 (telemetry), may be null
   int tiled;          // stencil windows staged in shared memory
   int tile_elems;     // window elements (max over CTAs)
+  int sep;            // radius 2/3: separable 1D passes (column walk) instead of the tap sum
 };
 
 // phase clock (CTA 0, thread 0) — only when A.prof != nullptr
@@ -183,6 +184,74 @@ __device__ __forceinline__ cd op_point_tile(const OpCoef& c, const Geom& g, cons
     }
   }
   return acc;
+}
+
+// Separable form of the radius-2/3 operator on this CTA's points (csrc/
+// kernels_stencil.cu k_rgc, same association of the products): each thread
+// walks one column of the window in segments of up to GSEG own rows.  Sweep 1
+// accumulates sum_a a_a (M u)_a (and the mass sum), sweep 2 continues with
+// sum_a m_a (A u)_a, so every output receives its terms in k_rgc's order.
+constexpr int GSEG = 4;
+template <int R>
+__device__ __forceinline__ void sep_cols(const OpCoef& c, const Geom& g, const Tile& T, const cd* ut,
+                                         const double* kt, bool uni, double ku, long long p0, long long p1, cd* ws) {
+  constexpr int N = 2 * R + 1;
+  const int nx = g.nx;
+  const int ylo = (int)(p0 / nx), yhi = (int)((p1 - 1) / nx);  // slab-local rows
+  for (int x = threadIdx.x; x < nx; x += kRT) {
+    const int ya = ylo + ((long long)ylo * nx + x < p0 ? 1 : 0);
+    const int yb = yhi - ((long long)yhi * nx + x >= p1 ? 1 : 0);
+    for (int s0 = ya; s0 <= yb; s0 += GSEG) {
+      const int len = min(GSEG, yb - s0 + 1);
+      cd lm[GSEG], lk[GSEG];
+#pragma unroll
+      for (int q = 0; q < GSEG; ++q) { lm[q] = mkc(0.0, 0.0); lk[q] = mkc(0.0, 0.0); }
+      const int tr0 = s0 + g.row0 - T.rlo;  // window row of H row s0 - R
+      for (int sweep = 0; sweep < 2; ++sweep) {
+        for (int rr = 0; rr < len + 2 * R; ++rr) {
+          const cd* urow = ut + (tr0 + rr) * T.cols + x;
+          cd hm = mkc(0.0, 0.0), hk = mkc(0.0, 0.0);
+#pragma unroll
+          for (int bb = 0; bb < N; ++bb) {
+            const cd v = urow[bb];
+            const double w = sweep == 0 ? c.sm[bb] : c.sa[bb];
+            hm.x = fma(w, v.x, hm.x); hm.y = fma(w, v.y, hm.y);
+            if (sweep == 0 && !uni) {
+              const double kq = kt[(tr0 + rr) * T.cols + x + bb];
+              hk.x = fma(c.sm[bb], kq * v.x, hk.x); hk.y = fma(c.sm[bb], kq * v.y, hk.y);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < GSEG; ++q) {
+            const int a = rr - q;
+            if (q < len && a >= 0 && a < N) {
+              const double wa = sweep == 0 ? c.sa[a] : c.sm[a];
+              lm[q].x = fma(wa, hm.x, lm[q].x); lm[q].y = fma(wa, hm.y, lm[q].y);
+              if (sweep == 0) {
+                const cd hq = uni ? hm : hk;
+                lk[q].x = fma(c.sm[a], hq.x, lk[q].x); lk[q].y = fma(c.sm[a], hq.y, lk[q].y);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < GSEG; ++q) {
+        if (q >= len) break;
+        const int y = s0 + q, gj = y + g.row0;
+        cd v;
+        if (pinned(g, c, gj, x)) {
+          v = ut[(tr0 + q + R) * T.cols + x + R];
+        } else {
+          cd m = lk[q];
+          if (uni) m = mkc(ku * m.x, ku * m.y);
+          v.x = fma(c.lsc, lm[q].x, fma(c.msc.x, m.x, -c.msc.y * m.y));
+          v.y = fma(c.lsc, lm[q].y, fma(c.msc.x, m.y, c.msc.y * m.x));
+        }
+        ws[(long long)y * nx + x - p0] = v;
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ cd warp_sum_c(cd v) {
@@ -489,6 +558,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
   if (A.tiled && cnt > 0) load_k_tile<R>(kt, T, A.ksq, A.g, A.c);
   const cd* ucoef = nullptr;
+  double kuni = 0.0;  // the window's k^2 when it is uniform
   if (A.tiled && R > 1) {
     if (threadIdx.x == 0) s.uniform = cnt > 0;
     __syncthreads();
@@ -504,6 +574,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
         s.coef[threadIdx.x] = mkc(__dadd_rn(A.c.lap[threadIdx.x], __dmul_rn(m.x, k00)), __dmul_rn(m.y, k00));
       }
       ucoef = s.coef;
+      kuni = k00;
     }
     __syncthreads();
   }
@@ -603,7 +674,9 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       s.decision = !finite ? 2 : ((hn < 1e-30 || rel <= A.tol) ? 1 : 0);
     }
     PHASE(10);
-    if (jv < A.cap) {  // the stencil of step jv (skipped past the cap)
+    if (jv < A.cap && R > 1 && A.sep && A.tiled) {
+      if (cnt > 0) sep_cols<R>(A.c, A.g, T, ut, kt, ucoef != nullptr, kuni, p0, p1, ws);
+    } else if (jv < A.cap) {  // the stencil of step jv (skipped past the cap)
       for (int q = t; q < cnt; q += kRT) {
         const long long p = p0 + q;
         const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
@@ -733,12 +806,21 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     if (cnt > 0) load_u_tile<R>(ut, T, A.x, A.ksq, A.g, A.c);
     __syncthreads();
   }
-  for (int q = t; q < cnt; q += kRT) {
-    const long long p = p0 + q;
-    const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
-    const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
-    const cd d = c_sub(A.b[p], ax);
-    f = c_conjmul_acc(f, d, d);
+  if (R > 1 && A.sep && A.tiled) {
+    if (cnt > 0) sep_cols<R>(A.c, A.g, T, ut, kt, ucoef != nullptr, kuni, p0, p1, ws);
+    __syncthreads();
+    for (int q = t; q < cnt; q += kRT) {
+      const cd d = c_sub(A.b[p0 + q], ws[q]);
+      f = c_conjmul_acc(f, d, d);
+    }
+  } else {
+    for (int q = t; q < cnt; q += kRT) {
+      const long long p = p0 + q;
+      const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
+      const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
+      const cd d = c_sub(A.b[p], ax);
+      f = c_conjmul_acc(f, d, d);
+    }
   }
   const double fin = sqrt(fmax(sy.reduce(f, s, buf, A.gpart).x, 0.0)) / bnorm;
   if (rank == 0 && t == 0) {
@@ -890,6 +972,7 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
   ResidentArgs a{};
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
   a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
+  a.sep = c.sep && !rg_exact_on();
   if (ortho == 1 && cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
   if (ortho == 2 && cap + 2 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
   const bool ok = ortho == 2 ? launch_any<2>(mode, a, c.radius, st)
@@ -1244,6 +1327,7 @@ struct LsSmem {
   MgsSmem red;
   cd stage[kRT / 32][kLsStage];            // warp partials; reused for g, l, t-row and h
   uint64_t full[kLsRing], empty[kLsRing];
+  const cd* vptr[kLsMaxJ + 1];             // basis pointers (the producer's chunk sources)
 };
 constexpr size_t kLsHead = ((sizeof(LsSmem) + 127) / 128) * 128;
 
@@ -1270,7 +1354,7 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     const int e0 = c * kLsChunk;
     const int ne = cnt - e0 < kLsChunk ? cnt - e0 : kLsChunk;
     bytes = ne > 0 ? ne * (int)sizeof(cd) : 0;
-    return V[k] + p0 + e0;
+    return s.vptr[k] + p0 + e0;
   };
   auto issue = [&](int q) {  // thread 0
     const int st = q % kLsRing;
@@ -1290,6 +1374,7 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (t <= j) s.vptr[t] = V[t];  // no global pointer load on the producer's refill path
   __syncthreads();
   if (t == 0)
     for (int q = 0; q < kLsRing && q < nchunks; ++q) issue(q);
@@ -1310,10 +1395,14 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     f(rb);
     __syncwarp();
     if (lane == 0) mbar_arrive1(&s.empty[st]);
-    if (t == 0 && qn + kLsRing < nchunks) {  // refill this stage once every warp has released it
-      mbar_wait(&s.empty[st], (uint32_t)((qn / kLsRing) & 1));
+    // refill the stage of the PREVIOUS chunk (every warp has long released it) with the
+    // chunk kLsRing ahead of it: the producer does not wait for this chunk's stragglers
+    const int qp = qn - 1;
+    if (t == 0 && qp >= 0 && qp + kLsRing < nchunks) {
+      const int sp = qp % kLsRing;
+      mbar_wait(&s.empty[sp], (uint32_t)((qp / kLsRing) & 1));
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(qn + kLsRing);
+      issue(qp + kLsRing);
     }
     ++qn;
   };

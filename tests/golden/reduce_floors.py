@@ -75,6 +75,15 @@ def main():
                        cycle_iters=b["cycle_iters"], cslp_iters=b["cslp_iters"], solution_stride=np.array(4),
                        solution_sub=b["solution"][::4, ::4])
             rec.update(floors(b, pp, 4))
+            # k^2 checksums of the reference's own hierarchy (levels 1 and 3) for this raster
+            sys.path.insert(0, "/root/reference/pkg/src")
+            sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+            from helmdef import VelocityModel, build_hierarchy
+            from paper_2412_04980_b200.models import C4_DOMAIN, synthetic_layered_velocity
+            v = synthetic_layered_velocity(2412, dx=6.0)
+            vel = VelocityModel(kind="gridfile", values=v.values, dx=v.dx, dy=v.dy, x0=v.x0, y0=v.y0)
+            hier = build_hierarchy(C4_DOMAIN, h=6.0, ml=3, velocity=vel, f=40.0)
+            rec["ksq_checksum"] = np.array([hier.ksq[0].sum(), hier.ksq[2].sum()])
             np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **rec)
             print(name, int(b["outer_iterations"]), float(rec["floor_hist_abs"]), float(rec["floor_sol_rel"]))
 

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle
-from gold import golden
+from gold import golden, parity_bar
 
 pytestmark = pytest.mark.gpu
 
@@ -130,13 +130,21 @@ def test_separable_galerkin_vs_exact_taps(shape, level, bnd, uniform):
                             level_scale=4.0 ** (level - 1))
     u, b = _rand(rng, shape), _rand(rng, shape)
     au = ref.apply(u)
-    got = op.apply(u)
-    assert np.abs(got - au).max() <= 8 * np.finfo(float).eps * np.abs(au).max()
-    res = op.residual(b, u)
-    assert np.abs(res - (b - au)).max() <= 8 * np.finfo(float).eps * np.abs(b - au).max()
-    if bnd[0] == "dirichlet":
-        np.testing.assert_array_equal(got[:, 0], u[:, 0])
-        np.testing.assert_array_equal(got[0, :], u[0, :])
+    from paper_2412_04980_b200 import _lib
+    outs = []
+    for form in (1, 0):  # column-marching kernel (default), tile kernel
+        _lib.check(_lib.lib().hdb_option(b"rg_form", form))
+        got = op.apply(u)
+        assert np.abs(got - au).max() <= 8 * np.finfo(float).eps * np.abs(au).max()
+        res = op.residual(b, u)
+        assert np.abs(res - (b - au)).max() <= 8 * np.finfo(float).eps * np.abs(b - au).max()
+        if bnd[0] == "dirichlet":
+            np.testing.assert_array_equal(got[:, 0], u[:, 0])
+            np.testing.assert_array_equal(got[0, :], u[0, :])
+        outs.append(got)
+    _lib.check(_lib.lib().hdb_option(b"rg_form", 1))
+    if not uniform:  # same association of the products (the uniform shortcut depends on the tile shape)
+        np.testing.assert_array_equal(outs[0], outs[1])
 
 
 @pytest.mark.parametrize("shape", [(1025, 1025), (600, 2050), (2049, 517), (777, 1111)])
@@ -376,7 +384,7 @@ def test_full_solve_vs_reference(name):
 
 def test_config1_dirichlet_first_20_outer_iterations():
     """BASELINE configs[0] as written (chaotic, never converges in the reference):
-    the first 20 outer iterations are held to the count and to the early history."""
+    the first 20 outer iterations against the reference's 20-iteration record."""
     g = golden("solve_c1_cap20.npz")
     prob = _solve_case("c1_cap20")
     cfg = hdb.preset("MADP", prob.hierarchy, outer_stop=hdb.StopRule(1e-6, 20))
@@ -384,9 +392,35 @@ def test_config1_dirichlet_first_20_outer_iterations():
         _, rep = s.solve(prob.rhs)
     assert rep.outer_iterations == int(g["outer_iterations"]) == 20
     h, hr = np.array(rep.residual_history), g["residual_history"]
-    # the oracle itself moves by 2.3e-3 within these 20 iterations under a 1e-15 rhs
-    # perturbation (solve_c1_cap20.npz floor_hist_abs), so only the first steps are pinned
-    assert np.abs(h[:3] - hr[:3]).max() <= 1e-6
+    # the reference itself moves by 2.3e-3 within these 20 iterations under a 1e-15 rhs
+    # perturbation (floor_hist_abs); measured GPU delta over the 20: ~1e-5 (profiles/r02e_parity.json)
+    assert np.abs(h[:3] - hr[:3]).max() <= 1e-9
+    assert np.abs(h - hr).max() <= 10 * float(g["floor_hist_abs"])
+
+
+def test_config1_dirichlet_full_150_iteration_stall():
+    """BASELINE configs[0] as written, run like the reference to its cap: 150 outer
+    iterations, not converged (madp.py:112), against the reference's full record
+    (tests/golden/solve_c1_full.npz).  The reference is chaotic here (its own history
+    moves by 2.3e-3 and its solution by 1.0e-2 under a 1e-15 rhs perturbation), so
+    the history and solution are held to 10x that floor and the early history to
+    the BASELINE bar."""
+    g = golden("solve_c1_full.npz")
+    prob = _solve_case("c1_cap20")
+    with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
+        u, rep = s.solve(prob.rhs)
+    assert rep.outer_iterations == int(g["outer_iterations"]) == 150
+    assert not rep.converged and not bool(g["converged"])
+    h, hr = np.array(rep.residual_history), g["residual_history"]
+    assert len(h) == len(hr) == 151
+    assert np.abs(h[:3] - hr[:3]).max() <= 1e-9
+    hb, xb = parity_bar(g)
+    assert np.abs(h - hr).max() <= hb
+    st = int(g["solution_stride"])
+    xs = u.grid_view(prob.hierarchy)[::st, ::st]
+    assert np.linalg.norm(xs - g["solution_sub"]) <= xb * np.linalg.norm(g["solution_sub"])
+    # the stall level: the reference ends at 7.9e-5 (its perturbed twin at 3.7e-6)
+    assert 1e-6 < rep.final_relres < 1e-3
 
 
 def test_preconditioner_apply_vs_oracle():
@@ -520,6 +554,36 @@ def test_lowsync_mgs_step_matches_mgs_order():
     assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
 
 
+@pytest.mark.parametrize("level,modes", [(4, (1,)), (6, (0, 1)), (7, (0, 1))])
+def test_resident_separable_stencil_vs_exact_taps(level, modes):
+    """The device-resident GMRES with the separable column-walk stencil (default)
+    against the same solve with the reference's exact tap order, on config 2's
+    coarse CSLP levels (513^2 grid mode, 129^2 and 65^2 cluster and grid mode):
+    same iteration count, relres and iterate to rounding."""
+    import ctypes as C
+    import torch
+    from paper_2412_04980_b200 import _lib
+    L = _lib.lib()
+    hier = hdb.mp1_problem(k=200.0, n=4097, ml=7).hierarchy
+    op = hdb.cslp_operator(hier, level, 0.5)
+    rng = _rng(60 + level)
+    b = torch.from_numpy(_rand(rng, op.shape)).cuda()
+    cap = hdb.cslp_iteration_cap(op.npoints)
+    for mode in modes:
+        res = []
+        for exact in (0, 1):
+            _lib.check(L.hdb_option(b"rg_exact", exact))
+            x = torch.empty_like(b)
+            its, rel = C.c_int(), C.c_double()
+            _lib.check(L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), 0.1, cap, mode, C.byref(its), C.byref(rel)))
+            res.append((its.value, rel.value, x.cpu().numpy()))
+        _lib.check(L.hdb_option(b"rg_exact", 0))
+        (i0, r0, x0), (i1, r1, x1) = res
+        assert i0 == i1
+        assert abs(r0 - r1) <= 1e-10 * r1
+        assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x1)
+
+
 ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 
 
@@ -545,9 +609,9 @@ def test_config2_analogue_vs_reference():
 @pytest.mark.slow
 def test_config2_full_vs_reference():
     """BASELINE configs[1] at full size (4097^2, 7 levels) against the reference's own
-    27-minute run: outer count +-1; history and solution at the config-2-analogue
-    noise floor scale (the oracle moves by 1.3e-5 / 2.4e-7 there under a 1e-15 input
-    perturbation)."""
+    27-minute run: outer count +-1; history and solution within 10x the reference's
+    own config-2 noise floor (its 1e-15-perturbed twin run: 5.8e-6 / 3.9e-7;
+    measured GPU deltas 9.5e-7 / 5.5e-7, profiles/r02e_parity.json)."""
     g = golden("solve_c2.npz")
     prob = hdb.mp1_problem(k=200.0, n=4097, ml=7, boundary="sommerfeld")
     with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
@@ -556,11 +620,12 @@ def test_config2_full_vs_reference():
     assert rep.converged and rep.final_relres <= 1e-6
     h, hr = np.array(rep.residual_history), g["residual_history"]
     n = min(len(h), len(hr))
-    assert np.abs(h[:n] - hr[:n]).max() <= 1e-4
+    hb, xb = parity_bar(g)  # 10x the reference's config-2 floor: 5.8e-5 / 3.9e-6
+    assert np.abs(h[:n] - hr[:n]).max() <= hb
     st = int(g["solution_stride"])
     xs = u.grid_view(prob.hierarchy)[::st, ::st]
     ref = g["solution_sub"]
-    assert np.linalg.norm(xs - ref) <= 1e-5 * np.linalg.norm(ref)
+    assert np.linalg.norm(xs - ref) <= xb * np.linalg.norm(ref)
 
 
 # ------------------------------------------------------------- Bi-CGSTAB
@@ -627,34 +692,40 @@ def test_presets_and_bicgstab_cslp_vs_reference(name):
 @pytest.mark.parametrize("f", [10, 20, 40])
 def test_config3_wedge_vs_reference(f):
     """BASELINE configs[2]: wedge with the BASELINE interfaces, h = 0.5 m (1201 x 2001), 5 levels,
-    against the reference's own full runs (tests/golden/solve_c3_*.npz)."""
+    against the reference's own full runs (tests/golden/solve_c3_*.npz), at the BASELINE
+    bar: same outer count, history within 1e-9 per iteration, solution within 1e-8
+    relative L2 (every 8th point).  Measured: <= 2.2e-14 / 7.6e-14; the reference's
+    own floors are 1.0e-11 / 8.6e-10 / 3.1e-5 (history) at 10 / 20 / 40 Hz."""
     g = golden(f"solve_c3_{f}.npz")
     prob = hdb.wedge_problem(f=float(f), nx=1201, ml=5, layers=hdb.grid.BASELINE_WEDGE_LAYERS)
     with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
         u, rep = s.solve(prob.rhs)
-    assert abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
+    assert rep.outer_iterations == int(g["outer_iterations"])
     assert rep.converged and rep.final_relres <= 1e-6
     h, hr = np.array(rep.residual_history), g["residual_history"]
-    n = min(len(h), len(hr))
-    assert np.abs(h[:n] - hr[:n]).max() <= 1e-6
+    assert np.abs(h - hr).max() <= 1e-9
     st = int(g["solution_stride"])
     xs = u.grid_view(prob.hierarchy)[::st, ::st]
     ref = g["solution_sub"]
-    assert np.linalg.norm(xs - ref) <= 1e-6 * np.linalg.norm(ref)
+    assert np.linalg.norm(xs - ref) <= 1e-8 * np.linalg.norm(ref)
 
 
 def test_config4_synthetic_layered_vs_reference():
     """BASELINE configs[3] model (seeded generator, models.py) at h = 6 m, 40 Hz, 3 levels, against
-    the reference solving the same raster (tests/golden/solve_c4_h6_f40.npz)."""
+    the reference solving the same raster through its gridfile path (tests/golden/
+    solve_c4_h6_f40.npz): outer count +-1, history / solution at the BASELINE bar or
+    10x the reference's own floor for this case (gold.parity_bar)."""
     g = golden("solve_c4_h6_f40.npz")
     prob = hdb.synthetic_layered_problem(40.0, 6.0, 3)
     hier = prob.hierarchy
-    np.testing.assert_allclose([hier.ksq[0].sum(), hier.ksq[2].sum()], g["ksq_checksum"], rtol=0, atol=0)
+    np.testing.assert_array_equal([hier.ksq[0].sum(), hier.ksq[2].sum()], g["ksq_checksum"])
     with hdb.MadpSolver(hier, hdb.preset("MADP", hier)) as s:
         u, rep = s.solve(prob.rhs)
     assert abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
+    assert rep.converged == bool(g["converged"])
     h, hr = np.array(rep.residual_history), g["residual_history"]
     n = min(len(h), len(hr))
-    assert np.abs(h[:n] - hr[:n]).max() <= 1e-6
+    hb, xb = parity_bar(g)
+    assert np.abs(h[:n] - hr[:n]).max() <= hb
     st = int(g["solution_stride"])
-    assert np.linalg.norm(u.grid_view(hier)[::st, ::st] - g["solution_sub"]) <= 1e-6 * np.linalg.norm(g["solution_sub"])
+    assert np.linalg.norm(u.grid_view(hier)[::st, ::st] - g["solution_sub"]) <= xb * np.linalg.norm(g["solution_sub"])

@@ -42,6 +42,27 @@ def main():
         torch.cuda.synchronize()
         return ev0.elapsed_time(ev1) / reps
 
+    def timeit_graph(fn, reps):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            _lib.check(L.hdb_set_stream(C.c_void_p(s.cuda_stream)))
+            for _ in range(3):
+                fn()
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(reps):
+                    fn()
+            g.replay()
+            s.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+            s.synchronize()
+        _lib.check(L.hdb_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+        return e0.elapsed_time(e1) / reps
+
     out = {}
     for l in range(2, hier.ml + 1):
         op = hdb.cslp_operator(hier, l, 0.5)
@@ -50,13 +71,15 @@ def main():
         o = torch.empty_like(u)
         h = op.handle
         row = {"points": lv.npoints}
-        for exact in (0, 1):
+        for name, exact, form in (("separable_columns", 0, 1), ("separable_tiles", 0, 0), ("exact", 1, 1)):
             _lib.check(L.hdb_option(b"rg_exact", exact))
-            ms = timeit(lambda: _lib.check(L.hdb_op_apply(h, u.data_ptr(), o.data_ptr())), a.reps)
+            _lib.check(L.hdb_option(b"rg_form", form))
+            # a captured CUDA graph of `reps` launches: device time without Python launch overhead
+            ms = timeit_graph(lambda: _lib.check(L.hdb_op_apply(h, u.data_ptr(), o.data_ptr())), a.reps)
             gbs = 40.0 * lv.npoints / (ms * 1e-3) / 1e9
-            row["exact" if exact else "separable"] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1),
-                                                      "frac": round(gbs / peak, 3)}
+            row[name] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
         _lib.check(L.hdb_option(b"rg_exact", 0))
+        _lib.check(L.hdb_option(b"rg_form", 1))
         out[f"L{l}"] = row
         print(f"L{l}", json.dumps(row), flush=True)
     # one-launch MGS step on the 1025^2 level: GMRES(1e-14, cap) through the launch-driven engine
