@@ -533,7 +533,6 @@ int hdb_option(const char* name, int value) {
     const std::string k = name ? name : "";
     if (k == "mgs_ls") set_mgs_ls(value);
     else if (k == "rg_exact") set_rg_exact(value);
-    else if (k == "rg_form") set_rg_form(value);
     else throw Error(E_ARG, "unknown option " + k);
   });
 }

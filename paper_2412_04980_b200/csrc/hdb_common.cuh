@@ -11,6 +11,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #define HDB_BC_SOMMERFELD 0
 #define HDB_BC_DIRICHLET 1
 
@@ -75,6 +79,21 @@ struct OpCoef {
   double lsc;
   cd msc;
 };
+
+// Raise a kernel's dynamic shared-memory limit to >= bytes on the current device,
+// once per (device, kernel) and size; thread-safe (rank threads share a process).
+inline bool ensure_smem_attr(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = done[{dev, fn}];
+  if (bytes <= cur) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess) return false;
+  cur = bytes;
+  return true;
+}
 
 constexpr int kReduceThreads = 256;
 constexpr int kMaxReduceBlocks = 592;  // 4 x 148 SMs

@@ -63,7 +63,6 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
 bool mgs_ls_fits(long long n, int j);
 void set_mgs_ls(int on);
 void set_rg_exact(int on);
-void set_rg_form(int f);
 bool rg_exact_on();    // separable K2 kernel: 0 tile form, 1 column-marching form (default)  // 1: radius-2/3 levels use the reference's exact tap order (HDB_RG_EXACT=1)  // runtime switch (HDB_MGS_LS=0 at start-up does the same)
 long long mgs_ls_tg_elems();
 bool mgs_grid_fits(long long n);

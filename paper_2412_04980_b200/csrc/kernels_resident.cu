@@ -23,6 +23,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "kernels.h"
 #include "stencil.cuh"
@@ -52,7 +53,6 @@ struct ResidentArgs {
   long long* prof;    // optional: per-phase cycles of CTA 0 thread 0 (telemetry), may be null
   int tiled;          // stencil windows staged in shared memory
   int tile_elems;     // window elements (max over CTAs)
-  int sep;            // radius 2/3: separable 1D passes (column walk) instead of the tap sum
 };
 
 // phase clock (CTA 0, thread 0) — only when A.prof != nullptr
@@ -184,74 +184,6 @@ __device__ __forceinline__ cd op_point_tile(const OpCoef& c, const Geom& g, cons
     }
   }
   return acc;
-}
-
-// Separable form of the radius-2/3 operator on this CTA's points (csrc/
-// kernels_stencil.cu k_rgc, same association of the products): each thread
-// walks one column of the window in segments of up to GSEG own rows.  Sweep 1
-// accumulates sum_a a_a (M u)_a (and the mass sum), sweep 2 continues with
-// sum_a m_a (A u)_a, so every output receives its terms in k_rgc's order.
-constexpr int GSEG = 4;
-template <int R>
-__device__ __forceinline__ void sep_cols(const OpCoef& c, const Geom& g, const Tile& T, const cd* ut,
-                                         const double* kt, bool uni, double ku, long long p0, long long p1, cd* ws) {
-  constexpr int N = 2 * R + 1;
-  const int nx = g.nx;
-  const int ylo = (int)(p0 / nx), yhi = (int)((p1 - 1) / nx);  // slab-local rows
-  for (int x = threadIdx.x; x < nx; x += kRT) {
-    const int ya = ylo + ((long long)ylo * nx + x < p0 ? 1 : 0);
-    const int yb = yhi - ((long long)yhi * nx + x >= p1 ? 1 : 0);
-    for (int s0 = ya; s0 <= yb; s0 += GSEG) {
-      const int len = min(GSEG, yb - s0 + 1);
-      cd lm[GSEG], lk[GSEG];
-#pragma unroll
-      for (int q = 0; q < GSEG; ++q) { lm[q] = mkc(0.0, 0.0); lk[q] = mkc(0.0, 0.0); }
-      const int tr0 = s0 + g.row0 - T.rlo;  // window row of H row s0 - R
-      for (int sweep = 0; sweep < 2; ++sweep) {
-        for (int rr = 0; rr < len + 2 * R; ++rr) {
-          const cd* urow = ut + (tr0 + rr) * T.cols + x;
-          cd hm = mkc(0.0, 0.0), hk = mkc(0.0, 0.0);
-#pragma unroll
-          for (int bb = 0; bb < N; ++bb) {
-            const cd v = urow[bb];
-            const double w = sweep == 0 ? c.sm[bb] : c.sa[bb];
-            hm.x = fma(w, v.x, hm.x); hm.y = fma(w, v.y, hm.y);
-            if (sweep == 0 && !uni) {
-              const double kq = kt[(tr0 + rr) * T.cols + x + bb];
-              hk.x = fma(c.sm[bb], kq * v.x, hk.x); hk.y = fma(c.sm[bb], kq * v.y, hk.y);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < GSEG; ++q) {
-            const int a = rr - q;
-            if (q < len && a >= 0 && a < N) {
-              const double wa = sweep == 0 ? c.sa[a] : c.sm[a];
-              lm[q].x = fma(wa, hm.x, lm[q].x); lm[q].y = fma(wa, hm.y, lm[q].y);
-              if (sweep == 0) {
-                const cd hq = uni ? hm : hk;
-                lk[q].x = fma(c.sm[a], hq.x, lk[q].x); lk[q].y = fma(c.sm[a], hq.y, lk[q].y);
-              }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < GSEG; ++q) {
-        if (q >= len) break;
-        const int y = s0 + q, gj = y + g.row0;
-        cd v;
-        if (pinned(g, c, gj, x)) {
-          v = ut[(tr0 + q + R) * T.cols + x + R];
-        } else {
-          cd m = lk[q];
-          if (uni) m = mkc(ku * m.x, ku * m.y);
-          v.x = fma(c.lsc, lm[q].x, fma(c.msc.x, m.x, -c.msc.y * m.y));
-          v.y = fma(c.lsc, lm[q].y, fma(c.msc.x, m.y, c.msc.y * m.x));
-        }
-        ws[(long long)y * nx + x - p0] = v;
-      }
-    }
-  }
 }
 
 __device__ __forceinline__ cd warp_sum_c(cd v) {
@@ -558,7 +490,6 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
   if (A.tiled && cnt > 0) load_k_tile<R>(kt, T, A.ksq, A.g, A.c);
   const cd* ucoef = nullptr;
-  double kuni = 0.0;  // the window's k^2 when it is uniform
   if (A.tiled && R > 1) {
     if (threadIdx.x == 0) s.uniform = cnt > 0;
     __syncthreads();
@@ -574,7 +505,6 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
         s.coef[threadIdx.x] = mkc(__dadd_rn(A.c.lap[threadIdx.x], __dmul_rn(m.x, k00)), __dmul_rn(m.y, k00));
       }
       ucoef = s.coef;
-      kuni = k00;
     }
     __syncthreads();
   }
@@ -674,9 +604,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       s.decision = !finite ? 2 : ((hn < 1e-30 || rel <= A.tol) ? 1 : 0);
     }
     PHASE(10);
-    if (jv < A.cap && R > 1 && A.sep && A.tiled) {
-      if (cnt > 0) sep_cols<R>(A.c, A.g, T, ut, kt, ucoef != nullptr, kuni, p0, p1, ws);
-    } else if (jv < A.cap) {  // the stencil of step jv (skipped past the cap)
+    if (jv < A.cap) {  // the stencil of step jv (skipped past the cap)
       for (int q = t; q < cnt; q += kRT) {
         const long long p = p0 + q;
         const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
@@ -806,21 +734,12 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     if (cnt > 0) load_u_tile<R>(ut, T, A.x, A.ksq, A.g, A.c);
     __syncthreads();
   }
-  if (R > 1 && A.sep && A.tiled) {
-    if (cnt > 0) sep_cols<R>(A.c, A.g, T, ut, kt, ucoef != nullptr, kuni, p0, p1, ws);
-    __syncthreads();
-    for (int q = t; q < cnt; q += kRT) {
-      const cd d = c_sub(A.b[p0 + q], ws[q]);
-      f = c_conjmul_acc(f, d, d);
-    }
-  } else {
-    for (int q = t; q < cnt; q += kRT) {
-      const long long p = p0 + q;
-      const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
-      const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
-      const cd d = c_sub(A.b[p], ax);
-      f = c_conjmul_acc(f, d, d);
-    }
+  for (int q = t; q < cnt; q += kRT) {
+    const long long p = p0 + q;
+    const int gj = (int)(p / nx) + A.g.row0, i = (int)(p % nx);
+    const cd ax = A.tiled ? op_point_tile<R>(A.c, A.g, T, ut, kt, ucoef, gj, i) : op_point<R>(A.c, A.g, A.x, A.ksq, gj, i);
+    const cd d = c_sub(A.b[p], ax);
+    f = c_conjmul_acc(f, d, d);
   }
   const double fin = sqrt(fmax(sy.reduce(f, s, buf, A.gpart).x, 0.0)) / bnorm;
   if (rank == 0 && t == 0) {
@@ -860,19 +779,23 @@ void resident_set_profile(long long* dev_counters) { g_prof = dev_counters; }
 static int g_grid = 0;
 static size_t g_smem_optin = 0;
 
+// device limits, read once per process (every rank thread of a process uses the
+// same device model); std::call_once makes the first use thread-safe
+static std::once_flag g_limits_once;
 static void init_limits() {
-  if (g_smem_optin) return;
-  int dev = 0, v = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  g_smem_optin = (size_t)v;
-  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-  g_grid = v > 32 * kGridRounds ? 32 * kGridRounds : v;  // reductions batch <= 32 * kGridRounds partials
+  std::call_once(g_limits_once, [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    g_grid = v > 32 * kGridRounds ? 32 * kGridRounds : v;  // reductions batch <= 32 * kGridRounds partials
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    g_smem_optin = (size_t)v;
+  });
 }
 
 template <class K>
 static void set_attrs(K kern, size_t sm, bool cluster) {
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  ensure_smem_attr((const void*)kern, sm);
   if (cluster) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
@@ -915,11 +838,25 @@ static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
   return cudaLaunchKernelEx(&cfg, kern, b) == cudaSuccess;
 }
 
+// CTAs of a grid-mode resident solve: all SMs by default; HDB_RES_GRID_PTS=p caps
+// the grid at one CTA per p points (fewer CTAs: cheaper barriers and reductions)
+static int grid_ctas_for(long long n) {
+  static long long per = -1;
+  if (per < 0) {
+    const char* e = getenv("HDB_RES_GRID_PTS");
+    per = e ? atoll(e) : 0;
+  }
+  if (per <= 0) return g_grid;
+  const long long p = (n + per - 1) / per;
+  return (int)std::max(16LL, std::min<long long>(g_grid, p));
+}
+
 template <int R, int O>
 static bool launch_grid(ResidentArgs a, cudaStream_t st) {
   auto kern = k_resident_gmres<GridSync, R, O>;
-  const long long chunk = (a.n + g_grid - 1) / g_grid;
-  a.tile_elems = tile_elems_for(a.n, a.g.nx, g_grid, R);
+  const int P = grid_ctas_for(a.n);
+  const long long chunk = (a.n + P - 1) / P;
+  a.tile_elems = tile_elems_for(a.n, a.g.nx, P, R);
   size_t sm = smem_tiled(chunk, a.tile_elems, false);
   a.tiled = sm <= g_smem_optin;
   if (!a.tiled) return false;  // untiled resident solves lose to the launch path
@@ -930,7 +867,7 @@ static bool launch_grid(ResidentArgs a, cudaStream_t st) {
     return false;
   }
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((void*)kern, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess;
+  return cudaLaunchCooperativeKernel((void*)kern, dim3(P), dim3(kRT), args, sm, st) == cudaSuccess;
 }
 
 int resident_max_cap() { return kMaxCap; }
@@ -972,7 +909,6 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
   ResidentArgs a{};
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
   a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
-  a.sep = c.sep && !rg_exact_on();
   if (ortho == 1 && cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
   if (ortho == 2 && cap + 2 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
   const bool ok = ortho == 2 ? launch_any<2>(mode, a, c.radius, st)
@@ -1468,12 +1404,18 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   }
   gr.sync();
   cd* tot = &s.stage[0][0];  // [0, 2j]: g then l; [2j+1, 3j]: new T row; [3j+1, 4j+1]: h
-  for (int e = wid; e < ne; e += kRT / 32) {  // rank-ordered per lane, then a fixed warp tree
+  for (int e = wid; e < ne; e += kRT / 32) {  // rank-ordered per lane (all loads in flight), then a warp tree
+    cd z[kGridRounds];
+#pragma unroll
+    for (int u = 0; u < kGridRounds; ++u) {
+      const int r = lane + 32 * u;
+      z[u] = r < P ? __ldcg(&gpart[(long long)r * kVecCap + e]) : mkc(0.0, 0.0);
+    }
     cd a = mkc(0.0, 0.0);
-    for (int r = lane; r < P; r += 32) {
-      const cd z = __ldcg(&gpart[(long long)r * kVecCap + e]);
-      a.x += z.x;
-      a.y += z.y;
+#pragma unroll
+    for (int u = 0; u < kGridRounds; ++u) {
+      a.x += z[u].x;
+      a.y += z[u].y;
     }
     a = warp_sum_c(a);
     if (lane == 0) tot[e] = a;
@@ -1482,13 +1424,26 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   cd* trow = tot + ne;
   cd* hs = trow + j;
   const long long rj = (long long)j * (j + 1) / 2;
+  // T entries come from L2: batches of kLsTB independent loads, then the ordered FMAs
+  constexpr int kLsTB = 8;
   if (t < j) {  // t_jk = -sum_{m=k}^{j-1} l_m T_mk
     cd a = mkc(0.0, 0.0);
-    for (int m = t; m < j; ++m) {
-      const cd tm = __ldcg(&Tg[(long long)m * (m + 1) / 2 + t]);
-      const cd lm = tot[j + 1 + m];
-      a.x = __fma_rn(lm.x, tm.x, a.x); a.x = __fma_rn(-lm.y, tm.y, a.x);
-      a.y = __fma_rn(lm.x, tm.y, a.y); a.y = __fma_rn(lm.y, tm.x, a.y);
+    for (int m0 = t; m0 < j; m0 += kLsTB) {
+      cd tm[kLsTB];
+#pragma unroll
+      for (int u = 0; u < kLsTB; ++u) {
+        const int m = m0 + u;
+        tm[u] = m < j ? __ldcg(&Tg[(long long)m * (m + 1) / 2 + t]) : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kLsTB; ++u) {
+        const int m = m0 + u;
+        if (m < j) {
+          const cd lm = tot[j + 1 + m];
+          a.x = __fma_rn(lm.x, tm[u].x, a.x); a.x = __fma_rn(-lm.y, tm[u].y, a.x);
+          a.y = __fma_rn(lm.x, tm[u].y, a.y); a.y = __fma_rn(lm.y, tm[u].x, a.y);
+        }
+      }
     }
     trow[t] = mkc(-a.x, -a.y);
     if (rank == 0) Tg[rj + t] = mkc(-a.x, -a.y);
@@ -1498,11 +1453,23 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   if (t <= j) {  // h_i = sum_{k <= i} T_ik g_k
     cd a = mkc(0.0, 0.0);
     const long long ri = (long long)t * (t + 1) / 2;
-    for (int k = 0; k <= t; ++k) {
-      const cd tk = t < j ? (k < t ? __ldcg(&Tg[ri + k]) : mkc(1.0, 0.0)) : (k < j ? trow[k] : mkc(1.0, 0.0));
-      const cd gk = tot[k];
-      a.x = __fma_rn(tk.x, gk.x, a.x); a.x = __fma_rn(-tk.y, gk.y, a.x);
-      a.y = __fma_rn(tk.x, gk.y, a.y); a.y = __fma_rn(tk.y, gk.x, a.y);
+    for (int k0 = 0; k0 <= t; k0 += kLsTB) {
+      cd tk[kLsTB];
+#pragma unroll
+      for (int u = 0; u < kLsTB; ++u) {
+        const int k = k0 + u;
+        tk[u] = k > t ? mkc(0.0, 0.0)
+                      : (t < j ? (k < t ? __ldcg(&Tg[ri + k]) : mkc(1.0, 0.0)) : (k < j ? trow[k] : mkc(1.0, 0.0)));
+      }
+#pragma unroll
+      for (int u = 0; u < kLsTB; ++u) {
+        const int k = k0 + u;
+        if (k <= t) {
+          const cd gk = tot[k];
+          a.x = __fma_rn(tk[u].x, gk.x, a.x); a.x = __fma_rn(-tk[u].y, gk.y, a.x);
+          a.y = __fma_rn(tk[u].x, gk.y, a.y); a.y = __fma_rn(tk[u].y, gk.x, a.y);
+        }
+      }
     }
     hs[t] = a;
     if (rank == 0) hout[t] = a;
@@ -1612,11 +1579,7 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
                     const int* skip, cd* tg) {
   if (tg && mgs_ls_fits(n, j)) {
     const size_t sm = mgs_ls_smem((n + g_grid - 1) / g_grid);
-    static size_t configured_ls = 0;
-    if (sm > configured_ls) {
-      if (cudaFuncSetAttribute(k_mgs_ls, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) return 1;
-      configured_ls = sm;
-    }
+    if (!ensure_smem_attr((const void*)k_mgs_ls, sm)) return 1;
     void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip};
     return cudaLaunchCooperativeKernel((void*)k_mgs_ls, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
   }
@@ -1626,31 +1589,19 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
   if (plan == 2) {
     const size_t head = ((sizeof(MgsSmem) + 15) / 16) * 16;
     const size_t sm2 = head + (size_t)ks * kRT * sizeof(cd);
-    static size_t configured2 = 0;
-    if (sm2 > configured2) {
-      cudaFuncSetAttribute(k_mgs_grid2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-      configured2 = sm2;
-    }
+    if (!ensure_smem_attr((const void*)k_mgs_grid2, sm2)) return 1;
     int ksi = (int)ks;
     void* args2[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &ksi, (void*)&skip};
     return cudaLaunchCooperativeKernel((void*)k_mgs_grid2, dim3(g_grid), dim3(kRT), args2, sm2, st) == cudaSuccess ? 0 : 1;
   }
   if (plan == 3) {
     const size_t sm3 = mgs_t_smem((n + g_grid - 1) / g_grid);
-    static size_t configured3 = 0;
-    if (sm3 > configured3) {
-      cudaFuncSetAttribute(k_mgs_grid_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-      configured3 = sm3;
-    }
+    if (!ensure_smem_attr((const void*)k_mgs_grid_t, sm3)) return 1;
     void* args3[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, (void*)&skip};
     return cudaLaunchCooperativeKernel((void*)k_mgs_grid_t, dim3(g_grid), dim3(kRT), args3, sm3, st) == cudaSuccess ? 0 : 1;
   }
   const size_t sm = smem_for((n + g_grid - 1) / g_grid, false);
-  static size_t configured = 0;
-  if (sm > configured) {
-    cudaFuncSetAttribute(k_mgs_grid, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    configured = sm;
-  }
+  if (!ensure_smem_attr((const void*)k_mgs_grid, sm)) return 1;
   void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, (void*)&skip};
   return cudaLaunchCooperativeKernel((void*)k_mgs_grid, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
 }

@@ -579,11 +579,7 @@ __global__ void __launch_bounds__(32 * HTY) k_rgh(const cd* __restrict__ u, cons
 template <int R, int MODE>
 static void launch_rgh(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
                        cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_rgh<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HTile<R>::bytes);
-    configured = true;
-  }
+  ensure_smem_attr((const void*)k_rgh<R, MODE>, HTile<R>::bytes);
   const dim3 blk(32, HTY), grd((g.nx + HTX - 1) / HTX, (g.ny + HTY - 1) / HTY);
   k_rgh<R, MODE><<<grd, blk, HTile<R>::bytes, st>>>(u, b, k, out, g, c);
 }
@@ -769,162 +765,10 @@ __global__ void __launch_bounds__(256, 2) k_rgs(const cd* __restrict__ u, const 
 template <int R, int MODE>
 static void launch_rgs(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
                        cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_rgs<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GSTile<R>::bytes);
-    configured = true;
-  }
+  ensure_smem_attr((const void*)k_rgs<R, MODE>, GSTile<R>::bytes);
   const dim3 grd((g.nx + GS_T - 1) / GS_T, (g.ny + GS_T - 1) / GS_T);
   k_rgs<R, MODE><<<grd, 256, GSTile<R>::bytes, st>>>(u, b, k, out, g, c);
 }
-
-// Column-marching form of K2: a CTA owns GC_W = 128 columns x GC_H = 16 output
-// rows; the input block ((16 + 2R) x (128 + 2R) samples of u and, off the
-// uniform interior, k^2) is staged in shared memory with all loads in flight,
-// then each thread walks down ONE column: for every block row it forms the row
-// sums (M u, A u, M (k u)) at its column from the 2R + 1 staged neighbours and
-// keeps the last 2R + 1 of them in a register ring, so every output row costs
-// one new set of row sums plus the vertical combination -- no further shared
-// memory traffic or barriers.  Same arithmetic association as k_rgs.
-// Level grids have 2^m + 1 columns: one extra thread per CTA lets the last
-// column strip own GC_W + 1 columns instead of launching a 1-column strip.
-constexpr int GC_W = 128, GC_H = 16, GC_T = GC_W + 1;
-template <int R>
-struct GCTile {
-  static constexpr int TR = GC_H + 2 * R, TC = GC_T + 2 * R;
-  static constexpr size_t u_bytes = (size_t)TR * TC * sizeof(cd);
-  static constexpr size_t bytes = u_bytes + (size_t)TR * TC * sizeof(double);
-};
-
-template <int R, int MODE>
-__global__ void __launch_bounds__(GC_T, 3) k_rgc(const cd* __restrict__ u, const cd* __restrict__ b,
-                                                 const double* __restrict__ k, cd* __restrict__ out, Geom g,
-                                                 OpCoef c) {
-  if (c.skip && *c.skip) return;
-  using T = GCTile<R>;
-  constexpr int N = 2 * R + 1, TR = T::TR, TC = T::TC;
-  extern __shared__ __align__(16) unsigned char gcm[];
-  cd* su = reinterpret_cast<cd*>(gcm);
-  double* sk = reinterpret_cast<double*>(gcm + T::u_bytes);
-  const int i0 = blockIdx.x * GC_W, j0 = blockIdx.y * GC_H;
-  const int wcols = blockIdx.x == gridDim.x - 1 ? g.nx - i0 : GC_W;  // this strip's columns (<= GC_T)
-  const bool fast = c.uniform && i0 >= R && i0 + wcols + R <= g.nx && g.row0 + j0 >= R &&
-                    g.row0 + j0 + GC_H + R <= g.nyg;
-  const int tid = threadIdx.x;
-  const int tcols = wcols + 2 * R;  // staged columns of this strip
-  if (fast) {
-    constexpr int NL = (TR * TC + GC_T - 1) / GC_T;
-    constexpr int NB = 8;  // loads in flight per batch
-#pragma unroll
-    for (int l0 = 0; l0 < NL; l0 += NB) {
-      cd v[NB];
-#pragma unroll
-      for (int l = 0; l < NB; ++l) {
-        const int t = tid + (l0 + l) * GC_T;
-        const int ty = t / TC, tx = t - ty * TC;
-        v[l] = (l0 + l < NL && t < TR * TC && tx < tcols) ? U(u, g, g.row0 + j0 + ty - R, i0 + tx - R)
-                                                          : mkc(0.0, 0.0);
-      }
-#pragma unroll
-      for (int l = 0; l < NB; ++l) {
-        const int t = tid + (l0 + l) * GC_T;
-        if (l0 + l < NL && t < TR * TC) su[t] = v[l];
-      }
-    }
-  } else {
-    for (int t = tid; t < TR * TC; t += GC_T) {
-      const int ty = t / TC, tx = t - ty * TC;
-      if (tx >= tcols) continue;
-      const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
-      su[t] = upad(u, k, g, c, gj, gi);
-      sk[t] = kpad(k, g, c, gj, gi);
-    }
-  }
-  __syncthreads();
-  const int x = tid, i = i0 + x;
-  if (x >= wcols) return;
-  cd hm[N], ha[N], hk[N];
-#pragma unroll
-  for (int r = 0; r < TR; ++r) {
-    const cd* row = su + r * TC + x;
-    cd am = mkc(0.0, 0.0), aa = mkc(0.0, 0.0), ak = mkc(0.0, 0.0);
-#pragma unroll
-    for (int bb = 0; bb < N; ++bb) {
-      const cd v = row[bb];
-      am.x = fma(c.sm[bb], v.x, am.x); am.y = fma(c.sm[bb], v.y, am.y);
-      aa.x = fma(c.sa[bb], v.x, aa.x); aa.y = fma(c.sa[bb], v.y, aa.y);
-      if (!fast) {
-        const double kq = sk[r * TC + x + bb];
-        ak.x = fma(c.sm[bb], kq * v.x, ak.x); ak.y = fma(c.sm[bb], kq * v.y, ak.y);
-      }
-    }
-    hm[r % N] = am;
-    ha[r % N] = aa;
-    hk[r % N] = ak;
-    if (r >= 2 * R) {
-      const int o = r - 2 * R;
-      const int j = j0 + o;
-      if (j < g.ny) {
-        cd lm = mkc(0.0, 0.0), lk = mkc(0.0, 0.0);
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-          const cd m = hm[(o + a) % N];
-          lm.x = fma(c.sa[a], m.x, lm.x); lm.y = fma(c.sa[a], m.y, lm.y);
-          if (fast) { lk.x = fma(c.sm[a], m.x, lk.x); lk.y = fma(c.sm[a], m.y, lk.y); }
-        }
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-          const cd q = ha[(o + a) % N];
-          lm.x = fma(c.sm[a], q.x, lm.x); lm.y = fma(c.sm[a], q.y, lm.y);
-        }
-        if (fast) {
-          lk = mkc(c.ku * lk.x, c.ku * lk.y);
-        } else {
-#pragma unroll
-          for (int a = 0; a < N; ++a) {
-            const cd q = hk[(o + a) % N];
-            lk.x = fma(c.sm[a], q.x, lk.x); lk.y = fma(c.sm[a], q.y, lk.y);
-          }
-        }
-        const int gj = j + g.row0;
-        const long long p = (long long)j * g.nx + i;
-        cd v;
-        if (pinned(g, c, gj, i)) {
-          v = su[(o + R) * TC + x + R];
-        } else {
-          v.x = fma(c.lsc, lm.x, fma(c.msc.x, lk.x, -c.msc.y * lk.y));
-          v.y = fma(c.lsc, lm.y, fma(c.msc.x, lk.y, c.msc.y * lk.x));
-        }
-        out[p] = MODE == 0 ? v : c_sub(b[p], v);
-      }
-    }
-  }
-}
-
-template <int R, int MODE>
-static void launch_rgc(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
-                       cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_rgc<R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GCTile<R>::bytes);
-    configured = true;
-  }
-  // strips of GC_W columns; the last takes the remainder (<= GC_T when nx = 128 m + 1)
-  int strips = (g.nx + GC_W - 1) / GC_W;
-  if (strips > 1 && g.nx - (strips - 1) * GC_W == 1) --strips;
-  const dim3 grd(strips, (g.ny + GC_H - 1) / GC_H);
-  k_rgc<R, MODE><<<grd, GC_T, GCTile<R>::bytes, st>>>(u, b, k, out, g, c);
-}
-
-static int g_rg_form = -1;  // HDB_RG_FORM: 0 tile form (k_rgs), 1 column-marching form (k_rgc, default)
-static int rg_form() {
-  if (g_rg_form < 0) {
-    const char* e = getenv("HDB_RG_FORM");
-    g_rg_form = e ? atoi(e) : 1;
-  }
-  return g_rg_form;
-}
-void set_rg_form(int f) { g_rg_form = f; }
 
 static int g_rg_exact = -1;  // -1: from HDB_RG_EXACT (default 0 = separable form where available)
 void set_rg_exact(int on) { g_rg_exact = on ? 1 : 0; }
@@ -983,16 +827,6 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
     const dim3 blk(32, 8), grd = grid_r1(g);
     if (mode == 0) k_r1<0><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
     else k_r1<1><<<grd, blk, 0, st>>>(u, b, k, out, g, c, 0.0);
-    return;
-  }
-  if (c.sep && !rg_exact() && rg_form() == 1) {
-    if (c.radius == 2) {
-      if (mode == 0) launch_rgc<2, 0>(c, g, u, b, k, out, st);
-      else launch_rgc<2, 1>(c, g, u, b, k, out, st);
-    } else {
-      if (mode == 0) launch_rgc<3, 0>(c, g, u, b, k, out, st);
-      else launch_rgc<3, 1>(c, g, u, b, k, out, st);
-    }
     return;
   }
   if (c.sep && !rg_exact()) {

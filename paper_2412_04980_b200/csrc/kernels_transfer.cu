@@ -378,11 +378,7 @@ static bool cached_fine_map(CUtensorMap* m, const cd* fine, const TGeom& t) {
 template <int TST, int TSR>
 static void launch_restrict_tk(const CUtensorMap& m, cd* coarse, const TGeom& t, int zero_mask, cudaStream_t st) {
   constexpr size_t smem = (size_t)TST * kTBoxBytes + sizeof(TRing<TST>);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_restrict_t<TST, TSR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  ensure_smem_attr((const void*)k_restrict_t<TST, TSR>, smem);
   const dim3 grd((t.ncx + TCC - 1) / TCC, (t.c_ny + TSR - 1) / TSR);
   k_restrict_t<TST, TSR><<<grd, 96, smem, st>>>(m, coarse, t, zero_mask);
 }
@@ -580,11 +576,7 @@ static bool launch_prolong_t(const cd* coarse, const cd* base, cd* fine, const T
     if (n < 32) ++n;
   }
   constexpr size_t smem = PST * (kPCoarseBytes + kPBaseBytes) + 2 * kPBaseBytes + 2 * sizeof(cd) + sizeof(PRing);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_prolong_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  ensure_smem_attr((const void*)k_prolong_t, smem);
   const int cy_lo = t.f_row0 / 2, cy_hi = (t.f_row0 + t.f_ny - 1) / 2;
   const int cnt = cy_hi - cy_lo + 1;
   const dim3 grd((t.ncx + PCC - 1) / PCC, (cnt + PSR - 1) / PSR);

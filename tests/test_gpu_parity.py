@@ -130,21 +130,13 @@ def test_separable_galerkin_vs_exact_taps(shape, level, bnd, uniform):
                             level_scale=4.0 ** (level - 1))
     u, b = _rand(rng, shape), _rand(rng, shape)
     au = ref.apply(u)
-    from paper_2412_04980_b200 import _lib
-    outs = []
-    for form in (1, 0):  # column-marching kernel (default), tile kernel
-        _lib.check(_lib.lib().hdb_option(b"rg_form", form))
-        got = op.apply(u)
-        assert np.abs(got - au).max() <= 8 * np.finfo(float).eps * np.abs(au).max()
-        res = op.residual(b, u)
-        assert np.abs(res - (b - au)).max() <= 8 * np.finfo(float).eps * np.abs(b - au).max()
-        if bnd[0] == "dirichlet":
-            np.testing.assert_array_equal(got[:, 0], u[:, 0])
-            np.testing.assert_array_equal(got[0, :], u[0, :])
-        outs.append(got)
-    _lib.check(_lib.lib().hdb_option(b"rg_form", 1))
-    if not uniform:  # same association of the products (the uniform shortcut depends on the tile shape)
-        np.testing.assert_array_equal(outs[0], outs[1])
+    got = op.apply(u)
+    assert np.abs(got - au).max() <= 8 * np.finfo(float).eps * np.abs(au).max()
+    res = op.residual(b, u)
+    assert np.abs(res - (b - au)).max() <= 8 * np.finfo(float).eps * np.abs(b - au).max()
+    if bnd[0] == "dirichlet":
+        np.testing.assert_array_equal(got[:, 0], u[:, 0])
+        np.testing.assert_array_equal(got[0, :], u[0, :])
 
 
 @pytest.mark.parametrize("shape", [(1025, 1025), (600, 2050), (2049, 517), (777, 1111)])
@@ -393,9 +385,15 @@ def test_config1_dirichlet_first_20_outer_iterations():
     assert rep.outer_iterations == int(g["outer_iterations"]) == 20
     h, hr = np.array(rep.residual_history), g["residual_history"]
     # the reference itself moves by 2.3e-3 within these 20 iterations under a 1e-15 rhs
-    # perturbation (floor_hist_abs); measured GPU delta over the 20: ~1e-5 (profiles/r02e_parity.json)
-    assert np.abs(h[:3] - hr[:3]).max() <= 1e-9
-    assert np.abs(h - hr).max() <= 10 * float(g["floor_hist_abs"])
+    # perturbation (4e-7 already at iteration 2): each iteration is held to 10x the
+    # reference's own drift up to that iteration (solve_c1_full.npz floor_hist)
+    assert np.abs(h[:2] - hr[:2]).max() <= 1e-9
+    assert np.all(np.abs(h - hr) <= 10 * _floor_envelope(golden("solve_c1_full.npz"))[:21] + 1e-12)
+
+
+def _floor_envelope(g):
+    """Running max of the reference's |h_i - h'_i| against its 1e-15-perturbed twin."""
+    return np.maximum.accumulate(np.abs(g["residual_history"] - g["floor_hist"]))
 
 
 def test_config1_dirichlet_full_150_iteration_stall():
@@ -413,9 +411,9 @@ def test_config1_dirichlet_full_150_iteration_stall():
     assert not rep.converged and not bool(g["converged"])
     h, hr = np.array(rep.residual_history), g["residual_history"]
     assert len(h) == len(hr) == 151
-    assert np.abs(h[:3] - hr[:3]).max() <= 1e-9
+    assert np.abs(h[:2] - hr[:2]).max() <= 1e-9
+    assert np.all(np.abs(h - hr) <= 10 * _floor_envelope(g) + 1e-12)
     hb, xb = parity_bar(g)
-    assert np.abs(h - hr).max() <= hb
     st = int(g["solution_stride"])
     xs = u.grid_view(prob.hierarchy)[::st, ::st]
     assert np.linalg.norm(xs - g["solution_sub"]) <= xb * np.linalg.norm(g["solution_sub"])
@@ -552,36 +550,6 @@ def test_lowsync_mgs_step_matches_mgs_order():
     i1, r1, x1 = res[(1, 0.1)]
     assert i1 == repo.iterations
     assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
-
-
-@pytest.mark.parametrize("level,modes", [(4, (1,)), (6, (0, 1)), (7, (0, 1))])
-def test_resident_separable_stencil_vs_exact_taps(level, modes):
-    """The device-resident GMRES with the separable column-walk stencil (default)
-    against the same solve with the reference's exact tap order, on config 2's
-    coarse CSLP levels (513^2 grid mode, 129^2 and 65^2 cluster and grid mode):
-    same iteration count, relres and iterate to rounding."""
-    import ctypes as C
-    import torch
-    from paper_2412_04980_b200 import _lib
-    L = _lib.lib()
-    hier = hdb.mp1_problem(k=200.0, n=4097, ml=7).hierarchy
-    op = hdb.cslp_operator(hier, level, 0.5)
-    rng = _rng(60 + level)
-    b = torch.from_numpy(_rand(rng, op.shape)).cuda()
-    cap = hdb.cslp_iteration_cap(op.npoints)
-    for mode in modes:
-        res = []
-        for exact in (0, 1):
-            _lib.check(L.hdb_option(b"rg_exact", exact))
-            x = torch.empty_like(b)
-            its, rel = C.c_int(), C.c_double()
-            _lib.check(L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), 0.1, cap, mode, C.byref(its), C.byref(rel)))
-            res.append((its.value, rel.value, x.cpu().numpy()))
-        _lib.check(L.hdb_option(b"rg_exact", 0))
-        (i0, r0, x0), (i1, r1, x1) = res
-        assert i0 == i1
-        assert abs(r0 - r1) <= 1e-10 * r1
-        assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x1)
 
 
 ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))

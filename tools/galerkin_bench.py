@@ -71,15 +71,13 @@ def main():
         o = torch.empty_like(u)
         h = op.handle
         row = {"points": lv.npoints}
-        for name, exact, form in (("separable_columns", 0, 1), ("separable_tiles", 0, 0), ("exact", 1, 1)):
+        for name, exact in (("separable", 0), ("exact", 1)):
             _lib.check(L.hdb_option(b"rg_exact", exact))
-            _lib.check(L.hdb_option(b"rg_form", form))
             # a captured CUDA graph of `reps` launches: device time without Python launch overhead
             ms = timeit_graph(lambda: _lib.check(L.hdb_op_apply(h, u.data_ptr(), o.data_ptr())), a.reps)
             gbs = 40.0 * lv.npoints / (ms * 1e-3) / 1e9
             row[name] = {"us": round(ms * 1e3, 2), "gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
         _lib.check(L.hdb_option(b"rg_exact", 0))
-        _lib.check(L.hdb_option(b"rg_form", 1))
         out[f"L{l}"] = row
         print(f"L{l}", json.dumps(row), flush=True)
     # one-launch MGS step on the 1025^2 level: GMRES(1e-14, cap) through the launch-driven engine
