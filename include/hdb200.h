@@ -61,6 +61,10 @@ int hdb_stats(long long* launches, long long* bytes_alloc);
 int hdb_comm_unique_id(char* out128);
 int hdb_comm_init_nccl(const char* id128, int nranks, int rank);
 int hdb_comm_init_threads(long long group, int nranks, int rank);
+/* host-only rule of the sharded -> replicated level transition: the coarse rows
+ * [*row0, *row0 + *ny) this rank restricts before the all-gather, given every
+ * rank's fine slab start (no device needed)                                   */
+int hdb_plan_gather_rows(const int* fine_slab_row0, int nranks, int rank, int ncy_g, int* row0, int* ny);
 int hdb_thread_engine_begin(int device);
 int hdb_thread_engine_end(void);
 

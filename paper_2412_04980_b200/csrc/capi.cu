@@ -528,6 +528,14 @@ int hdb_op_set_separable(hdb_op* op, const double* sa, const double* sm, double 
   });
 }
 
+int hdb_plan_gather_rows(const int* fine_slab_row0, int nranks, int rank, int ncy_g, int* row0, int* ny) {
+  return guarded([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Error(E_ARG, "rank out of range");
+    std::vector<int> r0(fine_slab_row0, fine_slab_row0 + nranks);
+    gather_rows(r0, rank, ncy_g, *row0, *ny);
+  });
+}
+
 int hdb_option(const char* name, int value) {
   return guarded([&] {
     const std::string k = name ? name : "";

@@ -205,11 +205,14 @@ TGeom level_tgeom(const LevelOp& f, const LevelOp& c) {
 // takes coarse rows [ceil(f0/2), ceil(f1/2)) -- every centre lies inside its own
 // slab and the 5-tap restriction reads at most 2 rows beyond it (the exchanged
 // halo).  Cut rows of the last sharded depth can be odd (P not a power of two).
-static void coarse_slab_of(const LevelOp& f, int rank, int ncy_g, int& row0, int& ny) {
-  const int P = (int)f.slab_row0.size();
-  row0 = (f.slab_row0[rank] + 1) / 2;
-  const int end = rank == P - 1 ? ncy_g : (f.slab_row0[rank + 1] + 1) / 2;
+void gather_rows(const std::vector<int>& fine_slab_row0, int rank, int ncy_g, int& row0, int& ny) {
+  const int P = (int)fine_slab_row0.size();
+  row0 = (fine_slab_row0[rank] + 1) / 2;
+  const int end = rank == P - 1 ? ncy_g : (fine_slab_row0[rank + 1] + 1) / 2;
   ny = end - row0;
+}
+static void coarse_slab_of(const LevelOp& f, int rank, int ncy_g, int& row0, int& ny) {
+  gather_rows(f.slab_row0, rank, ncy_g, row0, ny);
 }
 
 void restrict_levels(const LevelOp& f, const LevelOp& c, const cd* fine, cd* out, cd* slab, int zero_mask) {

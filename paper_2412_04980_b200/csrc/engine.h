@@ -254,6 +254,9 @@ struct SmallSolve {  // device-resident GMRES on one level operator
   ~SmallSolve();
 };
 
+// coarse rows [row0, row0 + ny) a rank restricts (then all-gathers) when a sharded
+// level feeds a replicated one (host rule; exported as hdb_plan_gather_rows)
+void gather_rows(const std::vector<int>& fine_slab_row0, int rank, int ncy_g, int& row0, int& ny);
 // slab-to-slab / slab-to-replicated transfer between two levels
 TGeom level_tgeom(const LevelOp& fine, const LevelOp& coarse);
 // restrict fine (level op f) into coarse buffer `out` of level op c; gathers into

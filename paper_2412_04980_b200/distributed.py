@@ -25,7 +25,7 @@ import numpy as np
 
 from ._lib import check, lib
 
-__all__ = ["SlabPlan", "slab_plan", "DistContext"]
+__all__ = ["SlabPlan", "slab_plan", "gather_rows", "DistContext"]
 
 HALO = 3  # rows carried by vectors of sharded levels (max stencil radius)
 
@@ -91,6 +91,18 @@ def slab_plan(ny: int, ranks: int, max_depth: int, min_rows: int = 32) -> SlabPl
         if ok:
             return plan
     return SlabPlan(ranks, 0, 1, [0, ny], ny)  # nothing sharded: every rank replicates
+
+
+def gather_rows(plan: "SlabPlan", depth: int, rank: int):
+    """(row0, ny): the rows of depth `depth + 1` this rank restricts and all-gathers
+    when `depth` is the last sharded depth -- the library's own rule
+    (hdb_plan_gather_rows; no device needed)."""
+    from ._lib import load_library
+    L = load_library()
+    starts = (C.c_int * plan.ranks)(*[plan.slab(depth, r)[0] for r in range(plan.ranks)])
+    r0, n = C.c_int(), C.c_int()
+    check(L.hdb_plan_gather_rows(starts, plan.ranks, rank, plan.rows_at(depth + 1), C.byref(r0), C.byref(n)))
+    return r0.value, n.value
 
 
 _groups = itertools.count(1)
