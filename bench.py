@@ -176,7 +176,7 @@ def ncu_traffic(family, config):
         e = d["families"][family]
         if d.get("config") != config:
             return None, None
-        return e["traffic_bytes_per_launch"], e.get("alg_bytes_per_launch")
+        return e["traffic_bytes_per_launch"], d.get("source")
     except (OSError, KeyError, ValueError):
         return None, None
 
@@ -309,13 +309,12 @@ def roofline_entry(fams, peak, peak_src, config):
     name = max(hbm, key=lambda k: hbm[k]["ms"])
     v = hbm[name]
     per_launch_bytes = v["alg_MB"] * 1e6 / v["launches"]
-    traffic, ncu_alg = ncu_traffic(name, config)
+    traffic, ncu_src = ncu_traffic(name, config)
     return {"bound": "hbm", "kernel": f"{name}: {FAMILY_KERNELS.get(name, name)}",
             "achieved": v["gbs"], "peak": peak, "unit": "GB/s", "frac": round(v["gbs"] / peak, 4),
             "traffic": traffic,
-            "traffic_source": "profiles/r02_roofline_ncu.json (ncu --set full: dram read+write per launch, "
-                              "mean over the captured launches)" if traffic else None,
-            "traffic_alg_bytes_per_launch": ncu_alg,
+            "traffic_source": (f"profiles/r02_roofline_ncu.json: {ncu_src} (dram read+write, mean per captured "
+                               f"launch)") if traffic else None,
             "peak_source": peak_src, "share_of_solve": v["share"], "launches_per_solve": v["launches"],
             "algorithmic_bytes_per_launch": round(per_launch_bytes), "us_per_launch": round(v["ms"] * 1e3 / v["launches"], 2),
             "how": "one extra solve after the timed steps with a CUDA-event pair on the library stream around "

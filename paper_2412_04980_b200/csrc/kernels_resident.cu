@@ -336,11 +336,18 @@ struct GridSync {
       const int G = kRT / m, t = threadIdx.x, e = t % m, gi = t / m;
       cd q = mkc(0.0, 0.0);
       if (gi < G) {
-#pragma unroll 4
-        for (int r = gi; r < P; r += G) {
-          const cd z = __ldcg(&col[(long long)r * kVecCap + e]);
-          q.x += z.x;
-          q.y += z.y;
+        for (int r0 = gi; r0 < P; r0 += 8 * G) {  // 8 partial loads in flight, then summed in rank order
+          cd z[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int r = r0 + u * G;
+            z[u] = r < P ? __ldcg(&col[(long long)r * kVecCap + e]) : mkc(0.0, 0.0);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            q.x += z[u].x;
+            q.y += z[u].y;
+          }
         }
       }
       s.sub[t] = q;

@@ -55,13 +55,14 @@ def make(config):
         hier = build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=0.5, ml=5, velocity=vel, f=f)
         rhs = point_source_rhs(hier, (300.0, 0.0))
         return hier, rhs.grid_view(hier)
-    if config.startswith("c4_h6_f"):  # BASELINE configs[3] model at h = 6 m, ml = 3 (gridfile raster)
+    if config.startswith("c4_h"):  # BASELINE configs[3] model (gridfile raster): c4_h6_f40 (ml 3), c4_h12_f40 (ml 2)
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
         from paper_2412_04980_b200.models import C4_DOMAIN, C4_SOURCE, synthetic_layered_velocity
+        h = float(config.split("_h")[1].split("_")[0])
         f = float(config.split("_f")[1])
         v = synthetic_layered_velocity(2412, dx=6.0)
         vel = VelocityModel(kind="gridfile", values=v.values, dx=v.dx, dy=v.dy, x0=v.x0, y0=v.y0)
-        hier = build_hierarchy(C4_DOMAIN, h=6.0, ml=3, velocity=vel, f=f)
+        hier = build_hierarchy(C4_DOMAIN, h=h, ml=3 if h == 6.0 else 2, velocity=vel, f=f)
         return hier, point_source_rhs(hier, C4_SOURCE).grid_view(hier)
     raise SystemExit(f"unknown config {config}")
 
