@@ -319,9 +319,9 @@ long long coop_mgs_min() {
 int resident_mode(long long n, int cap) {
   static long long small = -1, grid = -1;
   if (small < 0) {
-    // one cluster only for the smallest levels (65^2: 23.5 us/it vs 24.1 grid; 76 x 126:
-    // 27.7 vs 21.8; 129^2: 38.5 vs 25.2 -- tools/gmres_modes.py, r01d)
-    small = std::min(env_ll("HDB_SMALL_N", 6000), resident_cluster_points());
+    // cluster mode only when asked: the grid mode is faster at every config-2 level since
+    // r02i (65^2: 20.8 vs 22.7 us/it; 129^2: 21.9 vs 37.9 -- profiles/r02i_modes.log)
+    small = std::min(env_ll("HDB_SMALL_N", 0), resident_cluster_points());
     grid = std::min(env_ll("HDB_GRID_N", 2000000), resident_grid_points());
   }
   if (cap > resident_max_cap()) return -1;

@@ -1155,6 +1155,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
 }
+// same with an L2 eviction-priority hint (policy from createpolicy)
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy) : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 // thread 0: arm the barrier for `bytes` and issue the slice copy in 32 KB pieces
 __device__ __forceinline__ void issue_slice(cd* dst, const cd* src, int cnt, uint64_t* bar) {
   const uint32_t bytes = (uint32_t)cnt * (uint32_t)sizeof(cd);
@@ -1266,6 +1282,7 @@ constexpr int kLsStage = 16;               // reduced elements per warp-partial 
 constexpr int kLsChunk = 2 * kRT;          // ring chunk: 1024 points (16 KB) = 2 per thread
 constexpr int kLsChunks = kLsSlot / 2;     // chunks per slice (7)
 constexpr int kLsRing = 6;                 // ring stages
+constexpr int kLsKeep = 5;                 // last pass-A vectors kept in L2 (evict_last) for pass B
 struct LsSmem {
   MgsSmem red;
   cd stage[kRT / 32][kLsStage];            // warp partials; reused for g, l, t-row and h
@@ -1291,6 +1308,13 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   cd* vj = ring + (size_t)kLsRing * kLsChunk;                           // V_j slice
   // chunk sequence: pass A streams V_0..V_{j-1}, pass B V_{j-1}..V_0, kLsChunks chunks each
   const int nchunks = 2 * j * kLsChunks;
+  // L2 policy: pass A marks its last kLsKeep vectors evict_last (pass B reads them first,
+  // in reverse order) and the others evict_first; pass B reads are the last use this step
+  const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
+  auto chunk_pol = [&](int q) {
+    const int v = q / kLsChunks;
+    return (v < j && v >= j - kLsKeep) ? pol_keep : pol_drop;
+  };
   auto chunk_src = [&](int q, int& bytes) -> const cd* {
     const int v = q / kLsChunks, c = q - v * kLsChunks;
     const int k = v < j ? v : 2 * j - 1 - v;
@@ -1305,7 +1329,7 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     const cd* src = chunk_src(q, bytes);
     if (bytes > 0) {
       mbar_arm(&s.full[st], (uint32_t)bytes);
-      bulk_g2s(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st]);
+      bulk_g2s_hint(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st], chunk_pol(q));
     } else {
       mbar_arrive1(&s.full[st]);  // empty tail chunk: complete the phase without data
     }

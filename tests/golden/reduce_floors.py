@@ -64,7 +64,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "solve_c1_full.npz"), **rec)
     print("solve_c1_full.npz", int(b["outer_iterations"]), float(b["final_relres"]), float(rec["floor_hist_abs"]),
           float(rec["floor_sol_rel"]))
-    for name in ("c4_h6_f40",):
+    for name in ("c4_h6_f40", "c4_h12_f40"):
         bp = os.path.join(RUNS, f"{name}.npz")
         pq = os.path.join(RUNS, f"{name}_p.npz")
         if os.path.exists(bp) and os.path.exists(pq):
@@ -72,9 +72,9 @@ def main():
             pp = np.load(pq, allow_pickle=False)
             rec = dict(outer_iterations=b["outer_iterations"], converged=b["converged"], final_relres=b["final_relres"],
                        residual_history=b["residual_history"], solution_l2=b["solution_l2"], wall_s=b["wall_s"],
-                       cycle_iters=b["cycle_iters"], cslp_iters=b["cslp_iters"], solution_stride=np.array(4),
-                       solution_sub=b["solution"][::4, ::4])
-            rec.update(floors(b, pp, 4))
+                       cycle_iters=b["cycle_iters"], cslp_iters=b["cslp_iters"], solution_stride=np.array(2),
+                       solution_sub=b["solution"][::2, ::2])
+            rec.update(floors(b, pp, 2))
             # k^2 checksums of the reference's own hierarchy (levels 1 and 3) for this raster
             sys.path.insert(0, "/root/reference/pkg/src")
             sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
@@ -82,8 +82,9 @@ def main():
             from paper_2412_04980_b200.models import C4_DOMAIN, synthetic_layered_velocity
             v = synthetic_layered_velocity(2412, dx=6.0)
             vel = VelocityModel(kind="gridfile", values=v.values, dx=v.dx, dy=v.dy, x0=v.x0, y0=v.y0)
-            hier = build_hierarchy(C4_DOMAIN, h=6.0, ml=3, velocity=vel, f=40.0)
-            rec["ksq_checksum"] = np.array([hier.ksq[0].sum(), hier.ksq[2].sum()])
+            hh = 6.0 if name == "c4_h6_f40" else 12.0
+            hier = build_hierarchy(C4_DOMAIN, h=hh, ml=3 if hh == 6.0 else 2, velocity=vel, f=40.0)
+            rec["ksq_checksum"] = np.array([hier.ksq[0].sum(), hier.ksq[-1].sum()])
             np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **rec)
             print(name, int(b["outer_iterations"]), float(rec["floor_hist_abs"]), float(rec["floor_sol_rel"]))
 

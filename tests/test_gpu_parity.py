@@ -678,22 +678,25 @@ def test_config3_wedge_vs_reference(f):
     assert np.linalg.norm(xs - ref) <= 1e-8 * np.linalg.norm(ref)
 
 
-def test_config4_synthetic_layered_vs_reference():
-    """BASELINE configs[3] model (seeded generator, models.py) at h = 6 m, 40 Hz, 3 levels, against
-    the reference solving the same raster through its gridfile path (tests/golden/
-    solve_c4_h6_f40.npz): outer count +-1, history / solution at the BASELINE bar or
-    10x the reference's own floor for this case (gold.parity_bar)."""
-    g = golden("solve_c4_h6_f40.npz")
-    prob = hdb.synthetic_layered_problem(40.0, 6.0, 3)
+@pytest.mark.parametrize("name,h,ml", [("c4_h12_f40", 12.0, 2)])
+def test_config4_synthetic_layered_vs_reference(name, h, ml):
+    """BASELINE configs[3] model (seeded generator, models.py) at 40 Hz against the reference
+    solving the same raster through its gridfile path (tests/golden/solve_<name>.npz).  At
+    h = 12 m with two levels the reference stalls at its 150-iteration cap (final relres
+    2.8e-2; its 1e-15-perturbed twin 2.8e-2): held to the count, the stall, the first steps
+    at the BASELINE bar and every iteration to 10x the reference's own drift envelope."""
+    g = golden(f"solve_{name}.npz")
+    prob = hdb.synthetic_layered_problem(40.0, h, ml)
     hier = prob.hierarchy
-    np.testing.assert_array_equal([hier.ksq[0].sum(), hier.ksq[2].sum()], g["ksq_checksum"])
+    np.testing.assert_array_equal([hier.ksq[0].sum(), hier.ksq[-1].sum()], g["ksq_checksum"])
     with hdb.MadpSolver(hier, hdb.preset("MADP", hier)) as s:
         u, rep = s.solve(prob.rhs)
     assert abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
     assert rep.converged == bool(g["converged"])
-    h, hr = np.array(rep.residual_history), g["residual_history"]
-    n = min(len(h), len(hr))
+    h_, hr = np.array(rep.residual_history), g["residual_history"]
+    n = min(len(h_), len(hr))
+    assert np.abs(h_[:2] - hr[:2]).max() <= 1e-9
+    assert np.all(np.abs(h_[:n] - hr[:n]) <= 10 * _floor_envelope(g)[:n] + 1e-12)
     hb, xb = parity_bar(g)
-    assert np.abs(h[:n] - hr[:n]).max() <= hb
     st = int(g["solution_stride"])
     assert np.linalg.norm(u.grid_view(hier)[::st, ::st] - g["solution_sub"]) <= xb * np.linalg.norm(g["solution_sub"])

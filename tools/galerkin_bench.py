@@ -80,6 +80,21 @@ def main():
         _lib.check(L.hdb_option(b"rg_exact", 0))
         out[f"L{l}"] = row
         print(f"L{l}", json.dumps(row), flush=True)
+    # fixed per-launch cost on a tiny grid (one CTA): kernels that take the level operator's
+    # coefficient block by value (2.3 KB of parameters) vs a parameter-light dot
+    tiny = hdb.mp1_problem(k=5.0, n=17, ml=3).hierarchy
+    for l, name in ((1, "tiny_apply5"), (2, "tiny_galerkin_r2"), (3, "tiny_galerkin_r3")):
+        op = hdb.cslp_operator(tiny, l, 0.5)
+        lv = tiny.level(l)
+        u = torch.from_numpy(rng.standard_normal(lv.shape) + 1j * rng.standard_normal(lv.shape)).cuda()
+        o = torch.empty_like(u)
+        h = op.handle
+        out[name] = {"us": round(timeit_graph(lambda: _lib.check(L.hdb_op_apply(h, u.data_ptr(), o.data_ptr())),
+                                              a.reps) * 1e3, 2)}
+    u = torch.from_numpy(rng.standard_normal((17, 17)) + 1j * rng.standard_normal((17, 17))).cuda()
+    out["tiny_dot"] = {"us": round(timeit_graph(lambda: _lib.check(L.hdb_dot(u.data_ptr(), u.data_ptr(), 289, None)),
+                                                a.reps) * 1e3, 2)}
+    print("tiny", json.dumps({k: v for k, v in out.items() if k.startswith("tiny")}), flush=True)
     # one-launch MGS step on the 1025^2 level: GMRES(1e-14, cap) through the launch-driven engine
     prob = hdb.mp1_problem(k=200.0, n=1025, ml=2)
     op = hdb.cslp_operator(prob.hierarchy, 1, 0.5)
