@@ -281,6 +281,8 @@ KWS::~KWS() {
   E.free(dV);
   E.free(gpart);
   E.free(tg);
+  E.free(tgh);
+  E.free(lpart);
   for (auto p : V) E.free_h(p, halo);
   for (auto p : Z) E.free_h(p, halo);
   E.free_h(tmp, halo);
@@ -308,6 +310,14 @@ bool step1_enabled() {
   static int v = -1;
   if (v < 0) v = (int)env_ll("HDB_STEP1", 1);
   return v != 0;
+}
+
+// levels from this many points (and not sharded) take the HBM-streaming low-sync
+// MGS step when the one-launch forms do not fit (HDB_LSH_N; 0 disables)
+static long long lsh_min() {
+  static long long v = -1;
+  if (v < 0) v = env_ll("HDB_LSH_N", 1LL << 20);
+  return v > 0 ? v : (1LL << 62);
 }
 
 long long coop_mgs_min() {
@@ -435,7 +445,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   g.push_back(cplx(beta, 0.0));
   int its = 0;
   bool conv = false;
-  bool ls_ok = true;
+  bool ls_ok = true, lsh_ok = true;
   for (int j = 0; j < stop.max_iters; ++j) {
     const cd* z = ws.v(j);
     if (M) {
@@ -480,16 +490,41 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
         E.kp.bytes[KF_MGS_COOP] -= (16.0 * (j + 1) + 32.0) * n;
       }
     }
-    if (!coop) {
+    // large unsharded levels: the low-synchronisation step as HBM streaming passes (every
+    // step of this Arnoldi process must use it: the T rows accumulate)
+    // sharded levels take it at any size: two all-reduces per Arnoldi step (the (2j+1)
+    // coefficient sums and ||w||^2) instead of one per MGS coefficient
+    bool lsh = false;
+    if (!coop && (shard || n >= lsh_min()) && mgs_ls_on() && (j == 0 || lsh_ok) && stop.max_iters <= 511) {
+      if (ws.tgh_cap < stop.max_iters) {
+        E.free(ws.tgh);
+        E.free(ws.lpart);
+        ws.tgh = E.alloc((long long)(stop.max_iters + 1) * (stop.max_iters + 2) / 2);
+        ws.lpart = E.alloc(lsh_part_elems(n, stop.max_iters));
+        ws.tgh_cap = stop.max_iters;
+      }
+      ensure_dv();
+      const int nl = (j == 0 ? 1 : (j + 7) / 8) + (j + 8) / 8 + 2;
+      int rc = 0;
+      std::function<void(cd*, int)> allred;
+      if (shard) allred = [&](cd* v, int m) { E.comm->allreduce((double*)v, 2 * m, E.st); };
+      E.kl(KF_MGS_CHAIN, (16.0 * (j + 1) + 32.0) * n, [&] {
+        rc = launch_mgs_lsh(w, (const cd* const*)ws.dV, ws.V.data(), j, n, ws.lpart, ws.tgh, E.dscal + kSlotH, E.st,
+                            allred);
+      }, nl);
+      lsh = rc == 0;
+    }
+    lsh_ok = lsh;
+    if (!coop && !lsh) {  // the fused MGS chain (algorithmic bytes booked: w + V_0, then each V_i, w out)
       E.kl(KF_MGS_CHAIN, 32.0 * n, [&] { launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st); });
       red(E.dscal + kSlotH);
       for (int i = 0; i < j; ++i) {
-        E.kl(KF_MGS_CHAIN, 64.0 * n, [&] {
+        E.kl(KF_MGS_CHAIN, 16.0 * n, [&] {
           launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
         });
         red(E.dscal + kSlotH + i + 1);
       }
-      E.kl(KF_MGS_CHAIN, 48.0 * n, [&] {
+      E.kl(KF_MGS_CHAIN, 16.0 * n, [&] {
         launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
       });
       red(E.dscal + kSlotH + j + 1);
@@ -686,7 +721,7 @@ void fgmres_step1(long long n, const LinOp& A, const LinOp& M, const cd* b, cd* 
   A(ws.z(0), w);
   E.kl(KF_MGS_CHAIN, 32.0 * n, [&] { launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, S + kS1H0, E.st); });
   red(kS1H0);
-  E.kl(KF_MGS_CHAIN, 48.0 * n, [&] { launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st); });
+  E.kl(KF_MGS_CHAIN, 16.0 * n, [&] { launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st); });
   red(kS1HN);
   E.kl(KF_CONTROL, 0.0, [&] { launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st); });
   ws.hbasis[0] = ws.z(0);

@@ -183,6 +183,9 @@ struct KWS {
   int dV_cap = 0, dV_n = 0;
   cd* gpart = nullptr;     // grid-reduction partials
   cd* tg = nullptr;        // T = (I + L)^{-1} rows of the low-synchronisation MGS (mgs_ls_tg_elems())
+  cd* tgh = nullptr;       // the same for the HBM-streaming form (cap + 1)(cap + 2) / 2
+  cd* lpart = nullptr;     // its block partials (lsh_part_elems)
+  int tgh_cap = 0;
   cd* tmp = nullptr;
   cd** dbasis = nullptr;   // device pointer table for the solution update
   cd* dy = nullptr;

@@ -1,5 +1,6 @@
 // Kernel launchers (internal C++ interface between the engine and the .cu files).
 #pragma once
+#include <functional>
 #include "hdb_common.cuh"
 
 namespace hdb {
@@ -61,6 +62,14 @@ void resident_set_profile(long long* dev_counters);
 int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
                     const int* skip = nullptr, cd* tg = nullptr);
 bool mgs_ls_fits(long long n, int j);
+// the same low-synchronisation step as streaming passes over HBM (w too large for
+// the one-launch form): Vtab device pointer table, Vhost the same pointers on the
+// host; part >= lsh_part_elems(n, j) elements; Tg (cap+1)(cap+2)/2; 1 = j too large
+long long lsh_part_elems(long long n, int maxj);
+// allreduce (may be empty): sums a device vector over the ranks of a sharded level, in place
+int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, long long n, cd* part, cd* Tg,
+                   cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce);
+bool mgs_ls_on();
 void set_mgs_ls(int on);
 void set_rg_exact(int on);
 bool rg_exact_on();    // separable K2 kernel: 0 tile form, 1 column-marching form (default)  // 1: radius-2/3 levels use the reference's exact tap order (HDB_RG_EXACT=1)  // runtime switch (HDB_MGS_LS=0 at start-up does the same)

@@ -6,6 +6,8 @@
 // ticket) sums them in a fixed order and writes the scalar to device memory.
 // Nothing returns to the host here; the Krylov driver reads the Hessenberg
 // column once per Arnoldi step.
+#include <functional>
+
 #include "kernels.h"
 #include "hdb_common.cuh"
 #include "reduce.cuh"
@@ -177,6 +179,208 @@ static inline int ew_blocks(long long n) {
   long long b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
   return (int)(b < 1 ? 1 : b);
+}
+
+// ---------------------------------------------------------------------------
+// Low-synchronisation MGS step for levels whose w does not fit on chip (the fine
+// level of config 2: 16.8M points): the same algorithm as k_mgs_ls (h = (I + L)^{-1}
+// V^H w, T = (I + L)^{-1} rows kept across the Arnoldi steps) as streaming passes
+// over HBM instead of the fused MGS chain's j + 2 launches of 64 B/pt:
+//   pass A  groups of kLsG basis vectors: g_k = <V_k, w>, l_k = <V_j, V_k>, and
+//           <V_j, w> with the first group -> per-block partials;
+//   finish  one block: ordered sum of the partials, the new T row, h = T g;
+//   pass B  groups: w -= h_j V_j, then h_k V_k for k = j-1 .. 0; the last group
+//           also forms the per-block partials of ||w||^2;
+//   norm    one block: ordered sum -> hout[j + 1].
+// At Arnoldi step j it moves (ceil(j/8) + ceil((j+1)/8)) 32 + 2 (j+1) 16 B/pt instead of
+// (j+2) 64: 640 vs 1024 B/pt at j = 14.
+constexpr int kLsG = 8;
+constexpr int kLsPE = 2 * kLsG + 1;  // partial elements per block per group
+
+__global__ void __launch_bounds__(kReduceThreads, 2) k_lsh_a(const cd* __restrict__ w, const cd* __restrict__ vj,
+                                                          const cd* const* V, int k0, int kn, int with_gj,
+                                                          long long n, cd* part) {
+  cd g[kLsG], l[kLsG], gj = mkc(0.0, 0.0);
+  const cd* vk[kLsG];
+#pragma unroll
+  for (int u = 0; u < kLsG; ++u) {
+    g[u] = mkc(0.0, 0.0);
+    l[u] = mkc(0.0, 0.0);
+    vk[u] = u < kn ? V[k0 + u] : nullptr;
+  }
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    const cd wv = w[p], vv = vj[p];
+    cd r[kLsG];
+#pragma unroll
+    for (int u = 0; u < kLsG; ++u) r[u] = u < kn ? vk[u][p] : mkc(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kLsG; ++u) {
+      if (u < kn) {
+        g[u] = c_conjmul_acc(g[u], r[u], wv);
+        l[u] = c_conjmul_acc(l[u], vv, r[u]);
+      }
+    }
+    if (with_gj) gj = c_conjmul_acc(gj, vv, wv);
+  }
+  cd* out = part + (long long)blockIdx.x * kLsPE;
+#pragma unroll
+  for (int u = 0; u < kLsG; ++u) {
+    if (u < kn) {  // kn is grid-uniform: every thread takes part in the block sums
+      const cd a = block_sum(g[u]);
+      const cd b = block_sum(l[u]);
+      if (threadIdx.x == 0) { out[u] = a; out[kLsG + u] = b; }
+    }
+  }
+  if (with_gj) {
+    const cd a = block_sum(gj);
+    if (threadIdx.x == 0) out[2 * kLsG] = a;
+  }
+}
+
+__device__ __forceinline__ void cfma_(cd& a, cd x, cd y) {  // a += x * y
+  a.x = __fma_rn(x.x, y.x, a.x); a.x = __fma_rn(-x.y, y.y, a.x);
+  a.y = __fma_rn(x.x, y.y, a.y); a.y = __fma_rn(x.y, y.x, a.y);
+}
+
+// ordered sum of the block partials -> sums[0 .. 2j] (g_0..g_j, l_0..l_{j-1}); one block
+// of 1024 threads; part: [group][block][kLsPE].  A sharded level all-reduces `sums`
+// (one collective per Arnoldi step) before k_lsh_th.
+constexpr int kLshF = 1024;
+__global__ void __launch_bounds__(kLshF) k_lsh_sum(const cd* part, int nblocks, int j, cd* sums) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int ne = 2 * j + 1;
+  for (int e = wid; e < ne; e += kLshF / 32) {
+    // element e -> (group, slot): g_k and l_k live in group k / kLsG; g_j in group 0's extra slot
+    int grp, slot;
+    if (e < j) { grp = e / kLsG; slot = e % kLsG; }
+    else if (e == j) { grp = 0; slot = 2 * kLsG; }
+    else { const int k = e - j - 1; grp = k / kLsG; slot = kLsG + k % kLsG; }
+    const cd* src = part + (long long)grp * nblocks * kLsPE + slot;
+    cd a = mkc(0.0, 0.0);
+    for (int b0 = lane; b0 < nblocks; b0 += 32 * 8) {  // 8 loads in flight per lane, block order per lane
+      cd z[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b = b0 + 32 * u;
+        z[u] = b < nblocks ? src[(long long)b * kLsPE] : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { a.x += z[u].x; a.y += z[u].y; }
+    }
+    a = warp_sum(a);
+    if (lane == 0) sums[e] = a;
+  }
+}
+
+// the new T row and h = T g from the reduced sums (every rank identically)
+__global__ void __launch_bounds__(kLshF) k_lsh_th(const cd* sums, int j, cd* Tg, cd* hout) {
+  __shared__ cd tot[2 * 512 + 1];
+  __shared__ cd trow[512];
+  const int t = threadIdx.x;
+  for (int e = t; e < 2 * j + 1; e += kLshF) tot[e] = sums[e];
+  __syncthreads();
+  const long long rj = (long long)j * (j + 1) / 2;
+  if (t < j) {  // t_jk = -sum_{m=k}^{j-1} l_m T_mk
+    cd a = mkc(0.0, 0.0);
+    for (int m0 = t; m0 < j; m0 += 8) {
+      cd tm[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tm[u] = m0 + u < j ? Tg[(long long)(m0 + u) * (m0 + u + 1) / 2 + t] : mkc(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (m0 + u < j) cfma_(a, tot[j + 1 + m0 + u], tm[u]);
+    }
+    trow[t] = mkc(-a.x, -a.y);
+    Tg[rj + t] = trow[t];
+  }
+  if (t == 0) Tg[rj + j] = mkc(1.0, 0.0);
+  __syncthreads();
+  if (t <= j) {  // h_i = sum_{k <= i} T_ik g_k
+    cd a = mkc(0.0, 0.0);
+    const long long ri = (long long)t * (t + 1) / 2;
+    for (int k0 = 0; k0 <= t; k0 += 8) {
+      cd tk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u;
+        tk[u] = k > t ? mkc(0.0, 0.0) : (t < j ? (k < t ? Tg[ri + k] : mkc(1.0, 0.0)) : (k < j ? trow[k] : mkc(1.0, 0.0)));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (k0 + u <= t) cfma_(a, tk[u], tot[k0 + u]);
+    }
+    hout[t] = a;
+  }
+}
+
+// w -= h_k V_k for k = kfirst, kfirst-1, ..., kfirst-kn+1 (descending); norm != 0: per-block ||w||^2
+__global__ void __launch_bounds__(kReduceThreads) k_lsh_b(cd* __restrict__ w, const cd* const* V, const cd* h,
+                                                          int kfirst, int kn, int norm, long long n, cd* part) {
+  cd hk[kLsG];
+  const cd* vk[kLsG];
+#pragma unroll
+  for (int u = 0; u < kLsG; ++u) {
+    hk[u] = u < kn ? h[kfirst - u] : mkc(0.0, 0.0);
+    vk[u] = u < kn ? V[kfirst - u] : nullptr;
+  }
+  cd acc = mkc(0.0, 0.0);
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
+    cd x = w[p];
+    cd r[kLsG];
+#pragma unroll
+    for (int u = 0; u < kLsG; ++u) r[u] = u < kn ? vk[u][p] : mkc(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < kLsG; ++u)
+      if (u < kn) x = c_sub(x, c_mul_np(hk[u], r[u]));
+    w[p] = x;
+    if (norm) acc = c_conjmul_acc(acc, x, x);
+  }
+  if (norm) {
+    const cd a = block_sum(acc);
+    if (threadIdx.x == 0) part[blockIdx.x] = a;
+  }
+}
+
+__global__ void __launch_bounds__(kReduceThreads) k_lsh_norm(const cd* part, int nblocks, cd* dst) {
+  cd v = mkc(0.0, 0.0);
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) { v.x += part[b].x; v.y += part[b].y; }
+  v = block_sum(v);
+  if (threadIdx.x == 0) *dst = v;
+}
+
+// buffer layout: [0, 1024) reduced sums (2j + 1 <= 1023), [1024, 1024 + G) norm partials,
+// then one region of G * kLsPE block partials per pass-A group
+constexpr int kLshSums = 1024;
+long long lsh_part_elems(long long n, int maxj) {
+  const long long G = reduce_blocks(n);
+  return kLshSums + G + (long long)((maxj + kLsG) / kLsG + 1) * G * kLsPE;
+}
+
+int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, long long n, cd* part, cd* Tg,
+                   cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce) {
+  if (j > 511) return 1;
+  const int G = reduce_blocks(n);
+  cd* sums = part;
+  cd* npart = part + kLshSums;
+  cd* apart = npart + G;
+  // pass A (the first group also carries <V_j, w>; with j = 0 it carries only that)
+  const int ga = j == 0 ? 1 : (j + kLsG - 1) / kLsG;
+  for (int q = 0; q < ga; ++q) {
+    const int k0 = q * kLsG, kn = j - k0 < kLsG ? j - k0 : kLsG;
+    k_lsh_a<<<G, kReduceThreads, 0, st>>>(w, Vhost[j], Vtab, k0, kn > 0 ? kn : 0, q == 0, n,
+                                          apart + (long long)q * G * kLsPE);
+  }
+  k_lsh_sum<<<1, kLshF, 0, st>>>(apart, G, j, sums);
+  if (allreduce) allreduce(sums, 2 * j + 1);
+  k_lsh_th<<<1, kLshF, 0, st>>>(sums, j, Tg, hout);
+  const int gb = (j + 1 + kLsG - 1) / kLsG;
+  for (int q = 0; q < gb; ++q) {
+    const int kfirst = j - q * kLsG, kn = kfirst + 1 < kLsG ? kfirst + 1 : kLsG;
+    k_lsh_b<<<G, kReduceThreads, 0, st>>>(w, Vtab, hout, kfirst, kn, q == gb - 1, n, npart);
+  }
+  k_lsh_norm<<<1, kReduceThreads, 0, st>>>(npart, G, hout + j + 1);
+  if (allreduce) allreduce(hout + j + 1, 1);
+  return 0;
 }
 
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st) {

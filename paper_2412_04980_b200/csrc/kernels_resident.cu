@@ -1599,6 +1599,8 @@ bool mgs_grid_fits(long long n) {
   return mgs_grid_plan(n, ks) != 0;
 }
 
+bool mgs_ls_on() { return mgs_ls_enabled(); }
+
 bool mgs_ls_fits(long long n, int j) {
   init_limits();
   const long long chunk = (n + g_grid - 1) / g_grid;

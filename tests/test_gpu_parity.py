@@ -552,6 +552,40 @@ def test_lowsync_mgs_step_matches_mgs_order():
     assert np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
 
 
+def test_lowsync_hbm_streaming_step_matches_mgs_chain():
+    """The HBM-streaming low-synchronisation MGS step (levels whose w does not fit on
+    chip; forced here on a 1025^2 level by disabling the one-launch forms) against
+    the fused MGS chain (HDB_LSH_N=0) and the oracle: GMRES(1e-8, 40) on a CSLP level."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys,json; sys.path.insert(0,'.'); import numpy as np, paper_2412_04980_b200 as h;"
+            "p=h.mp1_problem(k=100.0,n=1025,ml=3); op=h.cslp_operator(p.hierarchy,1,0.5);"
+            "rng=np.random.default_rng(5); b=rng.standard_normal(op.shape)+1j*rng.standard_normal(op.shape);"
+            "x,r=h.fgmres(op.apply,None,b,h.StopRule(1e-8,40)); np.save(sys.argv[1],x);"
+            "print(json.dumps([r.iterations,r.residual_history,r.final_relres]))")
+    outs = []
+    for i, env in enumerate(({"HDB_COOP_MGS_N": "1000000000000"},
+                             {"HDB_COOP_MGS_N": "1000000000000", "HDB_LSH_N": "0"})):
+        path = f"/tmp/hdb_lsh_{i}.npy"
+        r = subprocess.run([sys.executable, "-c", code, path], capture_output=True, text=True,
+                           env=dict(os.environ, **env), cwd=ROOT_DIR)
+        assert r.returncode == 0, r.stderr
+        its, hist, fin = json.loads(r.stdout.strip().splitlines()[-1])
+        outs.append((its, np.array(hist), fin, np.load(path)))
+    (i0, h0, f0, x0), (i1, h1, f1, x1) = outs
+    assert i0 == i1
+    assert np.abs(h0 - h1).max() <= 1e-12
+    assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x1)
+    oop = oracle.cslp_op(oracle.mp1_problem(100.0, 1025, 3)[0], 1, 0.5)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(oop.shape) + 1j * rng.standard_normal(oop.shape)
+    xo, repo = oracle.fgmres(oop.apply, None, b, oracle.Stop(1e-8, 40), dot=oracle.reduce_dot)
+    assert i0 == repo.iterations
+    assert np.abs(h0 - np.array(repo.residual_history)).max() <= 1e-12
+    assert np.linalg.norm(x0 - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
 ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 
 
