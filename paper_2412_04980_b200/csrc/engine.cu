@@ -298,10 +298,11 @@ static long long env_ll(const char* name, long long dflt) {
 int resident_ortho() {
   static int o = -1;
   if (o < 0) {
-    // dgks (default): CGS + DGKS re-orthogonalisation; cgs2: always two passes; mgs: the reference's order
+    // dgks (default): CGS + DGKS re-orthogonalisation; cgs2: always two passes; ls: the
+    // low-synchronisation MGS; mgs: the reference's order
     const char* e = getenv("HDB_ORTHO");
     const std::string v = e ? e : "dgks";
-    o = v == "mgs" ? 0 : (v == "cgs2" ? 1 : 2);
+    o = v == "mgs" ? 0 : (v == "cgs2" ? 1 : (v == "ls" ? 3 : 2));
   }
   return o;
 }
@@ -349,7 +350,7 @@ void SmallSolve::ensure(const LevelOp* o, int cap_) {
   op = o;
   cap = cap_;
   basis = E.alloc((long long)(cap + 1) * o->n);
-  Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap);
+  Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap + (long long)(cap + 1) * (cap + 2) / 2);
   gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
 }
 

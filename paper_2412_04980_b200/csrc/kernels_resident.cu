@@ -42,7 +42,8 @@ struct ResidentArgs {
   const cd* b;
   cd* x;
   cd* basis;          // (cap + 1) vectors of n points
-  cd* Rg;             // packed upper-triangular R (cap*(cap+1)/2) + y (cap), written by rank 0
+  cd* Rg;             // packed upper-triangular R (cap*(cap+1)/2) + y (cap), written by rank 0;
+                      // then (cap+1)(cap+2)/2 rows of T = (I + L)^{-1} (ORTHO 3)
   cd* gpart;          // GridSync: 2 * nranks partials
   long long n;
   double tol;
@@ -479,6 +480,97 @@ __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long 
   ph(8);
 }
 
+// Low-synchronisation MGS (one-reduce MGS, the k_mgs_ls algorithm) on this CTA's
+// slice: one reduction carries g = V^H w and the new row of L (<V_j, V_k>, k < j);
+// every CTA forms the new row of T = (I + L)^{-1} (rank 0 stores it in Tg) and
+// h = T g into s.hcol; then w -= h_k V_k (V_j first, then k = j-1 .. 0).  The caller
+// forms ||w||^2 with one more reduction.
+template <class Sync>
+__device__ void ls_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n, long long p0, int cnt, int j,
+                        int& buf, cd* gpart, cd* Tg, int rank) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, t = threadIdx.x;
+  constexpr int NW = kRT / 32;
+  const cd* vj = basis + (long long)j * n + p0;
+  for (int i = wid; i <= j; i += NW) {  // warp per basis vector: g_i and (i < j) l_i
+    const cd* vi = basis + (long long)i * n + p0;
+    cd a = mkc(0.0, 0.0), l = mkc(0.0, 0.0);
+#pragma unroll 4
+    for (int q = lane; q < cnt; q += 32) {
+      const cd v = vi[q];
+      a = c_conjmul_acc(a, v, ws[q]);
+      if (i < j) l = c_conjmul_acc(l, vj[q], v);
+    }
+    a = warp_sum_c(a);
+    l = warp_sum_c(l);
+    if (lane == 0) {
+      s.pv[i] = a;
+      if (i < j) s.pv[j + 1 + i] = l;
+    }
+  }
+  __syncthreads();
+  sy.reduce_vec(s, 2 * j + 1, s.hv, buf, gpart);  // hv: g_0..g_j, l_0..l_{j-1}
+  cd* trow = s.sub;
+  const long long rj = (long long)j * (j + 1) / 2;
+  for (int k = t; k < j; k += kRT) {  // t_jk = -sum_{m=k}^{j-1} l_m T_mk
+    cd a = mkc(0.0, 0.0);
+    for (int m0 = k; m0 < j; m0 += 8) {
+      cd tm[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tm[u] = m0 + u < j ? __ldcg(&Tg[(long long)(m0 + u) * (m0 + u + 1) / 2 + k]) : mkc(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (m0 + u < j) {
+          const cd lm = s.hv[j + 1 + m0 + u];
+          a.x = __fma_rn(lm.x, tm[u].x, a.x); a.x = __fma_rn(-lm.y, tm[u].y, a.x);
+          a.y = __fma_rn(lm.x, tm[u].y, a.y); a.y = __fma_rn(lm.y, tm[u].x, a.y);
+        }
+      }
+    }
+    trow[k] = mkc(-a.x, -a.y);
+    if (rank == 0) Tg[rj + k] = trow[k];
+  }
+  if (rank == 0 && t == 0) Tg[rj + j] = mkc(1.0, 0.0);
+  __syncthreads();
+  for (int i = t; i <= j; i += kRT) {  // h_i = sum_{k <= i} T_ik g_k
+    cd a = mkc(0.0, 0.0);
+    const long long ri = (long long)i * (i + 1) / 2;
+    for (int k0 = 0; k0 <= i; k0 += 8) {
+      cd tk[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u;
+        tk[u] = k > i ? mkc(0.0, 0.0) : (i < j ? (k < i ? __ldcg(&Tg[ri + k]) : mkc(1.0, 0.0))
+                                                : (k < j ? trow[k] : mkc(1.0, 0.0)));
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k0 + u <= i) {
+          const cd gk = s.hv[k0 + u];
+          a.x = __fma_rn(tk[u].x, gk.x, a.x); a.x = __fma_rn(-tk[u].y, gk.y, a.x);
+          a.y = __fma_rn(tk[u].x, gk.y, a.y); a.y = __fma_rn(tk[u].y, gk.x, a.y);
+        }
+      }
+    }
+    s.hcol[i] = a;
+  }
+  __syncthreads();
+  for (int q = t; q < cnt; q += kRT) {  // w -= h_j V_j, then h_k V_k for k = j-1 .. 0
+    cd w = ws[q];
+    const cd* vq = basis + p0 + q;
+    int i = j;
+    for (; i >= 7; i -= 8) {  // 8 loads in flight, then the dependent updates in order
+      cd v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i - u) * n];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) w = c_sub(w, c_mul_np(s.hcol[i - u], v[u]));
+    }
+    for (; i >= 0; --i) w = c_sub(w, c_mul_np(s.hcol[i], vq[(long long)i * n]));
+    ws[q] = w;
+  }
+  __syncthreads();
+}
+
 template <class Sync, int R, int ORTHO>
 __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -636,6 +728,9 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
         if (t == 0) s.hcol[i] = h;
         for (int q = t; q < cnt; q += kRT) ws[q] = c_sub(ws[q], c_mul_np(h, vi[q]));
       }
+    } else if (ORTHO == 3) {
+      __syncthreads();
+      ls_pass(sy, s, ws, A.basis, n, p0, cnt, j, buf, A.gpart, Rg + (long long)A.cap * (A.cap + 1) / 2 + A.cap, rank);
     } else if (ORTHO == 1) {
       // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
       // Hessenberg column in exact arithmetic, two reductions instead of j+1
@@ -917,8 +1012,10 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
   a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
   if (ortho == 1 && cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
+  if (ortho == 3 && 2 * cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 2;
   if (ortho == 2 && cap + 2 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
-  const bool ok = ortho == 2 ? launch_any<2>(mode, a, c.radius, st)
+  const bool ok = ortho == 3   ? launch_any<3>(mode, a, c.radius, st)
+                  : ortho == 2 ? launch_any<2>(mode, a, c.radius, st)
                   : ortho == 1 ? launch_any<1>(mode, a, c.radius, st) : launch_any<0>(mode, a, c.radius, st);
   return ok ? 0 : 1;
 }

@@ -617,169 +617,148 @@ __global__ void __launch_bounds__(256, 2) k_rgs(const cd* __restrict__ u, const 
   if (c.skip && *c.skip) return;
   using T = GSTile<R>;
   constexpr int N = 2 * R + 1, TR = T::TR, TC = T::TC, PC = T::PC, W = 4 + 2 * R;
-  constexpr int NL = (TR * TC + 255) / 256;
   extern __shared__ __align__(16) unsigned char gsm[];
   cd* su = reinterpret_cast<cd*>(gsm);
   double* sk = reinterpret_cast<double*>(gsm + T::u_bytes);
   cd* hm = reinterpret_cast<cd*>(gsm + T::u_bytes + T::k_bytes);  // (M u) rows
   cd* ha = hm + TR * GS_T;                                        // (A u) rows
   cd* hk = ha + TR * GS_T;                                        // (M (k u)) rows
+  const int i0 = blockIdx.x * GS_T, j0 = blockIdx.y * GS_T;
+  const bool fast = c.uniform && i0 >= R && i0 + GS_T + R <= g.nx && g.row0 + j0 >= R &&
+                    g.row0 + j0 + GS_T + R <= g.nyg;
   const int tid = threadIdx.x;
-  const int ntx = (g.nx + GS_T - 1) / GS_T, ntiles = ntx * ((g.ny + GS_T - 1) / GS_T);
-  // persistent over tiles: the samples of the NEXT interior (uniform, ghost-free) tile are
-  // loaded into registers while this tile's row sums and outputs are computed
-  auto fast_of = [&](int tile) {
-    const int i0 = (tile % ntx) * GS_T, j0 = (tile / ntx) * GS_T;
-    return c.uniform && i0 >= R && i0 + GS_T + R <= g.nx && g.row0 + j0 >= R && g.row0 + j0 + GS_T + R <= g.nyg;
-  };
-  cd pre[NL];
-  auto prefetch = [&](int tile) {
-    const int i0 = (tile % ntx) * GS_T, j0 = (tile / ntx) * GS_T;
+  constexpr int NL = (TR * TC + 255) / 256;
+  if (fast) {  // interior tile: every sample in range, all NL loads in flight before the stores
+    cd v[NL];
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       const int t = tid + l * 256;
       const int ty = t / TC, tx = t - ty * TC;
-      pre[l] = t < TR * TC ? U(u, g, g.row0 + j0 + ty - R, i0 + tx - R) : mkc(0.0, 0.0);
+      v[l] = t < TR * TC ? U(u, g, g.row0 + j0 + ty - R, i0 + tx - R) : mkc(0.0, 0.0);
     }
-  };
-  int tile = blockIdx.x;
-  bool pre_fast = tile < ntiles && fast_of(tile);
-  if (pre_fast) prefetch(tile);
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int i0 = (tile % ntx) * GS_T, j0 = (tile / ntx) * GS_T;
-    const bool fast = pre_fast;
-    if (fast) {
 #pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        const int t = tid + l * 256;
-        const int ty = t / TC, tx = t - ty * TC;
-        if (t < TR * TC) su[ty * PC + gskew(tx)] = pre[l];
-      }
-    } else {
-      for (int t = tid; t < TR * TC; t += 256) {
-        const int ty = t / TC, tx = t - ty * TC;
-        const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
-        const int si = ty * PC + gskew(tx);
-        su[si] = upad(u, k, g, c, gj, gi);
-        sk[si] = kpad(k, g, c, gj, gi);
-      }
+    for (int l = 0; l < NL; ++l) {
+      const int t = tid + l * 256;
+      const int ty = t / TC, tx = t - ty * TC;
+      if (t < TR * TC) su[ty * PC + gskew(tx)] = v[l];
     }
-    __syncthreads();
-    {
-      const int nt = tile + gridDim.x;
-      pre_fast = nt < ntiles && fast_of(nt);
-      if (pre_fast) prefetch(nt);
+  } else {
+    for (int t = tid; t < TR * TC; t += 256) {
+      const int ty = t / TC, tx = t - ty * TC;
+      const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
+      const int si = ty * PC + gskew(tx);
+      su[si] = upad(u, k, g, c, gj, gi);
+      sk[si] = kpad(k, g, c, gj, gi);
     }
-    // horizontal pass: item = (tile row r, column group xg of 4)
-    for (int it = tid; it < TR * (GS_T / 4); it += 256) {
-      const int r = it >> 3, x0 = (it & 7) * 4;
-      const cd* row = su + r * PC;
-      cd uv[W];
+  }
+  __syncthreads();
+  // horizontal pass: item = (tile row r, column group xg of 4)
+  for (int it = tid; it < TR * (GS_T / 4); it += 256) {
+    const int r = it >> 3, x0 = (it & 7) * 4;
+    const cd* row = su + r * PC;
+    cd uv[W];
 #pragma unroll
-      for (int q = 0; q < W; ++q) uv[q] = row[gskew(x0 + q)];
-      cd am[4], aa[4];
+    for (int q = 0; q < W; ++q) uv[q] = row[gskew(x0 + q)];
+    cd am[4], aa[4];
 #pragma unroll
-      for (int o = 0; o < 4; ++o) { am[o] = mkc(0.0, 0.0); aa[o] = mkc(0.0, 0.0); }
+    for (int o = 0; o < 4; ++o) { am[o] = mkc(0.0, 0.0); aa[o] = mkc(0.0, 0.0); }
 #pragma unroll
-      for (int bb = 0; bb < N; ++bb) {
-        const double mb = c.sm[bb], ab = c.sa[bb];
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-          const cd v = uv[o + bb];
-          am[o].x = fma(mb, v.x, am[o].x); am[o].y = fma(mb, v.y, am[o].y);
-          aa[o].x = fma(ab, v.x, aa[o].x); aa[o].y = fma(ab, v.y, aa[o].y);
-        }
-      }
+    for (int bb = 0; bb < N; ++bb) {
+      const double mb = c.sm[bb], ab = c.sa[bb];
 #pragma unroll
       for (int o = 0; o < 4; ++o) {
-        hm[r * GS_T + x0 + o] = am[o];
-        ha[r * GS_T + x0 + o] = aa[o];
-      }
-      if (!fast) {
-        const double* krow = sk + r * PC;
-        cd ak[4];
-#pragma unroll
-        for (int o = 0; o < 4; ++o) ak[o] = mkc(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < W; ++q) {
-          const double kq = krow[gskew(x0 + q)];
-          const cd ku = mkc(kq * uv[q].x, kq * uv[q].y);
-#pragma unroll
-          for (int o = 0; o < 4; ++o) {
-            const int bb = q - o;
-            if (bb >= 0 && bb < N) {
-              ak[o].x = fma(c.sm[bb], ku.x, ak[o].x);
-              ak[o].y = fma(c.sm[bb], ku.y, ak[o].y);
-            }
-          }
-        }
-#pragma unroll
-        for (int o = 0; o < 4; ++o) hk[r * GS_T + x0 + o] = ak[o];
+        const cd v = uv[o + bb];
+        am[o].x = fma(mb, v.x, am[o].x); am[o].y = fma(mb, v.y, am[o].y);
+        aa[o].x = fma(ab, v.x, aa[o].x); aa[o].y = fma(ab, v.y, aa[o].y);
       }
     }
-    __syncthreads();
-    // vertical pass: thread = (column x, row group y0 of 4)
-    const int x = tid & 31, y0 = (tid >> 5) * 4;
-    cd lm[4], lk[4];
 #pragma unroll
-    for (int o = 0; o < 4; ++o) { lm[o] = mkc(0.0, 0.0); lk[o] = mkc(0.0, 0.0); }
-    {
-      cd w[W];
+    for (int o = 0; o < 4; ++o) {
+      hm[r * GS_T + x0 + o] = am[o];
+      ha[r * GS_T + x0 + o] = aa[o];
+    }
+    if (!fast) {
+      const double* krow = sk + r * PC;
+      cd ak[4];
 #pragma unroll
-      for (int q = 0; q < W; ++q) w[q] = hm[(y0 + q) * GS_T + x];
+      for (int o = 0; o < 4; ++o) ak[o] = mkc(0.0, 0.0);
 #pragma unroll
-      for (int a = 0; a < N; ++a) {
-        const double aa = c.sa[a], ma = c.sm[a];
+      for (int q = 0; q < W; ++q) {
+        const double kq = krow[gskew(x0 + q)];
+        const cd ku = mkc(kq * uv[q].x, kq * uv[q].y);
 #pragma unroll
         for (int o = 0; o < 4; ++o) {
-          lm[o].x = fma(aa, w[o + a].x, lm[o].x); lm[o].y = fma(aa, w[o + a].y, lm[o].y);
-          lk[o].x = fma(ma, w[o + a].x, lk[o].x); lk[o].y = fma(ma, w[o + a].y, lk[o].y);
+          const int bb = q - o;
+          if (bb >= 0 && bb < N) {
+            ak[o].x = fma(c.sm[bb], ku.x, ak[o].x);
+            ak[o].y = fma(c.sm[bb], ku.y, ak[o].y);
+          }
         }
       }
 #pragma unroll
-      for (int q = 0; q < W; ++q) w[q] = ha[(y0 + q) * GS_T + x];
+      for (int o = 0; o < 4; ++o) hk[r * GS_T + x0 + o] = ak[o];
+    }
+  }
+  __syncthreads();
+  // vertical pass: thread = (column x, row group y0 of 4)
+  const int x = tid & 31, y0 = (tid >> 5) * 4;
+  cd lm[4], lk[4];
+#pragma unroll
+  for (int o = 0; o < 4; ++o) { lm[o] = mkc(0.0, 0.0); lk[o] = mkc(0.0, 0.0); }
+  {
+    cd w[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = hm[(y0 + q) * GS_T + x];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const double aa = c.sa[a], ma = c.sm[a];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        lm[o].x = fma(aa, w[o + a].x, lm[o].x); lm[o].y = fma(aa, w[o + a].y, lm[o].y);
+        lk[o].x = fma(ma, w[o + a].x, lk[o].x); lk[o].y = fma(ma, w[o + a].y, lk[o].y);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) w[q] = ha[(y0 + q) * GS_T + x];
+#pragma unroll
+    for (int a = 0; a < N; ++a) {
+      const double ma = c.sm[a];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) { lm[o].x = fma(ma, w[o + a].x, lm[o].x); lm[o].y = fma(ma, w[o + a].y, lm[o].y); }
+    }
+    if (!fast) {  // lk = sum_a m_a (M (k u))_a; the uniform form scales sum_a m_a (M u)_a by k
+#pragma unroll
+      for (int q = 0; q < W; ++q) w[q] = hk[(y0 + q) * GS_T + x];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) lk[o] = mkc(0.0, 0.0);
 #pragma unroll
       for (int a = 0; a < N; ++a) {
         const double ma = c.sm[a];
 #pragma unroll
-        for (int o = 0; o < 4; ++o) { lm[o].x = fma(ma, w[o + a].x, lm[o].x); lm[o].y = fma(ma, w[o + a].y, lm[o].y); }
+        for (int o = 0; o < 4; ++o) { lk[o].x = fma(ma, w[o + a].x, lk[o].x); lk[o].y = fma(ma, w[o + a].y, lk[o].y); }
       }
-      if (!fast) {  // lk = sum_a m_a (M (k u))_a; the uniform form scales sum_a m_a (M u)_a by k
+    } else {
 #pragma unroll
-        for (int q = 0; q < W; ++q) w[q] = hk[(y0 + q) * GS_T + x];
-#pragma unroll
-        for (int o = 0; o < 4; ++o) lk[o] = mkc(0.0, 0.0);
-#pragma unroll
-        for (int a = 0; a < N; ++a) {
-          const double ma = c.sm[a];
-#pragma unroll
-          for (int o = 0; o < 4; ++o) { lk[o].x = fma(ma, w[o + a].x, lk[o].x); lk[o].y = fma(ma, w[o + a].y, lk[o].y); }
-        }
-      } else {
-#pragma unroll
-        for (int o = 0; o < 4; ++o) lk[o] = mkc(c.ku * lk[o].x, c.ku * lk[o].y);
-      }
+      for (int o = 0; o < 4; ++o) lk[o] = mkc(c.ku * lk[o].x, c.ku * lk[o].y);
     }
-    const int i = i0 + x;
-    if (i < g.nx) {
+  }
+  const int i = i0 + x;
+  if (i >= g.nx) return;
 #pragma unroll
-      for (int o = 0; o < 4; ++o) {
-        const int j = j0 + y0 + o;
-        if (j >= g.ny) break;
-        const int gj = j + g.row0;
-        const long long p = (long long)j * g.nx + i;
-        cd v;
-        if (pinned(g, c, gj, i)) {
-          v = su[(y0 + o + R) * PC + gskew(x + R)];
-        } else {
-          // lsc * lap sums + msc * mass sum (complex msc)
-          v.x = fma(c.lsc, lm[o].x, fma(c.msc.x, lk[o].x, -c.msc.y * lk[o].y));
-          v.y = fma(c.lsc, lm[o].y, fma(c.msc.x, lk[o].y, c.msc.y * lk[o].x));
-        }
-        out[p] = MODE == 0 ? v : c_sub(b[p], v);
-      }
+  for (int o = 0; o < 4; ++o) {
+    const int j = j0 + y0 + o;
+    if (j >= g.ny) return;
+    const int gj = j + g.row0;
+    const long long p = (long long)j * g.nx + i;
+    cd v;
+    if (pinned(g, c, gj, i)) {
+      v = su[(y0 + o + R) * PC + gskew(x + R)];
+    } else {
+      // lsc * lap sums + msc * mass sum (complex msc)
+      v.x = fma(c.lsc, lm[o].x, fma(c.msc.x, lk[o].x, -c.msc.y * lk[o].y));
+      v.y = fma(c.lsc, lm[o].y, fma(c.msc.x, lk[o].y, c.msc.y * lk[o].x));
     }
-    __syncthreads();  // su / H are rewritten by the next tile
+    out[p] = MODE == 0 ? v : c_sub(b[p], v);
   }
 }
 
@@ -787,14 +766,7 @@ template <int R, int MODE>
 static void launch_rgs(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* out,
                        cudaStream_t st) {
   ensure_smem_attr((const void*)k_rgs<R, MODE>, GSTile<R>::bytes);
-  const int ntiles = ((g.nx + GS_T - 1) / GS_T) * ((g.ny + GS_T - 1) / GS_T);
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  const int grd = std::min(ntiles, 2 * sms);  // persistent: two CTAs per SM
+  const dim3 grd((g.nx + GS_T - 1) / GS_T, (g.ny + GS_T - 1) / GS_T);
   k_rgs<R, MODE><<<grd, 256, GSTile<R>::bytes, st>>>(u, b, k, out, g, c);
 }
 
