@@ -278,6 +278,7 @@ KWS::~KWS() {
   Engine& E = engine();
   E.free(gst);
   if (hflags) cudaFreeHost(hflags);
+  if (hvtab) cudaFreeHost(hvtab);
   E.free(dV);
   E.free(gpart);
   E.free(tg);
@@ -298,11 +299,13 @@ static long long env_ll(const char* name, long long dflt) {
 int resident_ortho() {
   static int o = -1;
   if (o < 0) {
-    // dgks (default): CGS + DGKS re-orthogonalisation; cgs2: always two passes; ls: the
-    // low-synchronisation MGS; mgs: the reference's order
+    // auto (default): the low-synchronisation MGS on levels >= 131072 points, CGS + DGKS
+    // below (measured per level, profiles/r02m_modes.log: 513^2 54.2 vs 60.5 us/it; 257^2 ..
+    // 65^2 DGKS 21-24 vs 25-29); dgks / ls force one; cgs2: always two passes; mgs: the
+    // reference's order
     const char* e = getenv("HDB_ORTHO");
-    const std::string v = e ? e : "dgks";
-    o = v == "mgs" ? 0 : (v == "cgs2" ? 1 : (v == "ls" ? 3 : 2));
+    const std::string v = e ? e : "auto";
+    o = v == "mgs" ? 0 : v == "cgs2" ? 1 : v == "dgks" ? 2 : v == "ls" ? 3 : 4;
   }
   return o;
 }
@@ -460,14 +463,19 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     bool coop = false;
     auto ensure_dv = [&] {
       if (ws.dV_cap < j + 1) {
+        E.sync();  // copies from the old pinned mirror may still be pending
         E.free(ws.dV);
+        if (ws.hvtab) cudaFreeHost(ws.hvtab);
         ws.dV_cap = std::max(2 * (j + 1), 64);
         ws.dV = (cd**)E.alloc_bytes(sizeof(cd*) * ws.dV_cap);
+        HDB_CUDA(cudaMallocHost(&ws.hvtab, sizeof(cd*) * ws.dV_cap));
         ws.dV_n = 0;
       }
-      while (ws.dV_n < j + 1) {  // append V pointers (their addresses never change)
-        ws.v(ws.dV_n);           // (allocates the vector if it does not exist yet)
-        HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, &ws.V[ws.dV_n], sizeof(cd*), cudaMemcpyHostToDevice, E.st));
+      // append V pointers (their addresses never change) through a pinned mirror: an
+      // asynchronous copy from ws.V itself could read storage a later push_back frees
+      while (ws.dV_n < j + 1) {
+        ws.hvtab[ws.dV_n] = ws.v(ws.dV_n);  // (allocates the vector if it does not exist yet)
+        HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, ws.hvtab + ws.dV_n, sizeof(cd*), cudaMemcpyHostToDevice, E.st));
         ws.dV_n++;
       }
     };
@@ -613,15 +621,18 @@ static void ensure_vtab(KWS& ws, int upto) {
   Engine& E = engine();
   ws.v(upto);
   if (ws.dV_cap < upto + 1) {
+    E.sync();  // copies from the old pinned mirror may still be pending
     E.free(ws.dV);
+    if (ws.hvtab) cudaFreeHost(ws.hvtab);
     ws.dV_cap = std::max(2 * (upto + 1), 64);
     ws.dV = (cd**)E.alloc_bytes(sizeof(cd*) * ws.dV_cap);
+    HDB_CUDA(cudaMallocHost(&ws.hvtab, sizeof(cd*) * ws.dV_cap));
     ws.dV_n = 0;
   }
-  if (ws.dV_n < upto + 1) {
-    HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, &ws.V[ws.dV_n], sizeof(cd*) * (upto + 1 - ws.dV_n),
+  if (ws.dV_n < upto + 1) {  // pinned mirror: the copy stays asynchronous, its source stays valid
+    for (int i = ws.dV_n; i <= upto; ++i) ws.hvtab[i] = ws.V[i];
+    HDB_CUDA(cudaMemcpyAsync(ws.dV + ws.dV_n, ws.hvtab + ws.dV_n, sizeof(cd*) * (upto + 1 - ws.dV_n),
                              cudaMemcpyHostToDevice, E.st));
-    HDB_CUDA(cudaStreamSynchronize(E.st));  // pageable source: keep it alive until copied
     ws.dV_n = upto + 1;
   }
 }

@@ -180,6 +180,7 @@ struct KWS {
   long long halo = 0;      // halo elements around every basis vector (sharded levels)
   std::vector<cd*> V, Z;
   cd** dV = nullptr;       // device table of V pointers (cooperative MGS)
+  cd** hvtab = nullptr;    // its pinned host mirror (the copy source)
   int dV_cap = 0, dV_n = 0;
   cd* gpart = nullptr;     // grid-reduction partials
   cd* tg = nullptr;        // T = (I + L)^{-1} rows of the low-synchronisation MGS (mgs_ls_tg_elems())

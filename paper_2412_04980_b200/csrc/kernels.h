@@ -84,7 +84,8 @@ void launch_gm_solve(cd* st, int cap, cudaStream_t s);
 void launch_gm_final(const cd* nn, const cd* st, int cap, int* its_out, double* rel_out, cd* flag, cudaStream_t s);
 const int* gm_flags(const cd* st);
 cd* gm_y(cd* st, int cap);  // 8 per-phase cycle counters or null
-// ortho 0: modified Gram-Schmidt (reference order), 1: CGS2 (caps <= resident_vec_cap())
+// ortho 0: modified Gram-Schmidt (reference order), 1: CGS2 (caps <= resident_vec_cap()),
+// 2: CGS + DGKS, 3: low-synchronisation MGS, 4: 3 on levels >= 131072 points, else 2
 int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, const double* ksq, const cd* b, cd* x,
                           cd* basis, cd* Rg, cd* gpart, long long n, double tol, int cap, int* its_out,
                           double* relres_out, cd* flag, cudaStream_t st);

@@ -1011,6 +1011,7 @@ int launch_resident_gmres(int mode, int ortho, const OpCoef& c, const Geom& g, c
   ResidentArgs a{};
   a.c = c; a.g = g; a.ksq = ksq; a.b = b; a.x = x; a.basis = basis; a.Rg = Rg; a.gpart = gpart; a.n = n;
   a.tol = tol; a.cap = cap; a.its_out = its_out; a.relres_out = relres_out; a.flag = flag; a.prof = g_prof;
+  if (ortho == 4) ortho = n >= 131072 ? 3 : 2;  // auto
   if (ortho == 1 && cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
   if (ortho == 3 && 2 * cap + 1 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 2;
   if (ortho == 2 && cap + 2 > (mode == 0 ? kGatherCap : kVecCap)) ortho = 0;
