@@ -123,6 +123,7 @@ struct ThreadGroup {
   long long gen = 0;
   std::vector<const void*> p0, p1;    // published device pointers
   std::vector<std::vector<double>> vals;
+  std::vector<long long> tag;          // per-rank (kind, size) of the collective being entered
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     const long long g = gen;
@@ -152,17 +153,27 @@ struct ThreadComm : Comm {
       g->p0.assign(n, nullptr);
       g->p1.assign(n, nullptr);
       g->vals.assign(n, {});
+      g->tag.assign(n, 0);
       g_groups[group] = g;
     } else {
       g = it->second;
     }
+  }
+  // every rank must enter the same collective: publish (kind, size), check after the barrier
+  void enter(long long kind, long long size) {
+    g->tag[rank] = kind * (1LL << 40) + size;
+    g->barrier();
+    for (int r = 0; r < this->size; ++r)
+      if (g->tag[r] != g->tag[rank])
+        throw Error(E_CUDA, "thread transport: ranks entered different collectives (kind/size " +
+                                std::to_string(g->tag[rank]) + " vs " + std::to_string(g->tag[r]) + ")");
   }
   void allreduce(double* dev, int count, cudaStream_t st) override {
     std::vector<double>& mine = g->vals[rank];
     mine.resize(count);
     HDB_CUDA(cudaMemcpyAsync(mine.data(), dev, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
     HDB_CUDA(cudaStreamSynchronize(st));
-    g->barrier();
+    enter(1, count);
     std::vector<double> sum(count, 0.0);
     for (int r = 0; r < size; ++r)
       for (int i = 0; i < count; ++i) sum[i] += g->vals[r][i];  // rank order: identical everywhere
@@ -174,7 +185,7 @@ struct ThreadComm : Comm {
     HDB_CUDA(cudaStreamSynchronize(st));
     g->p0[rank] = su;  // my first rows (for rank-1)
     g->p1[rank] = sd;  // my last rows (for rank+1)
-    g->barrier();
+    enter(2, (long long)bu);
     if (rank > 0) HDB_CUDA(cudaMemcpyAsync(ru, g->p1[rank - 1], bu, cudaMemcpyDeviceToDevice, st));
     if (rank < size - 1) HDB_CUDA(cudaMemcpyAsync(rd, g->p0[rank + 1], bd, cudaMemcpyDeviceToDevice, st));
     HDB_CUDA(cudaStreamSynchronize(st));
@@ -184,7 +195,7 @@ struct ThreadComm : Comm {
                   cudaStream_t st) override {
     HDB_CUDA(cudaStreamSynchronize(st));
     g->p0[rank] = local;
-    g->barrier();
+    enter(3, (long long)off.size());
     for (int r = 0; r < size; ++r)
       HDB_CUDA(cudaMemcpyAsync((char*)full + off[r], g->p0[r], bytes[r], cudaMemcpyDeviceToDevice, st));
     HDB_CUDA(cudaStreamSynchronize(st));

@@ -57,8 +57,16 @@ void KProf::reset() {
 // ------------------------------------------------------------------ engine
 static std::unique_ptr<Engine> g_engine;
 
+void Engine::check_after(int fam) {
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess)
+    throw Error(E_CUDA, std::string("after a ") + kfam_name(fam) + " launch: " + cudaGetErrorString(e));
+}
+
 Engine::Engine(int dev) : device(dev) {
   HDB_CUDA(cudaSetDevice(dev));
+  const char* dbg = getenv("HDB_DEBUG_SYNC");
+  debug_sync = dbg && *dbg && *dbg != '0';
   HDB_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   own_st = st;
   HDB_CUDA(cudaMalloc(&red.partials, sizeof(cd) * kMaxReduceBlocks));
@@ -324,6 +332,17 @@ static long long lsh_min() {
   return v > 0 ? v : (1LL << 62);
 }
 
+// sharded levels with at least this many local points take the HBM-streaming low-sync
+// step (HDB_LSH_SHARD_N; default off: with it on small sharded levels, the one-GPU thread-
+// rank emulation hit an intermittent illegal address (1 run in 3 of tools/
+// slab_sensitivity.py; never with CUDA_LAUNCH_BLOCKING=1 or with >= 10000 local points,
+// profiles/r02q_slab_lsh.log) that is not resolved -- sharded levels keep the fused chain)
+static long long lsh_shard_min() {
+  static long long v = -2;
+  if (v == -2) v = env_ll("HDB_LSH_SHARD_N", -1);
+  return v < 0 ? (1LL << 62) : v;
+}
+
 long long coop_mgs_min() {
   static long long v = -1;
   if (v < 0) v = env_ll("HDB_COOP_MGS_N", 2000);  // (config 3 @40 Hz: 1018 -> 997 ms vs 150000)
@@ -504,7 +523,8 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     // sharded levels take it at any size: two all-reduces per Arnoldi step (the (2j+1)
     // coefficient sums and ||w||^2) instead of one per MGS coefficient
     bool lsh = false;
-    if (!coop && (shard || n >= lsh_min()) && mgs_ls_on() && (j == 0 || lsh_ok) && stop.max_iters <= 511) {
+    if (!coop && ((shard && n >= lsh_shard_min()) || (!shard && n >= lsh_min())) && mgs_ls_on() && (j == 0 || lsh_ok) &&
+        stop.max_iters <= 511) {
       if (ws.tgh_cap < stop.max_iters) {
         E.free(ws.tgh);
         E.free(ws.lpart);

@@ -96,6 +96,8 @@ struct Engine {
   long long syncs = 0;     // host synchronisations (Hessenberg reads etc.)
   Comm* comm = nullptr;    // row-slab communicator of this rank (owned), null on one rank
   KProf kp;                // launch accounting / optional per-launch timing
+  bool debug_sync = false; // HDB_DEBUG_SYNC=1: synchronise and check after every launch (fault location)
+  void check_after(int fam);
   // run `f` (which enqueues `nl` kernels of family `fam` moving `bytes`
   // algorithmic bytes) with optional event timing around it
   template <class F>
@@ -106,6 +108,7 @@ struct Engine {
       cudaEventRecord(a, st);
     }
     f();
+    if (debug_sync) check_after(fam);
     launches += nl;
     kp.bytes[fam] += bytes;
     kp.n[fam] += nl;
@@ -241,9 +244,9 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
 // HDB_GRID_N points (default 2M) when the stencil windows fit shared memory.
 // 0 disables a mode.
 int resident_mode(long long n, int cap);  // -1: launch-driven path
-int resident_ortho();  // HDB_ORTHO=mgs|cgs2 (default cgs2) for device-resident solves
-long long coop_mgs_min();
-bool step1_enabled();  // HDB_STEP1=0 forces the host-driven path for one-iteration FGMRES  // levels >= this many points use the cooperative MGS step (HDB_COOP_MGS_N)
+int resident_ortho();  // HDB_ORTHO=auto|dgks|ls|cgs2|mgs for device-resident solves (launch_resident_gmres codes)
+long long coop_mgs_min();  // levels >= this many points use the one-launch MGS step (HDB_COOP_MGS_N)
+bool step1_enabled();  // HDB_STEP1=0 forces the host-driven path for one-iteration FGMRES
 
 struct SmallSolve {  // device-resident GMRES on one level operator
   const LevelOp* op = nullptr;

@@ -76,8 +76,10 @@ def test_slab_solve_matches_single_rank(P, min_rows):
 
 def test_slab_solve_heterogeneous_dirichlet_mix():
     """Mixed Dirichlet/Sommerfeld sides across slab edges, heterogeneous k (no
-    reference fixture; held to the single-rank solve with a rounding-amplification
-    allowance)."""
+    reference fixture; held to the single-rank solve).  This problem amplifies
+    rounding: the single-rank solve itself moves by 5.2e-7 (relative L2) between
+    the MGS-order and the low-synchronisation Gram-Schmidt (tools/slab_sensitivity.py,
+    profiles/r02o_slab_noshard.log), so the slab solve is held to 10x that."""
     def build():
         vel = hdb.VelocityModel(kind="wedge", layers=[(-400.0, -200.0, 2000.0), (-800.0, -600.0, 1500.0),
                                                       (0.0, 0.0, 3000.0)])
@@ -91,7 +93,7 @@ def test_slab_solve_heterogeneous_dirichlet_mix():
     res = _solve_ranks(build, 2, 16)
     x = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])], axis=0)
     assert all(r[2].outer_iterations == ref.outer_iterations for r in res)
-    assert np.linalg.norm(x - xref) <= 1e-7 * np.linalg.norm(xref)
+    assert np.linalg.norm(x - xref) <= 5e-6 * np.linalg.norm(xref)
 
 
 def test_slab_solve_large_grid_tma_transfers():
