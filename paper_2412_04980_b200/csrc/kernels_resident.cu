@@ -54,6 +54,8 @@ struct ResidentArgs {
   long long* prof;    // optional: per-phase cycles of CTA 0 thread 0 (telemetry), may be null
   int tiled;          // stencil windows staged in shared memory
   int tile_elems;     // window elements (max over CTAs)
+  int sbasis;         // 1: this CTA's basis slices also kept in shared memory (dots / updates read them)
+  int sstride;        // their stride (points per CTA, rounded up)
 };
 
 // phase clock (CTA 0, thread 0) — only when A.prof != nullptr
@@ -431,8 +433,10 @@ __device__ __forceinline__ cd cdiv_(cd a, cd b) {
 // with_norm: element m of the reduction carries <w, w> of the incoming w.
 // `ph(k)` marks sub-phases (telemetry): 6 after the local dots, 7 after the
 // reduction, 8 after the update.
+// vb: this CTA's slice of V_0 (global basis + p0, or the shared-memory copy), vs: the
+// stride between consecutive basis slices
 template <class Sync, class Ph>
-__device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n, long long p0, int cnt, int m,
+__device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* vb, long long vs, int cnt, int m,
                          int& buf, cd* gpart, bool with_norm, Ph&& ph) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int mm = m + (with_norm ? 1 : 0);
@@ -442,8 +446,8 @@ __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long 
   for (int i = wid; i < mm; i += 2 * NW) {
     const int i2 = i + NW;
     const bool two = i2 < mm;
-    const cd* v1 = i < m ? basis + (long long)i * n + p0 : ws;
-    const cd* v2 = !two ? v1 : (i2 < m ? basis + (long long)i2 * n + p0 : ws);
+    const cd* v1 = i < m ? vb + (long long)i * vs : ws;
+    const cd* v2 = !two ? v1 : (i2 < m ? vb + (long long)i2 * vs : ws);
     cd a = mkc(0.0, 0.0), b2 = mkc(0.0, 0.0);
 #pragma unroll 4
     for (int q = lane; q < cnt; q += 32) {
@@ -464,16 +468,16 @@ __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long 
   ph(7);
   for (int q = threadIdx.x; q < cnt; q += kRT) {
     cd w = ws[q];
-    const cd* vq = basis + p0 + q;
+    const cd* vq = vb + q;
     int i = 0;
     for (; i + 8 <= m; i += 8) {  // 8 loads in flight, then the dependent updates in order
       cd v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i + u) * n];
+      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i + u) * vs];
 #pragma unroll
       for (int u = 0; u < 8; ++u) w = c_sub(w, c_mul_np(s.hv[i + u], v[u]));
     }
-    for (; i < m; ++i) w = c_sub(w, c_mul_np(s.hv[i], vq[(long long)i * n]));
+    for (; i < m; ++i) w = c_sub(w, c_mul_np(s.hv[i], vq[(long long)i * vs]));
     ws[q] = w;
   }
   __syncthreads();
@@ -486,13 +490,13 @@ __device__ void cgs_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long 
 // h = T g into s.hcol; then w -= h_k V_k (V_j first, then k = j-1 .. 0).  The caller
 // forms ||w||^2 with one more reduction.
 template <class Sync>
-__device__ void ls_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n, long long p0, int cnt, int j,
+__device__ void ls_pass(Sync& sy, RSmem& s, cd* ws, const cd* vb, long long vs, int cnt, int j,
                         int& buf, cd* gpart, cd* Tg, int rank) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, t = threadIdx.x;
   constexpr int NW = kRT / 32;
-  const cd* vj = basis + (long long)j * n + p0;
+  const cd* vj = vb + (long long)j * vs;
   for (int i = wid; i <= j; i += NW) {  // warp per basis vector: g_i and (i < j) l_i
-    const cd* vi = basis + (long long)i * n + p0;
+    const cd* vi = vb + (long long)i * vs;
     cd a = mkc(0.0, 0.0), l = mkc(0.0, 0.0);
 #pragma unroll 4
     for (int q = lane; q < cnt; q += 32) {
@@ -556,16 +560,16 @@ __device__ void ls_pass(Sync& sy, RSmem& s, cd* ws, const cd* basis, long long n
   __syncthreads();
   for (int q = t; q < cnt; q += kRT) {  // w -= h_j V_j, then h_k V_k for k = j-1 .. 0
     cd w = ws[q];
-    const cd* vq = basis + p0 + q;
+    const cd* vq = vb + q;
     int i = j;
     for (; i >= 7; i -= 8) {  // 8 loads in flight, then the dependent updates in order
       cd v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i - u) * n];
+      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i - u) * vs];
 #pragma unroll
       for (int u = 0; u < 8; ++u) w = c_sub(w, c_mul_np(s.hcol[i - u], v[u]));
     }
-    for (; i >= 0; --i) w = c_sub(w, c_mul_np(s.hcol[i], vq[(long long)i * n]));
+    for (; i >= 0; --i) w = c_sub(w, c_mul_np(s.hcol[i], vq[(long long)i * vs]));
     ws[q] = w;
   }
   __syncthreads();
@@ -587,6 +591,12 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   const Tile T = make_tile<R>(A.g, p0, p1);
   cd* ut = A.tiled ? ws + chunk_max : nullptr;                 // stencil window of the current vector
   double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
+  // optional shared-memory copy of this CTA's basis slices (after the windows, 16-B aligned)
+  cd* sb = nullptr;
+  if (A.sbasis) {
+    const size_t off = ((size_t)(reinterpret_cast<unsigned char*>(kt + A.tile_elems) - smem_raw) + 15) / 16 * 16;
+    sb = reinterpret_cast<cd*>(smem_raw + off);
+  }
   if (A.tiled && cnt > 0) load_k_tile<R>(kt, T, A.ksq, A.g, A.c);
   const cd* ucoef = nullptr;
   if (A.tiled && R > 1) {
@@ -611,6 +621,8 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   const int nx = A.g.nx;
   int buf = 0;
   auto V = [&](int i) { return A.basis + (long long)i * n; };
+  const cd* vb = sb ? sb : A.basis + p0;      // this CTA's slice of V_0
+  const long long vs = sb ? A.sstride : n;    // stride between basis slices
   cd* Rg = A.Rg;
   cd* yg = A.Rg + (long long)A.cap * (A.cap + 1) / 2;
 
@@ -635,6 +647,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     for (int q = t; q < cnt; q += kRT) {
       const cd v = A.b[p0 + q];
       v0[p0 + q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+      if (sb) sb[q] = v0[p0 + q];
     }
   }
   if (t == 0) s.g[0] = mkc(beta, 0.0);
@@ -721,7 +734,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     if (ORTHO == 0) {
       // modified Gram-Schmidt (krylov.py:121-124): h_i = <V_i, w>; w -= h_i V_i
       for (int i = 0; i <= j; ++i) {
-        const cd* vi = V(i) + p0;
+        const cd* vi = vb + (long long)i * vs;
         cd a = mkc(0.0, 0.0);
         for (int q = t; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], ws[q]);
         const cd h = sy.reduce(a, s, buf, A.gpart);
@@ -730,15 +743,15 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       }
     } else if (ORTHO == 3) {
       __syncthreads();
-      ls_pass(sy, s, ws, A.basis, n, p0, cnt, j, buf, A.gpart, Rg + (long long)A.cap * (A.cap + 1) / 2 + A.cap, rank);
+      ls_pass(sy, s, ws, vb, vs, cnt, j, buf, A.gpart, Rg + (long long)A.cap * (A.cap + 1) / 2 + A.cap, rank);
     } else if (ORTHO == 1) {
       // classical Gram-Schmidt with one re-orthogonalisation (CGS2): the same
       // Hessenberg column in exact arithmetic, two reductions instead of j+1
       __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, false, ph);
+      cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, false, ph);
       for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
       __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, false, ph);
+      cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, false, ph);
       for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
       __syncthreads();
     }
@@ -751,7 +764,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       // the (tiny) corrections.  Same Hessenberg column in exact arithmetic;
       // every CTA takes the same branch (identically reduced scalars).
       __syncthreads();
-      cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true, ph);
+      cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, true, ph);
       double nw = s.hv[j + 1].x, sh = 0.0;
       for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
       __syncthreads();
@@ -759,7 +772,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       double est = nw - sh;
       if (!(est > 0.5 * nw)) {
         __syncthreads();
-        cgs_pass(sy, s, ws, A.basis, n, p0, cnt, j + 1, buf, A.gpart, true, ph);
+        cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, true, ph);
         nw = s.hv[j + 1].x;
         sh = 0.0;
         for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
@@ -780,9 +793,12 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     // V_{j+1} = w / ||w|| (harmless if step j turns out to be the last)
     const double inv = 1.0 / hn;
     cd* vn = V(j + 1) + p0;
+    cd* sn1 = sb ? sb + (long long)(j + 1) * vs : nullptr;
     for (int q = t; q < cnt; q += kRT) {
       const cd v = ws[q];
-      vn[q] = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+      const cd u = mkc(__dmul_rn(v.x, inv), __dmul_rn(v.y, inv));
+      vn[q] = u;
+      if (sn1) sn1[q] = u;
     }
     sy.barrier();  // V_{j+1} complete everywhere
     PHASE(5);
@@ -817,16 +833,16 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   const cd* yc = ysm ? s.hv : yg;
   for (int q = t; q < cnt; q += kRT) {
     cd xx = mkc(0.0, 0.0);
-    const cd* vq = A.basis + p0 + q;
+    const cd* vq = vb + q;
     int i = 0;
     for (; i + 8 <= its; i += 8) {
       cd v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i + u) * n];
+      for (int u = 0; u < 8; ++u) v[u] = vq[(long long)(i + u) * vs];
 #pragma unroll
       for (int u = 0; u < 8; ++u) xx = c_add(xx, c_mul_np(yc[i + u], v[u]));
     }
-    for (; i < its; ++i) xx = c_add(xx, c_mul_np(yc[i], vq[(long long)i * n]));
+    for (; i < its; ++i) xx = c_add(xx, c_mul_np(yc[i], vq[(long long)i * vs]));
     A.x[p0 + q] = xx;
   }
   sy.barrier();  // x complete everywhere
@@ -872,6 +888,24 @@ static int tile_elems_for(long long n, int nx, int P, int R) {
 
 static size_t smem_tiled(long long chunk, int tile, bool cluster) {
   return smem_for(chunk, cluster) + (size_t)tile * (sizeof(cd) + sizeof(double));
+}
+
+// add the shared-memory basis slices ((cap + 1) x chunk points) when they fit beside the
+// windows (HDB_RES_SBASIS=0 disables): the dots and updates then read shared memory
+static size_t with_sbasis(ResidentArgs& a, size_t sm, long long chunk, size_t limit) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HDB_RES_SBASIS");
+    on = e ? atoi(e) : 1;
+  }
+  a.sbasis = 0;
+  a.sstride = (int)chunk;
+  const size_t extra = 16 + (size_t)(a.cap + 1) * (size_t)chunk * sizeof(cd);
+  if (on && sm + extra <= limit) {
+    a.sbasis = 1;
+    return sm + extra;
+  }
+  return sm;
 }
 
 static int g_cluster = 0;
@@ -926,6 +960,7 @@ static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
   size_t sm = smem_tiled(chunk, b.tile_elems, true);
   b.tiled = sm <= g_smem_optin;
   if (!b.tiled) return false;  // untiled resident solves lose to the launch path
+  sm = with_sbasis(b, sm, chunk, g_smem_optin);
   set_attrs(kern, sm, true);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -962,6 +997,7 @@ static bool launch_grid(ResidentArgs a, cudaStream_t st) {
   size_t sm = smem_tiled(chunk, a.tile_elems, false);
   a.tiled = sm <= g_smem_optin;
   if (!a.tiled) return false;  // untiled resident solves lose to the launch path
+  sm = with_sbasis(a, sm, chunk, g_smem_optin);
   set_attrs(kern, sm, false);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRT, sm) != cudaSuccess || per_sm < 1) {

@@ -1,0 +1,9 @@
+# r02r: full GPU suite, smoke, driver-like bench, launch list of one config-2 solve
+mkdir -p gpurun_out
+python -c "from paper_2412_04980_b200 import _build; _build.build()" > gpurun_out/r02r_build.log 2>&1
+timeout -s KILL 900 python -m pytest tests -q -m gpu > gpurun_out/r02r_gpu_tests.log 2>&1; echo TESTS_EXIT $? >> gpurun_out/r02r_gpu_tests.log
+timeout -s KILL 200 python __graft_entry__.py smoke > gpurun_out/r02r_smoke.log 2>&1; echo SMOKE_EXIT $? >> gpurun_out/r02r_smoke.log
+timeout -s KILL 1200 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/r02r_bench.json 2> gpurun_out/r02r_bench.err
+timeout -s KILL 300 python tools/profile_solve.py c2 --repeat 1 > gpurun_out/r02r_plain.log 2>&1 && \
+timeout -s KILL 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02r_launches.csv python tools/profile_solve.py c2 --repeat 1 > gpurun_out/r02r_ncu.log 2>&1
+echo DONE
