@@ -373,7 +373,8 @@ void SmallSolve::ensure(const LevelOp* o, int cap_) {
   cap = cap_;
   basis = E.alloc((long long)(cap + 1) * o->n);
   Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap + (long long)(cap + 1) * (cap + 2) / 2);
-  gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
+  gpart = E.alloc(resident_gpart_elems());
+  HDB_CUDA(cudaMemsetAsync(gpart, 0, sizeof(cd) * (size_t)resident_gpart_elems(), E.st));  // sync words start at zero
 }
 
 bool SmallSolve::try_run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {

@@ -54,6 +54,7 @@ long long resident_cluster_points();
 long long resident_grid_points();
 int resident_grid_ctas();
 int resident_vec_cap();
+long long resident_gpart_elems();  // SmallSolve::gpart size (zeroed at allocation: it holds sync words)
 void resident_set_profile(long long* dev_counters);
 // one Arnoldi step's MGS chain in a cooperative launch (large levels); 1 = does not fit
 // tg != null: the low-synchronisation form (two grid reductions per step) where the

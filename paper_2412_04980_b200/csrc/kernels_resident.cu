@@ -56,7 +56,17 @@ struct ResidentArgs {
   int tile_elems;     // window elements (max over CTAs)
   int sbasis;         // 1: this CTA's basis slices also kept in shared memory (dots / updates read them)
   int sstride;        // their stride (points per CTA, rounded up)
+  unsigned* sw;       // GridSync sync words (zero between launches; kSw* layout), may be null
+  int flags;          // GridSync: 1 = neighbour flags + hierarchical last-arriver reductions
 };
+
+// GridSync sync-word layout (unsigned, zeroed at allocation, reset by every launch at exit)
+constexpr int kGrp = 16;          // CTAs per reduction group
+constexpr int kMaxGroups = 10;    // 160 CTAs
+constexpr int kSwTop = 16;        // arrivals of group last-arrivers
+constexpr int kSwFlag = 17;       // generation of the last published reduction
+constexpr int kSwReady = 32;      // [32, 32 + P): vectors published by CTA r
+constexpr int kSwWords = 32 + 160;
 
 // phase clock (CTA 0, thread 0) — only when A.prof != nullptr
 #define PHASE(k)                                                   \
@@ -90,7 +100,17 @@ struct RSmem {
   double cs[kMaxCap];
   cd g[kMaxCap + 2];
   int decision;
+  int wflag;                  // last-arriver role of this CTA in the current reduction
 };
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <int R>
 __device__ __forceinline__ cd op_point(const OpCoef& c, const Geom& g, const cd* u, const double* k, int gj, int i) {
@@ -299,6 +319,12 @@ struct ClusterSync {
     return s.bcast[0];
   }
   __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd*) { gather_sum(s, m, out, buf); }
+  // vector publication / window wait: one cluster barrier (DSMEM peers see global writes after it)
+  __device__ void publish(unsigned) {}
+  __device__ void wait_window(unsigned) { cl.sync(); }
+  __device__ void set_window(long long, long long, long long) {}
+  __device__ void setup(unsigned*, int) {}
+  __device__ void reset() {}
 };
 
 constexpr int kGridRounds = 5;  // ceil(148 SMs / 32): partial loads per lane in the grid reductions
@@ -308,15 +334,139 @@ struct GridSync {
   static constexpr bool kGather = false;
   static constexpr int kVecMax = kVecCap;
   cg::grid_group gr;
+  unsigned* sw = nullptr;  // sync words (flags mode)
+  int fl = 0;              // 1: neighbour flags + hierarchical last-arriver reductions
+  unsigned gen = 0;        // reductions done by this CTA (identical sequence in every CTA)
+  int wlo = 0, whi = -1;   // ranks whose slices intersect this CTA's stencil window
   __device__ GridSync() : gr(cg::this_grid()) {}
   __device__ int rank() const { return (int)blockIdx.x; }
   __device__ int nranks() const { return (int)gridDim.x; }
   __device__ void barrier() { gr.sync(); }
   __device__ void init(RSmem&, void*) {}
+  __device__ void setup(unsigned* sw_, int flags) { sw = sw_; fl = (sw_ && flags && gridDim.x <= kGrp * kMaxGroups) ? 1 : 0; }
+  // window point range [lo, hi) -> the ranks owning it (slices [n r / P, n (r + 1) / P))
+  __device__ void set_window(long long lo, long long hi, long long n) {
+    const int P = nranks();
+    auto owner = [&](long long p) {
+      int r = (int)((p * P) / n);
+      while (r + 1 < P && n * (r + 1) / P <= p) ++r;
+      while (r > 0 && n * r / P > p) --r;
+      return r;
+    };
+    wlo = owner(lo);
+    whi = owner(hi - 1);
+  }
+  // this CTA's slice of vector #val-1 is written (all threads): release it to the readers
+  __device__ void publish(unsigned val) {
+    if (!fl) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_u32(&sw[kSwReady + blockIdx.x], val);
+    }
+  }
+  // wait until every rank of the stencil window has published `val` vectors (flags mode),
+  // else a grid barrier.  The fence of the waiting threads also drops stale L1 lines.
+  __device__ void wait_window(unsigned val) {
+    if (!fl) {
+      gr.sync();
+      return;
+    }
+    const int r = wlo + (int)threadIdx.x;
+    if (r <= whi) {
+      while (ld_acquire_u32(&sw[kSwReady + r]) < val) {}
+      __threadfence();
+    }
+    __syncthreads();
+  }
+  // after the final barrier: zero the sync words for the next launch on this buffer
+  __device__ void reset() {
+    if (!sw) return;
+    if (threadIdx.x == 0) sw[kSwReady + blockIdx.x] = 0;
+    if (blockIdx.x == 0 && threadIdx.x < kSwReady) sw[threadIdx.x] = 0;
+  }
+  // Hierarchical last-arriver all-reduce (flags mode): every CTA stores its partials and
+  // takes a ticket of its group of kGrp CTAs; the group's last arriver sums the group's
+  // partials in rank order and takes a ticket at the top; the last group sums the group
+  // sums in group order, publishes them and releases the generation flag that everyone
+  // else spins on.  One grid-wide arrival wave instead of a barrier plus an all-to-all
+  // read of P x m partials; fixed summation order, identical sums in every CTA.
+  __device__ void reduce_vec_h(RSmem& s, int m, cd* out, cd* gpart) {
+    const int P = nranks(), r = blockIdx.x, t = threadIdx.x;
+    cd* col = gpart;
+    cd* gsum = gpart + (2LL * P + 2) * kVecCap;
+    cd* fsum = gsum + (long long)kMaxGroups * kVecCap;
+    ++gen;
+    for (int i = t; i < m; i += kRT) __stcg(&col[(long long)r * kVecCap + i], s.pv[i]);
+    __syncthreads();
+    const int g = r / kGrp, g0 = g * kGrp, gn = min(kGrp, P - g0), NG = (P + kGrp - 1) / kGrp;
+    if (t == 0) {
+      __threadfence();
+      const unsigned tk = atomicAdd(&sw[g], 1u);
+      s.wflag = tk == (unsigned)gn * gen - 1u ? 1 : 0;
+    }
+    __syncthreads();
+    if (s.wflag) {
+      __threadfence();
+      for (int i = t; i < m; i += kRT) {
+        cd z[kGrp];
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) z[u] = u < gn ? __ldcg(&col[(long long)(g0 + u) * kVecCap + i]) : mkc(0.0, 0.0);
+        cd q = mkc(0.0, 0.0);
+#pragma unroll
+        for (int u = 0; u < kGrp; ++u) {
+          q.x += z[u].x;
+          q.y += z[u].y;
+        }
+        __stcg(&gsum[(long long)g * kVecCap + i], q);
+      }
+      __syncthreads();
+      if (t == 0) {
+        __threadfence();
+        const unsigned tk = atomicAdd(&sw[kSwTop], 1u);
+        s.wflag = tk == (unsigned)NG * gen - 1u ? 2 : 1;
+      }
+      __syncthreads();
+      if (s.wflag == 2) {
+        __threadfence();
+        for (int i = t; i < m; i += kRT) {
+          cd z[kMaxGroups];
+#pragma unroll
+          for (int u = 0; u < kMaxGroups; ++u) z[u] = u < NG ? __ldcg(&gsum[(long long)u * kVecCap + i]) : mkc(0.0, 0.0);
+          cd q = mkc(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < kMaxGroups; ++u) {
+            q.x += z[u].x;
+            q.y += z[u].y;
+          }
+          __stcg(&fsum[i], q);
+          out[i] = q;
+        }
+        __syncthreads();
+        if (t == 0) {
+          __threadfence();
+          st_release_u32(&sw[kSwFlag], gen);
+        }
+        return;
+      }
+    }
+    if (t == 0) {
+      while (ld_acquire_u32(&sw[kSwFlag]) < gen) {}
+      __threadfence();
+    }
+    __syncthreads();
+    for (int i = t; i < m; i += kRT) out[i] = __ldcg(&fsum[i]);
+    __syncthreads();
+  }
   // s.pv[0..m) -> out[0..m), fixed rank order.  Two phases when m is large:
   // CTA i sums element i over the P partials (one column each), publishes it,
   // then every CTA reads the m sums; small m: every CTA sums everything itself.
   __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd* gpart) {
+    if (fl) {
+      reduce_vec_h(s, m, out, gpart);
+      buf ^= 1;
+      return;
+    }
     const int P = nranks();
     cd* col = gpart + (long long)buf * P * kVecCap;
     for (int i = threadIdx.x; i < m; i += blockDim.x) __stcg(&col[(long long)blockIdx.x * kVecCap + i], s.pv[i]);
@@ -393,6 +543,14 @@ struct GridSync {
   }
   __device__ cd reduce(cd v, RSmem& s, int& buf, cd* gpart) {
     const cd t = block_partial(v, s);
+    if (fl) {
+      if (threadIdx.x == 0) s.pv[0] = t;
+      __syncthreads();
+      reduce_vec_h(s, 1, &s.bcast[buf], gpart);
+      const cd r = s.bcast[buf];
+      buf ^= 1;
+      return r;
+    }
     const int P = nranks();
     if (threadIdx.x == 0) __stcg(&gpart[((long long)buf * P + blockIdx.x) * kVecCap], t);
     gr.sync();
@@ -582,6 +740,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   constexpr size_t kHead = ((sizeof(RSmem) + 15) / 16) * 16 + (Sync::kGather ? sizeof(GatherBuf) : 0);
   Sync sy;
   sy.init(s, smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);
+  sy.setup(A.sw, A.flags);
   const int P = sy.nranks(), rank = sy.rank();
   const long long n = A.n;
   const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
@@ -589,6 +748,17 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   const long long chunk_max = (n + P - 1) / P;
   cd* ws = reinterpret_cast<cd*>(smem_raw + kHead);  // this CTA's slice of w
   const Tile T = make_tile<R>(A.g, p0, p1);
+  if (cnt > 0) {
+    const long long wa = (long long)(T.rlo - R - A.g.row0) * A.g.nx, wb = wa + (long long)T.rows * A.g.nx;
+    const long long wlo = wa > 0 ? wa : 0, whi = wb < n ? wb : n;
+    sy.set_window(wlo, whi, n);
+  }
+  // every exit: a final barrier (no CTA leaves while a peer may still address its shared
+  // memory or wait on its flags), then the sync words are zeroed for the next launch
+  auto finish = [&] {
+    sy.barrier();
+    sy.reset();
+  };
   cd* ut = A.tiled ? ws + chunk_max : nullptr;                 // stencil window of the current vector
   double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
   // optional shared-memory copy of this CTA's basis slices (after the windows, 16-B aligned)
@@ -632,12 +802,12 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   if (bnorm == 0.0) {  // krylov.py:96-97
     for (int q = t; q < cnt; q += kRT) A.x[p0 + q] = mkc(0.0, 0.0);
     if (rank == 0 && t == 0) { *A.its_out = 0; *A.relres_out = 0.0; }
-    sy.barrier();
+    finish();
     return;
   }
   if (!isfinite(bnorm)) {
     if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = 0; }
-    sy.barrier();
+    finish();
     return;
   }
   const double beta = bnorm;  // r0 = b (zero initial guess); rel = 1 never triggers the early exit
@@ -659,6 +829,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   // overlapping that serial work with everybody else's stencil points.
   auto apply_M = [&](int jv, int givens_j, double hn_prev) {
     const cd* vj = V(jv);
+    sy.wait_window((unsigned)(jv + 1));  // V_jv complete over this CTA's window
     if (A.tiled) {
       if (cnt > 0) load_u_tile<R>(ut, T, vj, A.ksq, A.g, A.c);
       __syncthreads();
@@ -726,7 +897,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     }
     __syncthreads();
   };
-  sy.barrier();  // V_0 complete everywhere
+  sy.publish(1u);  // V_0 written (the window wait in apply_M completes it)
   apply_M(0, -1, 0.0);
   PHASE(1);
   int dec = 0;
@@ -800,7 +971,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       vn[q] = u;
       if (sn1) sn1[q] = u;
     }
-    sy.barrier();  // V_{j+1} complete everywhere
+    sy.publish((unsigned)(j + 2));  // V_{j+1}: its readers wait in apply_M
     PHASE(5);
     // Givens of step j on thread 0 while the stencil of step j+1 runs
     apply_M(j + 1, j, hn);
@@ -811,7 +982,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   }
   if (dec == 2) {
     if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = its; }
-    sy.barrier();
+    finish();
     return;
   }
   // least squares (krylov.py:161-168) on rank 0, y broadcast through global memory
@@ -865,7 +1036,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     *A.relres_out = fin;
     if (!isfinite(fin)) A.flag->x = 2.0;
   }
-  sy.barrier();  // no CTA leaves while a peer may still address its shared memory
+  finish();
 }
 
 // ------------------------------------------------------------------ launch
@@ -988,9 +1159,26 @@ static int grid_ctas_for(long long n) {
   return (int)std::max(16LL, std::min<long long>(g_grid, p));
 }
 
+// partials + group/final sums (cd elements), then the sync words
+constexpr long long kSwOffset = (2LL * kGrp * kMaxGroups + 2 + kMaxGroups + 1) * kVecCap;
+long long resident_gpart_elems() { return kSwOffset + (kSwWords * 4 + 15) / 16; }
+
+// HDB_RES_FLAGS=0: grid barriers + all-to-all partial reads (the r02 form) instead of the
+// neighbour flags and hierarchical last-arriver reductions
+static int res_flags() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HDB_RES_FLAGS");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 template <int R, int O>
 static bool launch_grid(ResidentArgs a, cudaStream_t st) {
   auto kern = k_resident_gmres<GridSync, R, O>;
+  a.sw = reinterpret_cast<unsigned*>(a.gpart + kSwOffset);
+  a.flags = res_flags();
   const int P = grid_ctas_for(a.n);
   const long long chunk = (a.n + P - 1) / P;
   a.tile_elems = tile_elems_for(a.n, a.g.nx, P, R);
