@@ -66,7 +66,9 @@ constexpr int kMaxGroups = 10;    // 160 CTAs
 constexpr int kSwTop = 16;        // arrivals of group last-arrivers
 constexpr int kSwFlag = 17;       // generation of the last published reduction
 constexpr int kSwReady = 32;      // [32, 32 + P): vectors published by CTA r
-constexpr int kSwWords = 32 + 160;
+constexpr int kSwLine = 32;       // one sync word per 128-byte line (no false sharing between spinners and atomics)
+constexpr int kSwWords = (32 + 160) * kSwLine;
+#define SW(i) sw[(i) * kSwLine]
 
 // phase clock (CTA 0, thread 0) — only when A.prof != nullptr
 #define PHASE(k)                                                   \
@@ -101,6 +103,7 @@ struct RSmem {
   cd g[kMaxCap + 2];
   int decision;
   int wflag;                  // last-arriver role of this CTA in the current reduction
+  double shv;                 // sum |h_i|^2 (DGKS), broadcast
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
@@ -337,13 +340,18 @@ struct GridSync {
   unsigned* sw = nullptr;  // sync words (flags mode)
   int fl = 0;              // 1: neighbour flags + hierarchical last-arriver reductions
   unsigned gen = 0;        // reductions done by this CTA (identical sequence in every CTA)
+  int onephase = kOnePhaseMax;  // largest m reduced with one barrier (all-to-all partial reads)
   int wlo = 0, whi = -1;   // ranks whose slices intersect this CTA's stencil window
   __device__ GridSync() : gr(cg::this_grid()) {}
   __device__ int rank() const { return (int)blockIdx.x; }
   __device__ int nranks() const { return (int)gridDim.x; }
   __device__ void barrier() { gr.sync(); }
   __device__ void init(RSmem&, void*) {}
-  __device__ void setup(unsigned* sw_, int flags) { sw = sw_; fl = (sw_ && flags && gridDim.x <= kGrp * kMaxGroups) ? 1 : 0; }
+  __device__ void setup(unsigned* sw_, int flags) {
+    sw = sw_;
+    fl = (sw_ && (flags & 1) && gridDim.x <= kGrp * kMaxGroups) ? 1 : 0;
+    if (flags & 2) onephase = 4;  // two-barrier reduce-scatter / all-gather from m = 5
+  }
   // window point range [lo, hi) -> the ranks owning it (slices [n r / P, n (r + 1) / P))
   __device__ void set_window(long long lo, long long hi, long long n) {
     const int P = nranks();
@@ -362,7 +370,7 @@ struct GridSync {
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
-      st_release_u32(&sw[kSwReady + blockIdx.x], val);
+      st_release_u32(&SW(kSwReady + blockIdx.x), val);
     }
   }
   // wait until every rank of the stencil window has published `val` vectors (flags mode),
@@ -374,7 +382,7 @@ struct GridSync {
     }
     const int r = wlo + (int)threadIdx.x;
     if (r <= whi) {
-      while (ld_acquire_u32(&sw[kSwReady + r]) < val) {}
+      while (ld_acquire_u32(&SW(kSwReady + r)) < val) {}
       __threadfence();
     }
     __syncthreads();
@@ -382,8 +390,8 @@ struct GridSync {
   // after the final barrier: zero the sync words for the next launch on this buffer
   __device__ void reset() {
     if (!sw) return;
-    if (threadIdx.x == 0) sw[kSwReady + blockIdx.x] = 0;
-    if (blockIdx.x == 0 && threadIdx.x < kSwReady) sw[threadIdx.x] = 0;
+    if (threadIdx.x == 0) SW(kSwReady + blockIdx.x) = 0;
+    if (blockIdx.x == 0 && threadIdx.x < kSwReady) SW(threadIdx.x) = 0;
   }
   // Hierarchical last-arriver all-reduce (flags mode): every CTA stores its partials and
   // takes a ticket of its group of kGrp CTAs; the group's last arriver sums the group's
@@ -402,7 +410,7 @@ struct GridSync {
     const int g = r / kGrp, g0 = g * kGrp, gn = min(kGrp, P - g0), NG = (P + kGrp - 1) / kGrp;
     if (t == 0) {
       __threadfence();
-      const unsigned tk = atomicAdd(&sw[g], 1u);
+      const unsigned tk = atomicAdd(&SW(g), 1u);
       s.wflag = tk == (unsigned)gn * gen - 1u ? 1 : 0;
     }
     __syncthreads();
@@ -423,7 +431,7 @@ struct GridSync {
       __syncthreads();
       if (t == 0) {
         __threadfence();
-        const unsigned tk = atomicAdd(&sw[kSwTop], 1u);
+        const unsigned tk = atomicAdd(&SW(kSwTop), 1u);
         s.wflag = tk == (unsigned)NG * gen - 1u ? 2 : 1;
       }
       __syncthreads();
@@ -445,13 +453,13 @@ struct GridSync {
         __syncthreads();
         if (t == 0) {
           __threadfence();
-          st_release_u32(&sw[kSwFlag], gen);
+          st_release_u32(&SW(kSwFlag), gen);
         }
         return;
       }
     }
     if (t == 0) {
-      while (ld_acquire_u32(&sw[kSwFlag]) < gen) {}
+      while (ld_acquire_u32(&SW(kSwFlag)) < gen) {}
       __threadfence();
     }
     __syncthreads();
@@ -481,7 +489,7 @@ struct GridSync {
         }
         out[i] = q;
       }
-    } else if (m <= kOnePhaseMax) {
+    } else if (m <= onephase) {
       // one grid barrier: every CTA sums all P partials of every element itself.
       // Thread t takes element e = t % m over ranks gi, gi + G, ... (gi = t / m,
       // G = kRT / m groups), the G sub-sums are then added in group order --
@@ -936,18 +944,26 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       // every CTA takes the same branch (identically reduced scalars).
       __syncthreads();
       cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, true, ph);
-      double nw = s.hv[j + 1].x, sh = 0.0;
-      for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
-      __syncthreads();
+      // sum |h_i|^2 on warp 0 (lane-strided, fixed shuffle tree: identical in every CTA)
+      auto sum_h2 = [&] {
+        if (t < 32) {
+          double a = 0.0;
+          for (int i = t; i <= j; i += 32) a += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+          if (t == 0) s.shv = a;
+        }
+        __syncthreads();
+        return s.shv;
+      };
+      double nw = s.hv[j + 1].x, sh = sum_h2();
       for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
       double est = nw - sh;
       if (!(est > 0.5 * nw)) {
         __syncthreads();
         cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, true, ph);
         nw = s.hv[j + 1].x;
-        sh = 0.0;
-        for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
-        __syncthreads();
+        sh = sum_h2();
         for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
         est = nw - sh;
       }
@@ -1169,7 +1185,7 @@ static int res_flags() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("HDB_RES_FLAGS");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 0;
   }
   return v;
 }
@@ -1618,7 +1634,7 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
 }
 
 __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, int j, long long n, cd* gpart,
-                                                   cd* hout, cd* Tg, const int* skip) {
+                                                   cd* hout, cd* Tg, const int* skip, int keep) {
   if (skip && *skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LsSmem& s = *reinterpret_cast<LsSmem*>(smem_raw);
@@ -1635,7 +1651,7 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
   auto chunk_pol = [&](int q) {
     const int v = q / kLsChunks;
-    return (v < j && v >= j - kLsKeep) ? pol_keep : pol_drop;
+    return (v < j && v >= j - keep) ? pol_keep : pol_drop;
   };
   auto chunk_src = [&](int q, int& bytes) -> const cd* {
     const int v = q / kLsChunks, c = q - v * kLsChunks;
@@ -1651,7 +1667,8 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     const cd* src = chunk_src(q, bytes);
     if (bytes > 0) {
       mbar_arm(&s.full[st], (uint32_t)bytes);
-      bulk_g2s_hint(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st], chunk_pol(q));
+      if (keep >= 0) bulk_g2s_hint(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st], chunk_pol(q));
+      else bulk_g2s(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st]);
     } else {
       mbar_arrive1(&s.full[st]);  // empty tail chunk: complete the phase without data
     }
@@ -1935,7 +1952,12 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
   if (tg && mgs_ls_fits(n, j)) {
     const size_t sm = mgs_ls_smem((n + g_grid - 1) / g_grid);
     if (!ensure_smem_attr((const void*)k_mgs_ls, sm)) return 1;
-    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip};
+    static const int keep = [] {  // HDB_LS_KEEP: pass-A vectors marked evict_last (-1: no L2 hints)
+      const char* e = getenv("HDB_LS_KEEP");
+      return e ? atoi(e) : kLsKeep;
+    }();
+    int kp = keep;
+    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip, &kp};
     return cudaLaunchCooperativeKernel((void*)k_mgs_ls, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
   }
   long long ks = 0;
