@@ -82,6 +82,30 @@ int hdb_op_create_slab(hdb_op** out, int nx, int ny_global, int radius, double h
                        const double* lap, const double* mass_re, const double* mass_im,
                        const double* ksq_full_host, int row0, int ny_local, int halo, int nranks,
                        const int* slab_row0, const int* slab_ny);
+/* the same operator from a k^2 field already on the device (GPU-side setup, below): the
+   field is range-checked (finite, nonnegative: grid.py:266-267) and copied device to
+   device; whole grid, one rank */
+int hdb_op_create_dev(hdb_op** out, int nx, int ny, int radius, double h, const int* bc4, const double* lap,
+                      const double* mass_re, const double* mass_im, const double* ksq_dev);
+
+/* ---- problem setup on the device; every field bit-identical to grid.py ----
+   k^2 = (w / c)^2 with w = 2 pi f at the vertices (ox + hx i, oy + hy j), row-major (ny, nx):
+   _fine_ksq grid.py:261-268; constant: the value itself; wedge: `nlayers` (y at first x, y at
+   last x, velocity) triples top to bottom, the last one the catch-all (grid.py:120-135);
+   raster: bilinear sampling of a device float64 raster (rny, rnx), origin (rx0, ry0), steps
+   (rdx, rdy), clamped (grid.py:138-160) */
+int hdb_setup_ksq_constant(double* out_dev, long long n, double ksq);
+int hdb_setup_ksq_wedge(double* out_dev, int nx, int ny, double ox, double oy, double hx, double hy, double w,
+                        int nlayers, const double* layers3);
+int hdb_setup_ksq_raster(double* out_dev, int nx, int ny, double ox, double oy, double hx, double hy, double w,
+                         const double* raster_dev, int rnx, int rny, double rx0, double ry0, double rdx, double rdy);
+/* coarse k^2 by injection at coincident vertices, ksq[::2, ::2] (grid.py:285) */
+int hdb_setup_inject(const double* fine_dev, int nfx, int nfy, double* coarse_dev);
+/* out3 = { min, max, number of non-finite values } of a device float64 array (finite values only) */
+int hdb_setup_stats(const double* a_dev, long long n, double* out3);
+/* point_source_rhs (grid.py:309-320): rhs = 0 except rhs[index] = value (= 1 / (hx hy)) */
+int hdb_setup_point_source(void* rhs_dev, long long n, long long index, double value);
+
 /* LevelOperator.apply (operators.py:130-147): out = A u, Dirichlet rows pinned */
 int hdb_op_apply(hdb_op* op, const void* u, void* out);
 /* out = b - A u  (MG residual mg.py:116, A-DEF1 v - A t madp.py:325-326) */
@@ -93,6 +117,15 @@ int hdb_op_residual(hdb_op* op, const void* b, const void* u, void* out);
 int hdb_op_resnorm(hdb_op* op, const void* b, const void* u, double* out2);
 /* one damped-Jacobi sweep (_kernels.py:53-68 + mg.py:88-102); x == NULL: from zero */
 int hdb_op_jacobi(hdb_op* op, const void* x, const void* b, void* out, double omega);
+/* fused MG coarse right-hand side (mg.py:116-117): coarse = Z^T (b - A u), coarse Dirichlet
+   rows zeroed per zero_mask (bit 0 west, 1 east, 2 south, 3 north); one pass, the residual is
+   not stored (44 B per fine point instead of 56 + 20); unsharded radius-1 operators;
+   bit-identical to hdb_op_residual followed by hdb_restrict */
+int hdb_op_residual_restrict(hdb_op* op, const void* b, const void* u, void* coarse, int zero_mask);
+/* the last post-smoothing sweep with the A-DEF1 sum folded in (mg.py:122 + madp.py:327):
+   out = Jacobi(x), out2 = out + addt; bit-identical to hdb_op_jacobi followed by the add */
+int hdb_op_jacobi_add(hdb_op* op, const void* x, const void* b, void* out, double omega, const void* addt,
+                      void* out2);
 
 /* ---- transfers: replaces restrict_array / prolong_array (transfers.py:59-88) */
 /* zero_mask bits 1 W, 2 E, 4 S, 8 N: coarse rows set to 0 (mg.py:118-119)  */

@@ -20,8 +20,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          f"-I{os.path.join(os.path.dirname(PKG), 'include')}"]
-SOURCES = ["kernels_stencil.cu", "kernels_transfer.cu", "kernels_blas.cu", "kernels_resident.cu", "engine.cu",
-           "comm.cu", "capi.cu"]
+SOURCES = ["kernels_stencil.cu", "kernels_transfer.cu", "kernels_blas.cu", "kernels_resident.cu", "kernels_setup.cu",
+           "engine.cu", "comm.cu", "capi.cu"]
 
 
 def _stale(force: bool) -> bool:

@@ -41,9 +41,18 @@ SIGNATURES = {
     "hdb_thread_engine_begin": [i32],
     "hdb_thread_engine_end": [],
     "hdb_op_apply": [vp, vp, vp],
+    "hdb_op_create_dev": [P(vp), i32, i32, i32, f64, P(i32), P(f64), P(f64), P(f64), vp],
+    "hdb_setup_ksq_constant": [vp, i64, f64],
+    "hdb_setup_ksq_wedge": [vp, i32, i32, f64, f64, f64, f64, f64, i32, P(f64)],
+    "hdb_setup_ksq_raster": [vp, i32, i32, f64, f64, f64, f64, f64, vp, i32, i32, f64, f64, f64, f64],
+    "hdb_setup_inject": [vp, i32, i32, vp],
+    "hdb_setup_stats": [vp, i64, P(f64)],
+    "hdb_setup_point_source": [vp, i64, i64, f64],
     "hdb_op_residual": [vp, vp, vp, vp],
     "hdb_op_resnorm": [vp, vp, vp, P(f64)],
     "hdb_op_jacobi": [vp, vp, vp, vp, f64],
+    "hdb_op_residual_restrict": [vp, vp, vp, vp, i32],
+    "hdb_op_jacobi_add": [vp, vp, vp, vp, f64, vp, vp],
     "hdb_restrict": [vp, i32, i32, vp, i32],
     "hdb_prolong": [vp, i32, i32, vp, vp],
     "hdb_dot": [vp, vp, i64, P(f64)],

@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/hdb200.h"
 #include "engine.h"
@@ -126,6 +127,92 @@ int hdb_op_create(hdb_op** out, int nx, int ny, int radius, double h, const int*
   });
 }
 
+// (min, max, non-finite count) of a device float64 array -> host
+static void device_stats(const double* a, long long n, double out3[3]) {
+  Engine& E = engine();
+  double* part = (double*)E.alloc_bytes(sizeof(double) * 3 * (size_t)(setup_stats_blocks(n) + 1));
+  double* res = part + 3 * (size_t)setup_stats_blocks(n);
+  launch_setup_stats(a, n, part, E.red.ticket, res, E.st);
+  HDB_CUDA(cudaMemcpyAsync(out3, res, sizeof(double) * 3, cudaMemcpyDeviceToHost, E.st));
+  HDB_CUDA(cudaStreamSynchronize(E.st));
+  E.free(part);
+}
+
+// the same operator from a k^2 field that already lives on the device (GPU-side setup:
+// no host copy of the level exists); whole grid, one rank
+int hdb_op_create_dev(hdb_op** out, int nx, int ny, int radius, double h, const int* bc4, const double* lap,
+                      const double* mass_re, const double* mass_im, const double* ksq_dev) {
+  return guarded([&] {
+    if (nx < 2 || ny < 2) throw Error(E_ARG, "grid needs at least 2 points per direction");
+    std::vector<double> dummy((size_t)nx * 2, 0.0);  // coefficients through the host path on a 2-row dummy field
+    hdb_op* o = nullptr;
+    const int st = hdb_op_create(&o, nx, 2, radius, h, bc4, lap, mass_re, mass_im, dummy.data());
+    if (st != HDB_OK) throw Error(st, g_err);
+    Engine& E = engine();
+    LevelOp& L = o->op;
+    E.free(L.ksq);
+    L.g.nx = nx; L.g.ny = ny; L.g.row0 = 0; L.g.nyg = ny;
+    L.n = (long long)nx * ny;
+    double st3[3];
+    device_stats(ksq_dev, L.n, st3);
+    if (st3[2] != 0.0 || st3[0] < 0.0) {
+      delete o;
+      throw Error(E_ARG, "k^2 field must be finite and nonnegative");
+    }
+    // constant k^2 (min == max): the per-tap coefficient table, as set_uniform builds it
+    const double ku[1] = {st3[0]};
+    L.c.uniform = 0;
+    if (st3[0] == st3[1]) set_uniform(L.c, ku, 1);
+    L.ksq = (double*)E.alloc_bytes(sizeof(double) * L.n);
+    HDB_CUDA(cudaMemcpyAsync(L.ksq, ksq_dev, sizeof(double) * L.n, cudaMemcpyDeviceToDevice, E.st));
+    HDB_CUDA(cudaStreamSynchronize(E.st));
+    *out = o;
+  });
+}
+
+// ---- device-side problem setup (grid.py:120-160, 261-287, 309-320) ----------------------
+int hdb_setup_ksq_constant(double* out_dev, long long n, double ksq) {
+  return guarded([&] { launch_setup_fill(out_dev, n, ksq, engine().st); check_launch(); });
+}
+int hdb_setup_ksq_wedge(double* out_dev, int nx, int ny, double ox, double oy, double hx, double hy, double w,
+                        int nlayers, const double* layers3) {
+  return guarded([&] {
+    if (nlayers < 1 || nlayers > 8) throw Error(E_ARG, "wedge model: 1..8 layers");
+    SetupLayers Ls;
+    Ls.n = nlayers;
+    for (int q = 0; q < nlayers; ++q) {
+      Ls.y0[q] = layers3[3 * q]; Ls.y1[q] = layers3[3 * q + 1]; Ls.v[q] = layers3[3 * q + 2];
+    }
+    launch_setup_wedge(out_dev, nx, ny, ox, oy, hx, hy, w, Ls, engine().st);
+    check_launch();
+  });
+}
+int hdb_setup_ksq_raster(double* out_dev, int nx, int ny, double ox, double oy, double hx, double hy, double w,
+                         const double* raster_dev, int rnx, int rny, double rx0, double ry0, double rdx, double rdy) {
+  return guarded([&] {
+    if (rnx < 1 || rny < 1) throw Error(E_ARG, "empty velocity raster");
+    launch_setup_raster(out_dev, nx, ny, ox, oy, hx, hy, w, raster_dev, rnx, rny, rx0, ry0, rdx, rdy, engine().st);
+    check_launch();
+  });
+}
+int hdb_setup_inject(const double* fine_dev, int nfx, int nfy, double* coarse_dev) {
+  return guarded([&] {
+    if ((nfx - 1) % 2 || (nfy - 1) % 2) throw Error(E_ARG, "cannot coarsen: n-1 must be even");
+    launch_setup_inject(fine_dev, nfx, coarse_dev, (nfx - 1) / 2 + 1, (nfy - 1) / 2 + 1, engine().st);
+    check_launch();
+  });
+}
+int hdb_setup_stats(const double* a_dev, long long n, double* out3) {
+  return guarded([&] { device_stats(a_dev, n, out3); check_launch(); });
+}
+int hdb_setup_point_source(void* rhs_dev, long long n, long long index, double value) {
+  return guarded([&] {
+    if (index < 0 || index >= n) throw Error(E_ARG, "source index outside the grid");
+    launch_setup_point((cd*)rhs_dev, n, index, value, engine().st);
+    check_launch();
+  });
+}
+
 // a row slab [row0, row0+ny_local) of a level with ny_global rows; `halo` rows of
 // k^2 are copied around it (from the full host array), vectors of this level
 // carry `halo` halo rows; slab_row0/slab_ny list every rank's slab.
@@ -226,6 +313,36 @@ int hdb_op_jacobi(hdb_op* op, const void* x, const void* b, void* out, double om
   return guarded([&] {
     if (op->op.c.radius != 1) throw Error(E_ARG, "Jacobi is only defined for radius-1 operators");
     op->op.jacobi((const cd*)x, (const cd*)b, (cd*)out, omega, x == nullptr);
+    check_launch();
+  });
+}
+
+int hdb_op_residual_restrict(hdb_op* op, const void* b, const void* u, void* coarse, int zero_mask) {
+  return guarded([&] {
+    const LevelOp& o = op->op;
+    if (o.c.radius != 1 || o.sharded) throw Error(E_ARG, "fused residual + restriction: unsharded radius-1 operators only");
+    if ((o.g.nx - 1) % 2 || (o.g.ny - 1) % 2 || o.g.nx < 3 || o.g.ny < 3)
+      throw Error(E_ARG, "cannot coarsen: n-1 must be even (transfers.py:53-56)");
+    Engine& E = engine();
+    E.kl(KF_RESRESTRICT, 44.0 * o.n, [&] {
+      launch_resrestrict(o.c, o.g, (const cd*)u, (const cd*)b, o.ksq, (cd*)coarse, zero_mask, E.st);
+    });
+    check_launch();
+  });
+}
+int hdb_op_jacobi_add(hdb_op* op, const void* x, const void* b, void* out, double omega, const void* addt,
+                      void* out2) {
+  return guarded([&] {
+    const LevelOp& o = op->op;
+    if (o.c.radius != 1) throw Error(E_ARG, "Jacobi is only defined for radius-1 operators");
+    if (!x || !addt || !out2) throw Error(E_ARG, "jacobi_add needs x, addt and out2");
+    if (o.jacobi_add_ok()) {
+      o.jacobi_add((const cd*)x, (const cd*)b, (cd*)out, omega, (const cd*)addt, (cd*)out2);
+    } else {  // small grids: the sweep, then the sum
+      o.jacobi((const cd*)x, (const cd*)b, (cd*)out, omega, false);
+      Engine& E = engine();
+      E.kl(KF_BLAS, 48.0 * o.n, [&] { launch_add((const cd*)out, (const cd*)addt, (cd*)out2, o.n, 0, E.st); });
+    }
     check_launch();
   });
 }

@@ -19,7 +19,7 @@ namespace hdb {
 const char* kfam_name(int f) {
   static const char* names[KF_COUNT] = {"apply5", "residual5", "jacobi5", "resnorm5", "galerkin", "restrict",
                                         "prolong", "mgs_coop", "mgs_chain", "blas1", "resident_gmres", "control",
-                                        "gemv"};
+                                        "gemv", "resrestrict"};
   return f >= 0 && f < KF_COUNT ? names[f] : "?";
 }
 
@@ -199,6 +199,12 @@ void LevelOp::jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_
   if (!from_zero) exchange(x, 1);
   E.kl(KF_JACOBI, (from_zero ? 40.0 : 56.0) * n, [&] { launch_jacobi(c, g, x, b, ksq, out, omega, from_zero, E.st); });
 }
+bool LevelOp::jacobi_add_ok() const { return c.radius == 1 && jacobi_add_fits(g); }
+void LevelOp::jacobi_add(const cd* x, const cd* b, cd* out, double omega, const cd* addt, cd* out2) const {
+  Engine& E = engine();
+  exchange(x, 1);
+  E.kl(KF_JACOBI, 88.0 * n, [&] { launch_jacobi_add(c, g, x, b, ksq, out, omega, addt, out2, E.st); });
+}
 
 // ----------------------------------------------------------- level transfers
 TGeom level_tgeom(const LevelOp& f, const LevelOp& c) {
@@ -374,7 +380,7 @@ void SmallSolve::ensure(const LevelOp* o, int cap_) {
   basis = E.alloc((long long)(cap + 1) * o->n);
   Rg = E.alloc((long long)cap * (cap + 1) / 2 + cap + (long long)(cap + 1) * (cap + 2) / 2);
   gpart = E.alloc(resident_gpart_elems());
-  HDB_CUDA(cudaMemsetAsync(gpart, 0, sizeof(cd) * (size_t)resident_gpart_elems(), E.st));  // sync words start at zero
+  HDB_CUDA(cudaMemsetAsync(gpart, 0, sizeof(cd) * (size_t)resident_gpart_elems(), E.st));
 }
 
 bool SmallSolve::try_run(const cd* b, cd* x, Stop stop, int* its_dev, double* rel_dev) {
@@ -923,7 +929,7 @@ Multigrid::~Multigrid() {
 // mg.py:111-123.  Input x is the zero vector at every level (vcycle starts
 // from x0 = 0 and the recursion passes zeros), so the first pre-smoothing
 // sweep is the closed form (w D^-1) b.  The result is written to x.
-void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
+void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init, const cd* addt, cd* xsum) {
   Engine& E = engine();
   const int L = (int)ops.size();
   if (i == L - 1) {  // mg.py:104-109
@@ -958,10 +964,17 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
   } else {
     HDB_CUDA(cudaMemsetAsync(cur, 0, sizeof(cd) * n, E.st));
   }
-  // coarse-grid correction
-  op->residual(b, cur, R[i]);
+  // coarse-grid correction: residual and restriction in one pass where the fused kernel
+  // applies (mg.py:116-117; bit-identical to the pair), else the two launches
   const LevelOp* co = ops[i + 1];
-  restrict_levels(*op, *co, R[i], B[i + 1], S[i + 1], dirichlet_mask(co->c));
+  if (!op->sharded && !co->sharded && resrestrict_fits(op->c, op->g)) {
+    E.kl(KF_RESRESTRICT, 44.0 * n, [&] {
+      launch_resrestrict(op->c, op->g, cur, b, op->ksq, B[i + 1], dirichlet_mask(co->c), E.st);
+    });
+  } else {
+    op->residual(b, cur, R[i]);
+    restrict_levels(*op, *co, R[i], B[i + 1], S[i + 1], dirichlet_mask(co->c));
+  }
   cycle(i + 1, B[i + 1], O[i + 1], nullptr);
   cd* dst = (post == 0) ? x : oth;
   prolong_levels(*co, *op, O[i + 1], cur, dst);
@@ -969,13 +982,17 @@ void Multigrid::cycle(int i, const cd* b, cd* x, const cd* x_init) {
   std::swap(cur, dst);  // cur = corrected iterate, dst = free buffer
   for (int s = 0; s < post; ++s) {
     cd* out = (s == post - 1) ? x : dst;
-    op->jacobi(cur, b, out, omega, false);
+    if (s == post - 1 && xsum) op->jacobi_add(cur, b, out, omega, addt, xsum);  // x and x + addt in one sweep
+    else op->jacobi(cur, b, out, omega, false);
     dst = cur;
     cur = out;
   }
 }
 
-void Multigrid::vcycle(const cd* b, cd* x, const cd* x0) {
+// the top level's last post-smoothing sweep can also write x + addt (madp.py:327)
+bool Multigrid::can_fold_sum() const { return post > 0 && ops.size() > 1 && ops[0]->jacobi_add_ok(); }
+
+void Multigrid::vcycle(const cd* b, cd* x, const cd* x0, const cd* addt, cd* xsum) {
   Engine& E = engine();
   if (X.empty()) setup();
   const LevelOp* op = ops[0];
@@ -985,7 +1002,7 @@ void Multigrid::vcycle(const cd* b, cd* x, const cd* x0) {
     E.kl(KF_BLAS, 16.0 * op->n, [&] { launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgR0, E.st); });
     op->reduce(E.dscal + kSlotMgR0);
   }
-  cycle(0, b, x, x0);
+  cycle(0, b, x, x0, addt, xsum);
   // divergence guard (mg.py:133-138), evaluated on device; raised at the next host sync.
   // One fused pass: (||b - M x||^2, ||b||^2) without storing the residual.
   op->resnorm(b, x, E.dscal + kSlotMgPost, R[0]);
@@ -1116,19 +1133,35 @@ void MadpSolver::A(int l, const cd* u, cd* out) {
 }
 
 // madp.py:277-299
-void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out) {
+void MadpSolver::cslp_apply(int l, const cd* rhs, cd* out, const cd* addt, cd* sum) {
   ProfScope ps(*this, l, PROF_CSLP);
   MadpLevel& L = lv[l];
   Engine& E = engine();
+  auto add_sum = [&] {  // sum = out + addt (madp.py:327) when the solve could not fold it in
+    if (sum) E.kl(KF_BLAS, 48.0 * L.A->n, [&] { launch_add(out, addt, sum, L.A->n, 0, E.st); });
+  };
   if (L.cslp == CSLP_NONE) {
     HDB_CUDA(cudaMemcpyAsync(out, rhs, sizeof(cd) * L.A->n, cudaMemcpyDeviceToDevice, E.st));
+    add_sum();
     return;
   }
   if (L.cslp == CSLP_MG) {
     rep.cslp_iters[l].push_back(1);
-    L.mg->vcycle(rhs, out);
+    if (sum && L.mg->can_fold_sum()) {
+      L.mg->vcycle(rhs, out, nullptr, addt, sum);
+    } else {
+      L.mg->vcycle(rhs, out);
+      add_sum();
+    }
     return;
   }
+  cslp_krylov(l, rhs, out);
+  add_sum();
+}
+
+// the Krylov forms of the CSLP solve (madp.py:288-297)
+void MadpSolver::cslp_krylov(int l, const cd* rhs, cd* out) {
+  MadpLevel& L = lv[l];
   const LevelOp* M = L.M;
   if (L.cslp == CSLP_BICGSTAB) {  // madp.py:292-297: a breakdown still yields a usable iterate
     LinOp Mop = [M](const cd* in, cd* o) { M->apply(in, o); };
@@ -1220,8 +1253,7 @@ void MadpSolver::precond(int l, const cd* v, cd* out) {
   prolong_levels(*N.A, *L.A, N.vtil, nullptr, L.t);
   rep.matvecs[l] += 1;
   L.A->residual(v, L.t, L.rhs);  // v - A t
-  cslp_apply(l, L.rhs, L.r);
-  E.kl(KF_BLAS, 48.0 * L.A->n, [&] { launch_add(L.r, L.t, out, L.A->n, 0, E.st); });  // r + t
+  cslp_apply(l, L.rhs, L.r, L.t, out);  // r = CSLP(rhs); out = r + t
 }
 
 void MadpSolver::solve(const cd* b, cd* x) {

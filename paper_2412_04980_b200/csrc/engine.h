@@ -55,6 +55,7 @@ enum KFam {
   KF_RESIDENT,     // device-resident GMRES solves (bytes from their iteration counts)
   KF_CONTROL,      // Givens, least squares, guards, flags (no field traffic)
   KF_GEMV,         // dense inverse at the multigrid bottom, 16 n^2 B
+  KF_RESRESTRICT,  // fused MG residual + restriction, 44 B per fine pt
   KF_COUNT
 };
 const char* kfam_name(int f);
@@ -168,6 +169,9 @@ struct LevelOp {
   void apply(const cd* u, cd* out) const;                 // out = A u
   void residual(const cd* b, const cd* u, cd* out) const;  // out = b - A u
   void jacobi(const cd* x, const cd* b, cd* out, double omega, bool from_zero) const;
+  // one sweep writing out = Jacobi(x) and out2 = out + addt (large radius-1 levels)
+  bool jacobi_add_ok() const;
+  void jacobi_add(const cd* x, const cd* b, cd* out, double omega, const cd* addt, cd* out2) const;
   // slot = (||b - A u||^2, ||b||^2), reduced over the distribution; `scratch`
   // (a level vector) is used only by the unfused radius-2/3 form
   void resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const;
@@ -283,8 +287,11 @@ struct Multigrid {
   double omega = 0.8, guard = 10.0;
   int pre = 1, post = 1;
   void setup();
-  void vcycle(const cd* b, cd* x, const cd* x0 = nullptr);  // mg.py:125-139 (guard -> device flag)
-  void cycle(int i, const cd* b, cd* x, const cd* x_init);
+  // mg.py:125-139 (guard -> device flag); xsum != null: also xsum = x + addt (folded into
+  // the last post-smoothing sweep; needs can_fold_sum())
+  void vcycle(const cd* b, cd* x, const cd* x0 = nullptr, const cd* addt = nullptr, cd* xsum = nullptr);
+  void cycle(int i, const cd* b, cd* x, const cd* x_init, const cd* addt = nullptr, cd* xsum = nullptr);
+  bool can_fold_sum() const;
   ~Multigrid();
 };
 
@@ -344,7 +351,9 @@ struct MadpSolver {
   void set_levels(int ml_);
   void reset_report();
   void setup();
-  void cslp_apply(int l, const cd* rhs, cd* out);
+  // out = CSLP_l(rhs); sum != null: also sum = out + addt (the A-DEF1 r + t)
+  void cslp_apply(int l, const cd* rhs, cd* out, const cd* addt = nullptr, cd* sum = nullptr);
+  void cslp_krylov(int l, const cd* rhs, cd* out);
   void precond(int l, const cd* v, cd* out);
   void A(int l, const cd* u, cd* out);
   void solve(const cd* b, cd* x);

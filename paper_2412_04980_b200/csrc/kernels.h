@@ -21,8 +21,16 @@ void launch_apply(const OpCoef& c, const Geom& g, const cd* u, const cd* b, cons
 long long resnorm_partials(const Geom& g);  // partial slots launch_resnorm needs
 void launch_resnorm(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* partials,
                     cd* dst, cudaStream_t st);
+// radius 1, unsharded: coarse = Z^T (b - A u) with coarse Dirichlet rows zeroed, one pass (mg.py:116-117)
+bool resrestrict_fits(const OpCoef& c, const Geom& g);
+void launch_resrestrict(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* coarse,
+                        int zero_mask, cudaStream_t st);
 void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out, double omega,
                    bool from_zero, cudaStream_t st);
+// Jacobi sweep with a second output out2 = out + addt (A-DEF1 r + t folded into the last post-smooth)
+bool jacobi_add_fits(const Geom& g);
+void launch_jacobi_add(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out,
+                       double omega, const cd* addt, cd* out2, cudaStream_t st);
 // transfer geometry: fine rows [f_row0, f_row0+f_ny) of nfy_g, coarse rows [c_row0, c_row0+c_ny) of ncy_g
 struct TGeom {
   int nfx, f_row0, f_ny, nfy_g;
@@ -31,6 +39,22 @@ struct TGeom {
 TGeom full_tgeom(int nfx, int nfy);
 void launch_restrict(const cd* fine, cd* coarse, const TGeom& t, int zero_mask, cudaStream_t st);
 void launch_prolong(const cd* coarse, const cd* base, cd* fine, const TGeom& t, int accumulate, cudaStream_t st);
+
+// device-side problem setup (kernels_setup.cu; grid.py:120-160, 261-287, 309-320)
+struct SetupLayers {
+  int n;
+  double y0[8], y1[8], v[8];
+};
+void launch_setup_fill(double* out, long long n, double v, cudaStream_t st);
+void launch_setup_wedge(double* out, int nx, int ny, double ox, double oy, double hx, double hy, double w,
+                        const SetupLayers& L, cudaStream_t st);
+void launch_setup_raster(double* out, int nx, int ny, double ox, double oy, double hx, double hy, double w,
+                         const double* g, int rnx, int rny, double rx0, double ry0, double rdx, double rdy,
+                         cudaStream_t st);
+void launch_setup_inject(const double* fine, int nfx, double* coarse, int ncx, int ncy, cudaStream_t st);
+int setup_stats_blocks(long long n);
+void launch_setup_stats(const double* a, long long n, double* part, unsigned* ticket, double* out3, cudaStream_t st);
+void launch_setup_point(cd* rhs, long long n, long long idx, double v, cudaStream_t st);
 
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st);
 void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st);
@@ -54,7 +78,7 @@ long long resident_cluster_points();
 long long resident_grid_points();
 int resident_grid_ctas();
 int resident_vec_cap();
-long long resident_gpart_elems();  // SmallSolve::gpart size (zeroed at allocation: it holds sync words)
+long long resident_gpart_elems();  // SmallSolve::gpart size (grid-reduction partials and sums)
 void resident_set_profile(long long* dev_counters);
 // one Arnoldi step's MGS chain in a cooperative launch (large levels); 1 = does not fit
 // tg != null: the low-synchronisation form (two grid reductions per step) where the

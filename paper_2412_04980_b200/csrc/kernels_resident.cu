@@ -56,19 +56,8 @@ struct ResidentArgs {
   int tile_elems;     // window elements (max over CTAs)
   int sbasis;         // 1: this CTA's basis slices also kept in shared memory (dots / updates read them)
   int sstride;        // their stride (points per CTA, rounded up)
-  unsigned* sw;       // GridSync sync words (zero between launches; kSw* layout), may be null
-  int flags;          // GridSync: 1 = neighbour flags + hierarchical last-arriver reductions
+  int rsm;            // 1: the packed R factor is also kept in shared memory (least squares reads it there)
 };
-
-// GridSync sync-word layout (unsigned, zeroed at allocation, reset by every launch at exit)
-constexpr int kGrp = 16;          // CTAs per reduction group
-constexpr int kMaxGroups = 10;    // 160 CTAs
-constexpr int kSwTop = 16;        // arrivals of group last-arrivers
-constexpr int kSwFlag = 17;       // generation of the last published reduction
-constexpr int kSwReady = 32;      // [32, 32 + P): vectors published by CTA r
-constexpr int kSwLine = 32;       // one sync word per 128-byte line (no false sharing between spinners and atomics)
-constexpr int kSwWords = (32 + 160) * kSwLine;
-#define SW(i) sw[(i) * kSwLine]
 
 // phase clock (CTA 0, thread 0) — only when A.prof != nullptr
 #define PHASE(k)                                                   \
@@ -102,18 +91,7 @@ struct RSmem {
   double cs[kMaxCap];
   cd g[kMaxCap + 2];
   int decision;
-  int wflag;                  // last-arriver role of this CTA in the current reduction
-  double shv;                 // sum |h_i|^2 (DGKS), broadcast
 };
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 template <int R>
 __device__ __forceinline__ cd op_point(const OpCoef& c, const Geom& g, const cd* u, const double* k, int gj, int i) {
@@ -322,12 +300,6 @@ struct ClusterSync {
     return s.bcast[0];
   }
   __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd*) { gather_sum(s, m, out, buf); }
-  // vector publication / window wait: one cluster barrier (DSMEM peers see global writes after it)
-  __device__ void publish(unsigned) {}
-  __device__ void wait_window(unsigned) { cl.sync(); }
-  __device__ void set_window(long long, long long, long long) {}
-  __device__ void setup(unsigned*, int) {}
-  __device__ void reset() {}
 };
 
 constexpr int kGridRounds = 5;  // ceil(148 SMs / 32): partial loads per lane in the grid reductions
@@ -337,144 +309,15 @@ struct GridSync {
   static constexpr bool kGather = false;
   static constexpr int kVecMax = kVecCap;
   cg::grid_group gr;
-  unsigned* sw = nullptr;  // sync words (flags mode)
-  int fl = 0;              // 1: neighbour flags + hierarchical last-arriver reductions
-  unsigned gen = 0;        // reductions done by this CTA (identical sequence in every CTA)
-  int onephase = kOnePhaseMax;  // largest m reduced with one barrier (all-to-all partial reads)
-  int wlo = 0, whi = -1;   // ranks whose slices intersect this CTA's stencil window
   __device__ GridSync() : gr(cg::this_grid()) {}
   __device__ int rank() const { return (int)blockIdx.x; }
   __device__ int nranks() const { return (int)gridDim.x; }
   __device__ void barrier() { gr.sync(); }
   __device__ void init(RSmem&, void*) {}
-  __device__ void setup(unsigned* sw_, int flags) {
-    sw = sw_;
-    fl = (sw_ && (flags & 1) && gridDim.x <= kGrp * kMaxGroups) ? 1 : 0;
-    if (flags & 2) onephase = 4;  // two-barrier reduce-scatter / all-gather from m = 5
-  }
-  // window point range [lo, hi) -> the ranks owning it (slices [n r / P, n (r + 1) / P))
-  __device__ void set_window(long long lo, long long hi, long long n) {
-    const int P = nranks();
-    auto owner = [&](long long p) {
-      int r = (int)((p * P) / n);
-      while (r + 1 < P && n * (r + 1) / P <= p) ++r;
-      while (r > 0 && n * r / P > p) --r;
-      return r;
-    };
-    wlo = owner(lo);
-    whi = owner(hi - 1);
-  }
-  // this CTA's slice of vector #val-1 is written (all threads): release it to the readers
-  __device__ void publish(unsigned val) {
-    if (!fl) return;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      st_release_u32(&SW(kSwReady + blockIdx.x), val);
-    }
-  }
-  // wait until every rank of the stencil window has published `val` vectors (flags mode),
-  // else a grid barrier.  The fence of the waiting threads also drops stale L1 lines.
-  __device__ void wait_window(unsigned val) {
-    if (!fl) {
-      gr.sync();
-      return;
-    }
-    const int r = wlo + (int)threadIdx.x;
-    if (r <= whi) {
-      while (ld_acquire_u32(&SW(kSwReady + r)) < val) {}
-      __threadfence();
-    }
-    __syncthreads();
-  }
-  // after the final barrier: zero the sync words for the next launch on this buffer
-  __device__ void reset() {
-    if (!sw) return;
-    if (threadIdx.x == 0) SW(kSwReady + blockIdx.x) = 0;
-    if (blockIdx.x == 0 && threadIdx.x < kSwReady) SW(threadIdx.x) = 0;
-  }
-  // Hierarchical last-arriver all-reduce (flags mode): every CTA stores its partials and
-  // takes a ticket of its group of kGrp CTAs; the group's last arriver sums the group's
-  // partials in rank order and takes a ticket at the top; the last group sums the group
-  // sums in group order, publishes them and releases the generation flag that everyone
-  // else spins on.  One grid-wide arrival wave instead of a barrier plus an all-to-all
-  // read of P x m partials; fixed summation order, identical sums in every CTA.
-  __device__ void reduce_vec_h(RSmem& s, int m, cd* out, cd* gpart) {
-    const int P = nranks(), r = blockIdx.x, t = threadIdx.x;
-    cd* col = gpart;
-    cd* gsum = gpart + (2LL * P + 2) * kVecCap;
-    cd* fsum = gsum + (long long)kMaxGroups * kVecCap;
-    ++gen;
-    for (int i = t; i < m; i += kRT) __stcg(&col[(long long)r * kVecCap + i], s.pv[i]);
-    __syncthreads();
-    const int g = r / kGrp, g0 = g * kGrp, gn = min(kGrp, P - g0), NG = (P + kGrp - 1) / kGrp;
-    if (t == 0) {
-      __threadfence();
-      const unsigned tk = atomicAdd(&SW(g), 1u);
-      s.wflag = tk == (unsigned)gn * gen - 1u ? 1 : 0;
-    }
-    __syncthreads();
-    if (s.wflag) {
-      __threadfence();
-      for (int i = t; i < m; i += kRT) {
-        cd z[kGrp];
-#pragma unroll
-        for (int u = 0; u < kGrp; ++u) z[u] = u < gn ? __ldcg(&col[(long long)(g0 + u) * kVecCap + i]) : mkc(0.0, 0.0);
-        cd q = mkc(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < kGrp; ++u) {
-          q.x += z[u].x;
-          q.y += z[u].y;
-        }
-        __stcg(&gsum[(long long)g * kVecCap + i], q);
-      }
-      __syncthreads();
-      if (t == 0) {
-        __threadfence();
-        const unsigned tk = atomicAdd(&SW(kSwTop), 1u);
-        s.wflag = tk == (unsigned)NG * gen - 1u ? 2 : 1;
-      }
-      __syncthreads();
-      if (s.wflag == 2) {
-        __threadfence();
-        for (int i = t; i < m; i += kRT) {
-          cd z[kMaxGroups];
-#pragma unroll
-          for (int u = 0; u < kMaxGroups; ++u) z[u] = u < NG ? __ldcg(&gsum[(long long)u * kVecCap + i]) : mkc(0.0, 0.0);
-          cd q = mkc(0.0, 0.0);
-#pragma unroll
-          for (int u = 0; u < kMaxGroups; ++u) {
-            q.x += z[u].x;
-            q.y += z[u].y;
-          }
-          __stcg(&fsum[i], q);
-          out[i] = q;
-        }
-        __syncthreads();
-        if (t == 0) {
-          __threadfence();
-          st_release_u32(&SW(kSwFlag), gen);
-        }
-        return;
-      }
-    }
-    if (t == 0) {
-      while (ld_acquire_u32(&SW(kSwFlag)) < gen) {}
-      __threadfence();
-    }
-    __syncthreads();
-    for (int i = t; i < m; i += kRT) out[i] = __ldcg(&fsum[i]);
-    __syncthreads();
-  }
   // s.pv[0..m) -> out[0..m), fixed rank order.  Two phases when m is large:
   // CTA i sums element i over the P partials (one column each), publishes it,
   // then every CTA reads the m sums; small m: every CTA sums everything itself.
   __device__ void reduce_vec(RSmem& s, int m, cd* out, int& buf, cd* gpart) {
-    if (fl) {
-      reduce_vec_h(s, m, out, gpart);
-      buf ^= 1;
-      return;
-    }
     const int P = nranks();
     cd* col = gpart + (long long)buf * P * kVecCap;
     for (int i = threadIdx.x; i < m; i += blockDim.x) __stcg(&col[(long long)blockIdx.x * kVecCap + i], s.pv[i]);
@@ -489,7 +332,7 @@ struct GridSync {
         }
         out[i] = q;
       }
-    } else if (m <= onephase) {
+    } else if (m <= kOnePhaseMax) {
       // one grid barrier: every CTA sums all P partials of every element itself.
       // Thread t takes element e = t % m over ranks gi, gi + G, ... (gi = t / m,
       // G = kRT / m groups), the G sub-sums are then added in group order --
@@ -551,14 +394,6 @@ struct GridSync {
   }
   __device__ cd reduce(cd v, RSmem& s, int& buf, cd* gpart) {
     const cd t = block_partial(v, s);
-    if (fl) {
-      if (threadIdx.x == 0) s.pv[0] = t;
-      __syncthreads();
-      reduce_vec_h(s, 1, &s.bcast[buf], gpart);
-      const cd r = s.bcast[buf];
-      buf ^= 1;
-      return r;
-    }
     const int P = nranks();
     if (threadIdx.x == 0) __stcg(&gpart[((long long)buf * P + blockIdx.x) * kVecCap], t);
     gr.sync();
@@ -748,7 +583,6 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   constexpr size_t kHead = ((sizeof(RSmem) + 15) / 16) * 16 + (Sync::kGather ? sizeof(GatherBuf) : 0);
   Sync sy;
   sy.init(s, smem_raw + ((sizeof(RSmem) + 15) / 16) * 16);
-  sy.setup(A.sw, A.flags);
   const int P = sy.nranks(), rank = sy.rank();
   const long long n = A.n;
   const long long p0 = n * rank / P, p1 = n * (rank + 1) / P;
@@ -756,17 +590,6 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   const long long chunk_max = (n + P - 1) / P;
   cd* ws = reinterpret_cast<cd*>(smem_raw + kHead);  // this CTA's slice of w
   const Tile T = make_tile<R>(A.g, p0, p1);
-  if (cnt > 0) {
-    const long long wa = (long long)(T.rlo - R - A.g.row0) * A.g.nx, wb = wa + (long long)T.rows * A.g.nx;
-    const long long wlo = wa > 0 ? wa : 0, whi = wb < n ? wb : n;
-    sy.set_window(wlo, whi, n);
-  }
-  // every exit: a final barrier (no CTA leaves while a peer may still address its shared
-  // memory or wait on its flags), then the sync words are zeroed for the next launch
-  auto finish = [&] {
-    sy.barrier();
-    sy.reset();
-  };
   cd* ut = A.tiled ? ws + chunk_max : nullptr;                 // stencil window of the current vector
   double* kt = A.tiled ? reinterpret_cast<double*>(ut + A.tile_elems) : nullptr;  // k^2 window (constant)
   // optional shared-memory copy of this CTA's basis slices (after the windows, 16-B aligned)
@@ -774,6 +597,14 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   if (A.sbasis) {
     const size_t off = ((size_t)(reinterpret_cast<unsigned char*>(kt + A.tile_elems) - smem_raw) + 15) / 16 * 16;
     sb = reinterpret_cast<cd*>(smem_raw + off);
+  }
+  // optional shared-memory copy of the packed R factor (after the basis slices / windows):
+  // the back substitution's dependent chain then reads shared memory instead of L2
+  cd* Rs = nullptr;
+  if (A.rsm) {
+    const unsigned char* end = sb ? reinterpret_cast<unsigned char*>(sb + (size_t)(A.cap + 1) * A.sstride)
+                                  : reinterpret_cast<unsigned char*>(kt + A.tile_elems);
+    Rs = reinterpret_cast<cd*>(smem_raw + ((size_t)(end - smem_raw) + 15) / 16 * 16);
   }
   if (A.tiled && cnt > 0) load_k_tile<R>(kt, T, A.ksq, A.g, A.c);
   const cd* ucoef = nullptr;
@@ -810,12 +641,12 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   if (bnorm == 0.0) {  // krylov.py:96-97
     for (int q = t; q < cnt; q += kRT) A.x[p0 + q] = mkc(0.0, 0.0);
     if (rank == 0 && t == 0) { *A.its_out = 0; *A.relres_out = 0.0; }
-    finish();
+    sy.barrier();
     return;
   }
   if (!isfinite(bnorm)) {
     if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = 0; }
-    finish();
+    sy.barrier();
     return;
   }
   const double beta = bnorm;  // r0 = b (zero initial guess); rel = 1 never triggers the early exit
@@ -837,7 +668,6 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   // overlapping that serial work with everybody else's stencil points.
   auto apply_M = [&](int jv, int givens_j, double hn_prev) {
     const cd* vj = V(jv);
-    sy.wait_window((unsigned)(jv + 1));  // V_jv complete over this CTA's window
     if (A.tiled) {
       if (cnt > 0) load_u_tile<R>(ut, T, vj, A.ksq, A.g, A.c);
       __syncthreads();
@@ -885,7 +715,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       const cd sh = cmul_(sn, h2);
       col[j] = mkc(c * h1.x + sh.x, c * h1.y + sh.y);
       if (rank == 0) {
-        cd* Rc = Rg + (long long)j * (j + 1) / 2;
+        cd* Rc = (Rs ? Rs : Rg) + (long long)j * (j + 1) / 2;
         for (int i = 0; i <= j; ++i) Rc[i] = col[i];
       }
       const cd gj = s.g[j];
@@ -905,7 +735,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     }
     __syncthreads();
   };
-  sy.publish(1u);  // V_0 written (the window wait in apply_M completes it)
+  sy.barrier();  // V_0 complete everywhere
   apply_M(0, -1, 0.0);
   PHASE(1);
   int dec = 0;
@@ -944,26 +774,18 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       // every CTA takes the same branch (identically reduced scalars).
       __syncthreads();
       cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, true, ph);
-      // sum |h_i|^2 on warp 0 (lane-strided, fixed shuffle tree: identical in every CTA)
-      auto sum_h2 = [&] {
-        if (t < 32) {
-          double a = 0.0;
-          for (int i = t; i <= j; i += 32) a += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
-          if (t == 0) s.shv = a;
-        }
-        __syncthreads();
-        return s.shv;
-      };
-      double nw = s.hv[j + 1].x, sh = sum_h2();
+      double nw = s.hv[j + 1].x, sh = 0.0;
+      for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
+      __syncthreads();
       for (int i = t; i <= j; i += kRT) s.hcol[i] = s.hv[i];
       double est = nw - sh;
       if (!(est > 0.5 * nw)) {
         __syncthreads();
         cgs_pass(sy, s, ws, vb, vs, cnt, j + 1, buf, A.gpart, true, ph);
         nw = s.hv[j + 1].x;
-        sh = sum_h2();
+        sh = 0.0;
+        for (int i = 0; i <= j; ++i) sh += s.hv[i].x * s.hv[i].x + s.hv[i].y * s.hv[i].y;
+        __syncthreads();
         for (int i = t; i <= j; i += kRT) s.hcol[i] = c_add(s.hcol[i], s.hv[i]);
         est = nw - sh;
       }
@@ -987,7 +809,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
       vn[q] = u;
       if (sn1) sn1[q] = u;
     }
-    sy.publish((unsigned)(j + 2));  // V_{j+1}: its readers wait in apply_M
+    sy.barrier();  // V_{j+1} complete everywhere
     PHASE(5);
     // Givens of step j on thread 0 while the stencil of step j+1 runs
     apply_M(j + 1, j, hn);
@@ -998,18 +820,33 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
   }
   if (dec == 2) {
     if (rank == 0 && t == 0) { A.flag->x = 2.0; *A.its_out = its; }
-    finish();
+    sy.barrier();
     return;
   }
   // least squares (krylov.py:161-168) on rank 0, y broadcast through global memory
   if (rank == 0 && t == 0) {
-    for (int i = its - 1; i >= 0; --i) {
-      cd accy = s.g[i];
-      for (int k = i + 1; k < its; ++k) {
-        const cd pr = cmul_(Rg[(long long)k * (k + 1) / 2 + i], yg[k]);
-        accy = mkc(accy.x - pr.x, accy.y - pr.y);
+    if (Rs) {  // R and y in shared memory (s.pv is free here): same operations in the same order
+      cd* ys = s.pv;
+      const bool ysh = its <= kVecCap;
+      for (int i = its - 1; i >= 0; --i) {
+        cd accy = s.g[i];
+        for (int k = i + 1; k < its; ++k) {
+          const cd pr = cmul_(Rs[(long long)k * (k + 1) / 2 + i], ysh ? ys[k] : yg[k]);
+          accy = mkc(accy.x - pr.x, accy.y - pr.y);
+        }
+        const cd yi = cdiv_(accy, Rs[(long long)i * (i + 1) / 2 + i]);
+        if (ysh) ys[i] = yi;
+        yg[i] = yi;
       }
-      yg[i] = cdiv_(accy, Rg[(long long)i * (i + 1) / 2 + i]);
+    } else {
+      for (int i = its - 1; i >= 0; --i) {
+        cd accy = s.g[i];
+        for (int k = i + 1; k < its; ++k) {
+          const cd pr = cmul_(Rg[(long long)k * (k + 1) / 2 + i], yg[k]);
+          accy = mkc(accy.x - pr.x, accy.y - pr.y);
+        }
+        yg[i] = cdiv_(accy, Rg[(long long)i * (i + 1) / 2 + i]);
+      }
     }
   }
   sy.barrier();
@@ -1052,7 +889,7 @@ __global__ void __launch_bounds__(kRT) k_resident_gmres(ResidentArgs A) {
     *A.relres_out = fin;
     if (!isfinite(fin)) A.flag->x = 2.0;
   }
-  finish();
+  sy.barrier();  // no CTA leaves while a peer may still address its shared memory
 }
 
 // ------------------------------------------------------------------ launch
@@ -1090,6 +927,22 @@ static size_t with_sbasis(ResidentArgs& a, size_t sm, long long chunk, size_t li
   const size_t extra = 16 + (size_t)(a.cap + 1) * (size_t)chunk * sizeof(cd);
   if (on && sm + extra <= limit) {
     a.sbasis = 1;
+    return sm + extra;
+  }
+  return sm;
+}
+
+// add the shared-memory R factor (cap (cap + 1) / 2 entries) when it fits (HDB_RES_RSM=0 disables)
+static size_t with_rsm(ResidentArgs& a, size_t sm, size_t limit) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("HDB_RES_RSM");
+    on = e ? atoi(e) : 1;
+  }
+  a.rsm = 0;
+  const size_t extra = 16 + (size_t)a.cap * (a.cap + 1) / 2 * sizeof(cd);
+  if (on && sm + extra <= limit) {
+    a.rsm = 1;
     return sm + extra;
   }
   return sm;
@@ -1148,6 +1001,7 @@ static bool launch_cluster(const ResidentArgs& a, cudaStream_t st) {
   b.tiled = sm <= g_smem_optin;
   if (!b.tiled) return false;  // untiled resident solves lose to the launch path
   sm = with_sbasis(b, sm, chunk, g_smem_optin);
+  sm = with_rsm(b, sm, g_smem_optin);
   set_attrs(kern, sm, true);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -1175,26 +1029,9 @@ static int grid_ctas_for(long long n) {
   return (int)std::max(16LL, std::min<long long>(g_grid, p));
 }
 
-// partials + group/final sums (cd elements), then the sync words
-constexpr long long kSwOffset = (2LL * kGrp * kMaxGroups + 2 + kMaxGroups + 1) * kVecCap;
-long long resident_gpart_elems() { return kSwOffset + (kSwWords * 4 + 15) / 16; }
-
-// HDB_RES_FLAGS=0: grid barriers + all-to-all partial reads (the r02 form) instead of the
-// neighbour flags and hierarchical last-arriver reductions
-static int res_flags() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HDB_RES_FLAGS");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 template <int R, int O>
 static bool launch_grid(ResidentArgs a, cudaStream_t st) {
   auto kern = k_resident_gmres<GridSync, R, O>;
-  a.sw = reinterpret_cast<unsigned*>(a.gpart + kSwOffset);
-  a.flags = res_flags();
   const int P = grid_ctas_for(a.n);
   const long long chunk = (a.n + P - 1) / P;
   a.tile_elems = tile_elems_for(a.n, a.g.nx, P, R);
@@ -1202,6 +1039,7 @@ static bool launch_grid(ResidentArgs a, cudaStream_t st) {
   a.tiled = sm <= g_smem_optin;
   if (!a.tiled) return false;  // untiled resident solves lose to the launch path
   sm = with_sbasis(a, sm, chunk, g_smem_optin);
+  sm = with_rsm(a, sm, g_smem_optin);
   set_attrs(kern, sm, false);
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRT, sm) != cudaSuccess || per_sm < 1) {
@@ -1223,6 +1061,8 @@ long long mgs_global_tier_bytes() {
   return v;
 }
 int resident_vec_cap() { return kVecCap - 1; }  // gpart stride - 1
+// SmallSolve::gpart size: two buffers of per-CTA partial vectors plus the published sums
+long long resident_gpart_elems() { return 2LL * resident_grid_ctas() * kVecCap + 2LL * kVecCap; }
 
 long long resident_cluster_points() {
   init_limits();
@@ -1634,7 +1474,7 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
 }
 
 __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, int j, long long n, cd* gpart,
-                                                   cd* hout, cd* Tg, const int* skip, int keep) {
+                                                   cd* hout, cd* Tg, const int* skip) {
   if (skip && *skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LsSmem& s = *reinterpret_cast<LsSmem*>(smem_raw);
@@ -1651,7 +1491,7 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   const uint64_t pol_keep = l2_policy_evict_last(), pol_drop = l2_policy_evict_first();
   auto chunk_pol = [&](int q) {
     const int v = q / kLsChunks;
-    return (v < j && v >= j - keep) ? pol_keep : pol_drop;
+    return (v < j && v >= j - kLsKeep) ? pol_keep : pol_drop;
   };
   auto chunk_src = [&](int q, int& bytes) -> const cd* {
     const int v = q / kLsChunks, c = q - v * kLsChunks;
@@ -1667,8 +1507,7 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
     const cd* src = chunk_src(q, bytes);
     if (bytes > 0) {
       mbar_arm(&s.full[st], (uint32_t)bytes);
-      if (keep >= 0) bulk_g2s_hint(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st], chunk_pol(q));
-      else bulk_g2s(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st]);
+      bulk_g2s_hint(ring + (size_t)st * kLsChunk, src, (uint32_t)bytes, &s.full[st], chunk_pol(q));
     } else {
       mbar_arrive1(&s.full[st]);  // empty tail chunk: complete the phase without data
     }
@@ -1952,12 +1791,7 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
   if (tg && mgs_ls_fits(n, j)) {
     const size_t sm = mgs_ls_smem((n + g_grid - 1) / g_grid);
     if (!ensure_smem_attr((const void*)k_mgs_ls, sm)) return 1;
-    static const int keep = [] {  // HDB_LS_KEEP: pass-A vectors marked evict_last (-1: no L2 hints)
-      const char* e = getenv("HDB_LS_KEEP");
-      return e ? atoi(e) : kLsKeep;
-    }();
-    int kp = keep;
-    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip, &kp};
+    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip};
     return cudaLaunchCooperativeKernel((void*)k_mgs_ls, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
   }
   long long ks = 0;

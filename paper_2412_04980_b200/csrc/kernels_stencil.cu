@@ -78,10 +78,13 @@ __device__ __forceinline__ cd interior_dinv(const OpCoef& c, double kc) {
 constexpr int SX = 32, SY = 4, RB = 16;  // block 32x4 threads, 16 rows per thread
 
 // one output by the per-point closure path (boundaries, ragged edges, pinned rows)
+// MODE 4: the Jacobi sweep of MODE 2 plus a second output out2 = result + addt
+// (the A-DEF1 sum r + t, madp.py:327, folded into the last post-smoothing sweep)
 template <int MODE>
 __device__ __forceinline__ void r1_point(const cd* __restrict__ u, const cd* __restrict__ b,
                                          const double* __restrict__ k, cd* __restrict__ out, const Geom& g,
-                                         const OpCoef& c, double omega, int i, int j) {
+                                         const OpCoef& c, double omega, int i, int j,
+                                         const cd* __restrict__ addt = nullptr, cd* __restrict__ out2 = nullptr) {
   const int gj = j + g.row0;
   const long long p = (long long)j * g.nx + i;
   if (MODE == 3) {
@@ -94,7 +97,11 @@ __device__ __forceinline__ void r1_point(const cd* __restrict__ u, const cd* __r
   if (pinned(g, c, gj, i)) {
     if (MODE == 0) out[p] = uc;
     else if (MODE == 1) out[p] = c_sub(b[p], uc);
-    else out[p] = c_add(uc, c_scale(omega, c_sub(b[p], uc)));
+    else {
+      const cd res = c_add(uc, c_scale(omega, c_sub(b[p], uc)));
+      out[p] = res;
+      if (MODE == 4) out2[p] = c_add(res, addt[p]);
+    }
     return;
   }
   const cd Au = five_point(c.s, c.mc, k[p], uc, upad(u, k, g, c, gj, i - 1), upad(u, k, g, c, gj, i + 1),
@@ -102,7 +109,9 @@ __device__ __forceinline__ void r1_point(const cd* __restrict__ u, const cd* __r
   if (MODE == 0) { out[p] = Au; return; }
   const cd r1 = c_sub(b[p], Au);
   if (MODE == 1) { out[p] = r1; return; }
-  out[p] = c_add(uc, c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), r1));
+  const cd res = c_add(uc, c_mul(c_scale(omega, dinv_at(k, g, c, gj, i)), r1));
+  out[p] = res;
+  if (MODE == 4) out2[p] = c_add(res, addt[p]);
 }
 
 // rows [j0, j0 + n) of column i by the sliding window: no closure, no pinning
@@ -111,7 +120,8 @@ __device__ __forceinline__ void r1_point(const cd* __restrict__ u, const cd* __r
 template <int MODE, int UNR>
 __device__ __forceinline__ void r1_run(const cd* __restrict__ u, const cd* __restrict__ b,
                                        const double* __restrict__ k, cd* __restrict__ out, const Geom& g,
-                                       const OpCoef& c, double omega, int i, int j0, int n) {
+                                       const OpCoef& c, double omega, int i, int j0, int n,
+                                       const cd* __restrict__ addt = nullptr, cd* __restrict__ out2 = nullptr) {
   if (n <= 0) return;
   const int lane = threadIdx.x;
   const long long nx = g.nx;
@@ -142,7 +152,9 @@ __device__ __forceinline__ void r1_run(const cd* __restrict__ u, const cd* __res
   cd wl = (lane == 0) ? up[-1] : mkc(0.0, 0.0), el = (lane == SX - 1) ? up[1] : mkc(0.0, 0.0);
   double klast = 0.0;
   cd dlast = mkc(0.0, 0.0);
-  if (MODE == 2) { klast = kc; dlast = interior_dinv(c, kc); }
+  if (MODE == 2 || MODE == 4) { klast = kc; dlast = interior_dinv(c, kc); }
+  const cd* tp = MODE == 4 ? addt + (long long)j0 * nx + i : nullptr;
+  cd* o2 = MODE == 4 ? out2 + (long long)j0 * nx + i : nullptr;
 #pragma unroll (UNR)
   for (int r = 0; r < n; ++r) {
     const long long o = (long long)r * nx;
@@ -173,7 +185,9 @@ __device__ __forceinline__ void r1_run(const cd* __restrict__ u, const cd* __res
         op[o] = r1;
       } else {
         if (kc != klast) { klast = kc; dlast = interior_dinv(c, kc); }
-        op[o] = c_add(c_, c_mul(c_scale(omega, dlast), r1));
+        const cd res = c_add(c_, c_mul(c_scale(omega, dlast), r1));
+        op[o] = res;
+        if (MODE == 4) o2[o] = c_add(res, tp[o]);
       }
     }
     s_ = c_;
@@ -221,9 +235,10 @@ __global__ void __launch_bounds__(SX * SY, MODE == 2 ? 5 : (MODE == 1 ? 6 : 8)) 
 // faster than 94 registers at 5 CTAs/SM: 86.6 vs 83.4 % of the copy peak on
 // 4097^2, 95.2 vs 91.8 % on 8193^2 (profiles/r01e_jacobi_occupancy.txt).
 template <int MODE, int UNR>
-__global__ void __launch_bounds__(SX * SY, (MODE == 1 || MODE == 2) ? 6 : 8) k_r1w(const cd* __restrict__ u, const cd* __restrict__ b,
+__global__ void __launch_bounds__(SX * SY, (MODE == 1 || MODE == 2 || MODE == 4) ? 6 : 8) k_r1w(const cd* __restrict__ u, const cd* __restrict__ b,
                                                  const double* __restrict__ k, cd* __restrict__ out, Geom g,
-                                                 OpCoef c, double omega, int rb) {
+                                                 OpCoef c, double omega, int rb,
+                                                 const cd* __restrict__ addt = nullptr, cd* __restrict__ out2 = nullptr) {
   if (c.skip && *c.skip) return;
   const int i = blockIdx.x * SX + threadIdx.x;
   const int jbeg = (blockIdx.y * SY + threadIdx.y) * rb;  // local row
@@ -234,10 +249,10 @@ __global__ void __launch_bounds__(SX * SY, (MODE == 1 || MODE == 2) ? 6 : 8) k_r
   if (!interior) {
     if (i >= g.nx) return;
     const int je = min(jbeg + rb, g.ny);
-    for (int j = jbeg; j < je; ++j) r1_point<MODE>(u, b, k, out, g, c, omega, i, j);
+    for (int j = jbeg; j < je; ++j) r1_point<MODE>(u, b, k, out, g, c, omega, i, j, addt, out2);
     return;
   }
-  r1_run<MODE, UNR>(u, b, k, out, g, c, omega, i, jbeg, rb);
+  r1_run<MODE, UNR>(u, b, k, out, g, c, omega, i, jbeg, rb, addt, out2);
 }
 
 // ------------------------------------------------------------------------
@@ -782,6 +797,181 @@ static bool rg_exact() {
 bool rg_exact_on() { return rg_exact(); }
 
 // ------------------------------------------------------------------------
+// Fused multigrid residual + restriction (mg.py:116-117):
+//     coarse = Z^T (b - M x)        with the coarse Dirichlet rows zeroed
+// in ONE pass over x, b, k^2 (40 B per fine point) plus the coarse write (4 B
+// per fine point) -- the residual is never stored (the unfused pair moves 56 +
+// 20 B per fine point).  A warp owns 30 coarse columns and FRB coarse rows:
+// lane L holds the fine columns E = 2 (c0 + L), O = E + 1 and walks the strip's
+// 2 FRB + 3 fine rows top to bottom with rows y-1, y, y+1 of x in registers
+// (k_r1w's sliding window, two columns per lane; the x-neighbours come from
+// lane shuffles); the residuals of one fine row then feed the (1,4,6,4,1)/16
+// taps of the coarse points through shuffles (lanes 0 / 31 only supply the
+// neighbours' residuals).  Residuals use k_r1's arithmetic and every coarse sum
+// the reference's (b, a) term order, so the result is bit-identical to
+// launch_apply(mode 1) followed by launch_restrict.  Fine points on the boundary
+// ring or outside the grid (the reference's zero extension) take the per-point
+// closure path (rr_point) -- a few lanes / rows per boundary strip.  Unsharded
+// radius-1 levels only.
+constexpr int FWY = 4;              // warps per block
+constexpr int FCX = 30;             // coarse columns per warp
+__host__ __device__ constexpr double fw16(int i) { return (i == 0 || i == 4 ? 1.0 : (i == 2 ? 6.0 : 4.0)) / 16; }
+
+// b - M x at fine (y, x) by the closure path; zero outside the grid.  Out of line (it
+// serves the few boundary-ring points of a strip) and fed by value: a reference to
+// the kernel's OpCoef parameter would force a per-thread stack copy of the whole
+// coefficient block.  Same operations as r1_point<1> (upad / pinned / five_point).
+struct R1C {
+  int nx, ny, bc[4];
+  double two_h, s;
+  cd mc;
+};
+__device__ __noinline__ cd rr_point(const cd* __restrict__ u, const cd* __restrict__ b,
+                                    const double* __restrict__ k, R1C q, int y, int x) {
+  if (y < 0 || y >= q.ny || x < 0 || x >= q.nx) return mkc(0.0, 0.0);
+  const long long nx = q.nx, p = (long long)y * nx + x;
+  const cd uc = u[p];
+  if ((q.bc[0] == HDB_BC_DIRICHLET && x == 0) || (q.bc[1] == HDB_BC_DIRICHLET && x == q.nx - 1) ||
+      (q.bc[2] == HDB_BC_DIRICHLET && y == 0) || (q.bc[3] == HDB_BC_DIRICHLET && y == q.ny - 1))
+    return c_sub(b[p], uc);
+  const double kc = k[p];
+  // neighbours: in the grid, or the first ghost layer closed from (boundary point = centre, inner point)
+  const cd w = x > 0 ? u[p - 1] : ghost_val(q.bc[0], q.two_h, kc, uc, u[p + 1]);
+  const cd e = x < q.nx - 1 ? u[p + 1] : ghost_val(q.bc[1], q.two_h, kc, uc, u[p - 1]);
+  const cd so = y > 0 ? u[p - nx] : ghost_val(q.bc[2], q.two_h, kc, uc, u[p + nx]);
+  const cd no = y < q.ny - 1 ? u[p + nx] : ghost_val(q.bc[3], q.two_h, kc, uc, u[p - nx]);
+  return c_sub(b[p], five_point(q.s, q.mc, kc, uc, w, e, so, no));
+}
+
+// Every strip runs the sliding window with row and column indices clamped into the
+// grid (so all loads are legal); a fine point that is not strictly interior -- the
+// boundary ring (closure, pinned rows) or a position outside the grid (zero
+// extension) -- has its window value replaced by rr_point.  Only the lanes / rows
+// that own such points diverge.
+template <int FRB>
+__global__ void __launch_bounds__(32 * FWY, 4) k_resrestrict(const cd* __restrict__ u, const cd* __restrict__ b,
+                                                          const double* __restrict__ k, cd* __restrict__ coarse,
+                                                          Geom g, OpCoef c, int ncx, int ncy, int zero_mask) {
+  constexpr int FNR = 2 * FRB + 3;  // fine rows per strip
+  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+  const int c0 = blockIdx.x * FCX - 1;  // coarse column of lane 0 (a neighbour-only lane)
+  const int cx = c0 + lane;
+  const int cy0 = (blockIdx.y * FWY + wy) * FRB;
+  if (cy0 >= ncy) return;
+  const int nrows = min(FRB, ncy - cy0);
+  const int xE = 2 * cx, y0 = 2 * cy0 - 2;
+  const int nx = g.nx, ny = g.nyg;
+  R1C rc;
+  rc.nx = nx; rc.ny = ny; rc.two_h = 2.0 * c.h; rc.s = c.s; rc.mc = c.mc;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) rc.bc[q] = c.bc[q];
+  const bool inE = xE >= 1 && xE <= nx - 2, inO = xE + 1 >= 1 && xE + 1 <= nx - 2;  // strictly interior columns
+  auto cl = [](int v, int hi) { return v < 0 ? 0 : (v > hi ? hi : v); };
+  const int qE = cl(xE, nx - 1), qO = cl(xE + 1, nx - 1), qW = cl(xE - 1, nx - 1), qX = cl(xE + 2, nx - 1);
+  auto row = [&](int y) { return (long long)cl(y, ny - 1) * nx; };
+  double ar[FRB], ai[FRB];
+#pragma unroll
+  for (int q = 0; q < FRB; ++q) ar[q] = ai[q] = 0.0;
+  cd sE = u[row(y0 - 1) + qE], sO = u[row(y0 - 1) + qO];
+  cd cE = u[row(y0) + qE], cO = u[row(y0) + qO];
+  cd nE = u[row(y0 + 1) + qE], nO = u[row(y0 + 1) + qO];
+  cd bE = b[row(y0) + qE], bO = b[row(y0) + qO];
+  double kE = k[row(y0) + qE], kO = k[row(y0) + qO];
+  cd wl = mkc(0.0, 0.0), el = wl;
+  if (lane == 0) wl = u[row(y0) + qW];
+  if (lane == 31) el = u[row(y0) + qX];
+#pragma unroll
+  for (int r = 0; r < FNR; ++r) {
+    const int y = y0 + r;
+    cd n2E = mkc(0.0, 0.0), n2O = n2E, b2E = n2E, b2O = n2E, wl2 = n2E, el2 = n2E;
+    double k2E = 0.0, k2O = 0.0;
+    if (r + 1 < FNR) {  // next row's loads before this row's arithmetic
+      const long long o2 = row(y + 2), o1 = row(y + 1);
+      n2E = u[o2 + qE]; n2O = u[o2 + qO];
+      b2E = b[o1 + qE]; b2O = b[o1 + qO];
+      k2E = k[o1 + qE]; k2O = k[o1 + qO];
+      if (lane == 0) wl2 = u[o1 + qW];
+      if (lane == 31) el2 = u[o1 + qX];
+    }
+    cd wE, eO;
+    wE.x = __shfl_up_sync(0xffffffffu, cO.x, 1);
+    wE.y = __shfl_up_sync(0xffffffffu, cO.y, 1);
+    eO.x = __shfl_down_sync(0xffffffffu, cE.x, 1);
+    eO.y = __shfl_down_sync(0xffffffffu, cE.y, 1);
+    if (lane == 0) wE = wl;
+    if (lane == 31) eO = el;
+    cd rE = c_sub(bE, five_point(c.s, c.mc, kE, cE, wE, cO, sE, nE));
+    cd rO = c_sub(bO, five_point(c.s, c.mc, kO, cO, cE, eO, sO, nO));
+    const bool rin = y >= 1 && y <= ny - 2;  // strictly interior row (warp-uniform)
+    if (!(rin && inE)) rE = rr_point(u, b, k, rc, y, xE);
+    if (!(rin && inO)) rO = rr_point(u, b, k, rc, y, xE + 1);
+    sE = cE; sO = cO; cE = nE; cO = nO; nE = n2E; nO = n2O;
+    bE = b2E; bO = b2O; kE = k2E; kO = k2O; wl = wl2; el = el2;
+    // the five fine residuals under coarse column cx: columns 2cx-2 .. 2cx+2
+    cd v[5];
+    v[2] = rE;
+    v[3] = rO;
+    v[0].x = __shfl_up_sync(0xffffffffu, rE.x, 1);
+    v[0].y = __shfl_up_sync(0xffffffffu, rE.y, 1);
+    v[1].x = __shfl_up_sync(0xffffffffu, rO.x, 1);
+    v[1].y = __shfl_up_sync(0xffffffffu, rO.y, 1);
+    v[4].x = __shfl_down_sync(0xffffffffu, rE.x, 1);
+    v[4].y = __shfl_down_sync(0xffffffffu, rE.y, 1);
+    // fine row r is tap b = r - 2q of coarse row q (compile-time after unrolling)
+#pragma unroll
+    for (int q = 0; q < FRB; ++q) {
+      const int bt = r - 2 * q;
+      if (bt < 0 || bt > 4) continue;
+#pragma unroll
+      for (int a = 0; a < 5; ++a) {
+        const double w = fw16(bt) * fw16(a);  // exact (dyadic)
+        ar[q] = __dadd_rn(ar[q], __dmul_rn(w, v[a].x));
+        ai[q] = __dadd_rn(ai[q], __dmul_rn(w, v[a].y));
+      }
+    }
+    if (r >= 4 && ((r - 4) & 1) == 0) {  // coarse row q complete after its b = 4 row
+      const int q = (r - 4) / 2;
+      if (q < nrows && lane >= 1 && lane <= FCX && cx < ncx) {
+        const int cy = cy0 + q;
+        const bool z = ((zero_mask & 1) && cx == 0) || ((zero_mask & 2) && cx == ncx - 1) ||
+                       ((zero_mask & 4) && cy == 0) || ((zero_mask & 8) && cy == ncy - 1);
+        coarse[(long long)cy * ncx + cx] = z ? mkc(0.0, 0.0) : mkc(ar[q], ai[q]);
+      }
+    }
+  }
+}
+
+bool resrestrict_fits(const OpCoef& c, const Geom& g) {
+  static const bool on = [] {
+    const char* e = getenv("HDB_FUSE_RR");
+    return !e || atoi(e) != 0;
+  }();
+  // small grids: most strips are boundary strips (per-point path); keep the unfused pair there
+  static const int minn = [] {  // HDB_RR_MIN: smallest fine extent that takes the fused kernel
+    const char* e = getenv("HDB_RR_MIN");
+    return e ? atoi(e) : 513;
+  }();
+  return on && c.radius == 1 && g.row0 == 0 && g.ny == g.nyg && g.nx >= minn && g.ny >= minn && (g.nx & 1) && (g.ny & 1);
+}
+
+void launch_resrestrict(const OpCoef& c, const Geom& g, const cd* u, const cd* b, const double* k, cd* coarse,
+                        int zero_mask, cudaStream_t st) {
+  const int ncx = (g.nx - 1) / 2 + 1, ncy = (g.nyg - 1) / 2 + 1;
+  static const int forced = [] {  // HDB_RR_FRB=4|8: coarse rows per warp
+    const char* e = getenv("HDB_RR_FRB");
+    return e ? atoi(e) : 0;
+  }();
+  const int frb = forced ? forced : 4;  // measured: 4 rows per warp is as fast or faster at every size (profiles/r02z_fusion_microbench.log)
+  if (frb == 8) {
+    const dim3 grd((ncx + FCX - 1) / FCX, (ncy + FWY * 8 - 1) / (FWY * 8));
+    k_resrestrict<8><<<grd, 32 * FWY, 0, st>>>(u, b, k, coarse, g, c, ncx, ncy, zero_mask);
+  } else {
+    const dim3 grd((ncx + FCX - 1) / FCX, (ncy + FWY * 4 - 1) / (FWY * 4));
+    k_resrestrict<4><<<grd, 32 * FWY, 0, st>>>(u, b, k, coarse, g, c, ncx, ncy, zero_mask);
+  }
+}
+
+// ------------------------------------------------------------------------
 static inline dim3 grid_r1(const Geom& g) { return dim3((g.nx + 31) / 32, (g.ny + 7) / 8); }
 static inline dim3 grid_r1s(const Geom& g) { return dim3((g.nx + SX - 1) / SX, (g.ny + SY * RB - 1) / (SY * RB)); }
 static inline bool use_strip(const Geom& g) { return g.nx >= 512 && g.ny >= 512; }  // small grids: all blocks are boundary blocks
@@ -878,6 +1068,21 @@ void launch_jacobi(const OpCoef& c, const Geom& g, const cd* x, const cd* b, con
   const dim3 blk(32, 8), grd = grid_r1(g);
   if (from_zero) k_r1<3><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
   else k_r1<2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega);
+}
+
+// the last post-smoothing sweep with the A-DEF1 sum folded in: out = Jacobi(x), out2 = out + addt
+bool jacobi_add_fits(const Geom& g) {
+  static const bool on = [] {
+    const char* e = getenv("HDB_FUSE_RT");
+    return !e || atoi(e) != 0;
+  }();
+  return on && use_strip(g) && r1_wave();
+}
+void launch_jacobi_add(const OpCoef& c, const Geom& g, const cd* x, const cd* b, const double* k, cd* out,
+                       double omega, const cd* addt, cd* out2, cudaStream_t st) {
+  const int rb = r1_rows(2, g);
+  const dim3 blk(SX, SY), grd((g.nx + SX - 1) / SX, (g.ny + SY * rb - 1) / (SY * rb));
+  k_r1w<4, 2><<<grd, blk, 0, st>>>(x, b, k, out, g, c, omega, rb, addt, out2);
 }
 
 long long resnorm_partials(const Geom& g) {

@@ -28,7 +28,7 @@ from .errors import BreakdownError, ConfigError, LevelError
 from .grid import ComplexField, dimensionless_kmax, kh_of
 from .krylov import StopRule, cslp_iteration_cap
 from .mg import CslpMultigrid, MgConfig
-from .operators import LevelOperator, cslp_operator, helmholtz_operator
+from .operators import LevelOperator, cslp_operator, helmholtz_operator, level_ksq
 
 __all__ = ["Definiteness", "classify_levels", "LevelPolicy", "SolverConfig", "ConvergenceReport", "preset",
            "PRESET_NAMES", "MadpSolver", "solve", "DEFINITENESS_THRESHOLD"]
@@ -198,7 +198,7 @@ class MadpSolver:
                 self.M[l] = cslp_operator(hierarchy, l, pol.cslp_shift, config.beta1, slab=spec(l - 1))
             elif pol.cslp_method == CSLP_MG:
                 lv = hierarchy.level(l)
-                self.mg[l] = CslpMultigrid(lv.nx, lv.ny, lv.h, hierarchy.ksq_at(l), hierarchy.boundary,
+                self.mg[l] = CslpMultigrid(lv.nx, lv.ny, lv.h, level_ksq(hierarchy, l), hierarchy.boundary,
                                            beta2=pol.cslp_shift, beta1=config.beta1, config=config.mg_config,
                                            slabs=(lambda s, l=l: spec(l - 1 + s)))
         self._h = None

@@ -104,7 +104,8 @@ class CslpMultigrid:
         shift = complex(beta1, beta2)
         self.levels: list[_SubLevel] = []
         cx, cy, ch = int(nx), int(ny), float(h)
-        kk = np.ascontiguousarray(ksq, dtype=np.float64)
+        on_device = dev.is_device(ksq)  # GPU-built hierarchy: sub-level k^2 by injection on the device
+        kk = dev.to_device(ksq, dtype="f8") if on_device else np.ascontiguousarray(ksq, dtype=np.float64)
         while True:
             sl = slabs(len(self.levels)) if slabs is not None else None
             self.levels.append(_SubLevel(op=radius1_operator(cx, cy, ch, kk, boundary, shift, slab=sl)))
@@ -112,7 +113,12 @@ class CslpMultigrid:
                     and len(self.levels) < config.mg_levels):
                 break
             cx, cy, ch = (cx - 1) // 2 + 1, (cy - 1) // 2 + 1, 2.0 * ch
-            kk = kk[::2, ::2].copy()
+            if on_device:
+                nxt = dev.empty((cy, cx), dtype="f8")
+                check(lib().hdb_setup_inject(kk.data_ptr(), kk.shape[1], kk.shape[0], nxt.data_ptr()))
+                kk = nxt
+            else:
+                kk = kk[::2, ::2].copy()
         last = self.levels[-1]
         self._inv = None
         if last.op.npoints <= config.direct_coarsest_limit:

@@ -16,7 +16,7 @@ import math
 
 import numpy as np
 
-from .grid import Problem, VelocityModel, build_hierarchy, point_source_rhs
+from .grid import Problem, VelocityModel, build_hierarchy, point_source_device, point_source_rhs
 
 __all__ = ["synthetic_layered_velocity", "synthetic_layered_problem", "C4_DOMAIN", "C4_SOURCE", "c5_problem"]
 
@@ -79,18 +79,21 @@ def synthetic_layered_velocity(seed: int = 2412, dx: float = 6.0, n_layers: int 
     return VelocityModel(kind="gridfile", values=np.ascontiguousarray(vel), dx=dx, dy=dx, x0=x0, y0=y0)
 
 
-def synthetic_layered_problem(f: float, h: float, ml: int, seed: int = 2412, raster_dx: float = 6.0) -> Problem:
+def synthetic_layered_problem(f: float, h: float, ml: int, seed: int = 2412, raster_dx: float = 6.0,
+                              device: bool = False) -> Problem:
     """BASELINE configs[3]: the seeded model at mesh width h (9192 = 2^3 3 383 m, so h = 24/2^p
     and ml <= p + 1), point source at (4596, 0) m, Sommerfeld on all sides."""
     vel = synthetic_layered_velocity(seed, dx=raster_dx)
-    hier = build_hierarchy(C4_DOMAIN, h=h, ml=ml, velocity=vel, f=f, boundary="sommerfeld")
-    return Problem("synthetic-layered", hier, point_source_rhs(hier, C4_SOURCE))
+    hier = build_hierarchy(C4_DOMAIN, h=h, ml=ml, velocity=vel, f=f, boundary="sommerfeld", device=device)
+    rhs = point_source_device(hier, C4_SOURCE) if device else point_source_rhs(hier, C4_SOURCE)
+    return Problem("synthetic-layered", hier, rhs)
 
 
-def c5_problem(P: int = 1, ml: int = 7) -> Problem:
+def c5_problem(P: int = 1, ml: int = 7, device: bool = False) -> Problem:
     """BASELINE configs[4] (weak scaling): [0,1] x [0,P], h = 1/8192 (8193 x (8192P+1) points,
     SURVEY D8), k = (0.5 / h^2)^(1/3) so that k^3 h^2 = 0.5, centre source, Sommerfeld."""
     h = 1.0 / 8192
     k = (0.5 / h ** 2) ** (1.0 / 3.0)
-    hier = build_hierarchy(((0.0, 1.0), (0.0, float(P))), h=h, ml=ml, k=k, boundary="sommerfeld")
-    return Problem("c5", hier, point_source_rhs(hier, (0.5, P / 2.0)))
+    hier = build_hierarchy(((0.0, 1.0), (0.0, float(P))), h=h, ml=ml, k=k, boundary="sommerfeld", device=device)
+    rhs = point_source_device(hier, (0.5, P / 2.0)) if device else point_source_rhs(hier, (0.5, P / 2.0))
+    return Problem("c5", hier, rhs)

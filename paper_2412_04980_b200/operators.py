@@ -78,9 +78,16 @@ class LevelOperator:
             raise ShapeError("laplace and mass kernels must share a radius")
         self.level = level
         self.nx, self.ny, self.h = int(nx), int(ny), float(h)
-        self.ksq = np.ascontiguousarray(ksq, dtype=np.float64)
-        if self.ksq.shape != (self.ny, self.nx):
-            raise ShapeError(f"k^2 shape {self.ksq.shape} != {(self.ny, self.nx)}")
+        # k^2 as a host array (the reference's form) or a CUDA float64 tensor from the
+        # GPU-side setup (grid.build_hierarchy(device=True)); `ksq` then downloads on demand
+        self._ksq_dev = None
+        if dev.is_device(ksq):
+            self._ksq_dev = dev.to_device(ksq, dtype="f8")
+            self._ksq_host = None
+        else:
+            self._ksq_host = np.ascontiguousarray(ksq, dtype=np.float64)
+        if tuple(ksq.shape) != (self.ny, self.nx):
+            raise ShapeError(f"k^2 shape {tuple(ksq.shape)} != {(self.ny, self.nx)}")
         self.boundary = tuple(boundary)
         self.shift = complex(shift)
         self.radius = laplace.radius
@@ -92,6 +99,12 @@ class LevelOperator:
         self._handle = None
         self._kedges = None
         self._kpad = None
+
+    @property
+    def ksq(self) -> np.ndarray:
+        if self._ksq_host is None:
+            self._ksq_host = dev.to_host(self._ksq_dev)
+        return self._ksq_host
 
     # host-side closure data of the reference object (operators.py:114-116), built on first use
     @property
@@ -123,7 +136,10 @@ class LevelOperator:
             mre = np.ascontiguousarray(self.mass_coef.real)
             mim = np.ascontiguousarray(self.mass_coef.imag)
             f = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
-            if self.slab is None:
+            if self.slab is None and self._ksq_dev is not None:
+                check(L.hdb_op_create_dev(C.byref(h), self.nx, self.ny, self.radius, self.h, bc, f(lap), f(mre),
+                                          f(mim), self._ksq_dev.data_ptr()))
+            elif self.slab is None:
                 check(L.hdb_op_create(C.byref(h), self.nx, self.ny, self.radius, self.h, bc, f(lap), f(mre), f(mim),
                                       f(self.ksq)))
             else:
@@ -259,6 +275,27 @@ class LevelOperator:
         check(lib().hdb_op_jacobi(self.handle, xp, db.data_ptr(), dout.data_ptr(), float(omega)))
         return dev.to_host(dout) if host else dout
 
+    def residual_restrict(self, b, u, zero_mask=0):
+        """Z^T (b - A u) in one pass (mg.py:116-117): the multigrid coarse right-hand
+        side without storing the residual; bit-identical to ``residual`` followed by
+        ``restrict_array``.  zero_mask: coarse Dirichlet sides to zero (bit 0 west,
+        1 east, 2 south, 3 north).  Unsharded radius-1 operators."""
+        host, (du, db) = self._io(u, b)
+        ny, nx = self.shape
+        dout = dev.empty(((ny - 1) // 2 + 1, (nx - 1) // 2 + 1))
+        check(lib().hdb_op_residual_restrict(self.handle, db.data_ptr(), du.data_ptr(), dout.data_ptr(),
+                                             int(zero_mask)))
+        return dev.to_host(dout) if host else dout
+
+    def jacobi_add(self, x, b, t, omega=0.8):
+        """(Jacobi(x), Jacobi(x) + t) from one sweep: the last post-smoothing step with
+        the A-DEF1 sum r + t folded in (mg.py:122, madp.py:327)."""
+        host, (dx, db, dt) = self._io(x, b, t)
+        dout, dsum = dev.empty(self.shape), dev.empty(self.shape)
+        check(lib().hdb_op_jacobi_add(self.handle, dx.data_ptr(), db.data_ptr(), dout.data_ptr(), float(omega),
+                                      dt.data_ptr(), dsum.data_ptr()))
+        return (dev.to_host(dout), dev.to_host(dsum)) if host else (dout, dsum)
+
     def diagonal(self) -> np.ndarray:
         """Matrix diagonal incl. ghost-closure terms (operators.py:180-208), host setup."""
         if self.radius != 1:
@@ -298,10 +335,16 @@ class LevelOperator:
         return A
 
 
+def level_ksq(hierarchy, level):
+    """Level k^2 for an operator: the device tensor of a GPU-built hierarchy, else the host array."""
+    dk = hierarchy.device_ksq_at(level) if getattr(hierarchy, "device_ksq", None) is not None else None
+    return dk if dk is not None else hierarchy.ksq_at(level)
+
+
 def _level_operator(hierarchy, level, shift, slab=None):
     lv = hierarchy.level(level)
     lap, mass = level_kernels(level)
-    return LevelOperator(level, lv.nx, lv.ny, lv.h, hierarchy.ksq_at(level), hierarchy.boundary, lap, mass,
+    return LevelOperator(level, lv.nx, lv.ny, lv.h, level_ksq(hierarchy, level), hierarchy.boundary, lap, mass,
                          shift=shift, level_scale=mass_level_scale(level), slab=slab)
 
 

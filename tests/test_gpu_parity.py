@@ -160,6 +160,55 @@ def test_strip_kernels_bitexact_vs_oracle(shape, bnd):
     np.testing.assert_array_equal(op.jacobi(None, b, 0.8), ref.jacobi(np.zeros(shape, complex), b, 0.8))
 
 
+@pytest.mark.parametrize("shape", [(1025, 1025), (513, 2049), (2049, 577), (129, 129), (9, 5), (3, 3)])
+@pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld"),
+                                 ("dirichlet",) * 4])
+def test_fused_residual_restrict_bitexact_vs_oracle(shape, bnd):
+    """Fused multigrid coarse right-hand side Z^T (b - M x) with the coarse Dirichlet
+    rows zeroed (mg.py:116-117), one pass without storing the residual, against the
+    oracle's residual followed by its restriction, bit for bit (interior strips on
+    the sliding window, boundary strips on the closure path, ragged last strips)."""
+    rng = _rng(7 * shape[0] + shape[1])
+    ny, nx = shape
+    ksq = 900.0 + 500.0 * rng.random((ny, nx))
+    op = hdb.radius1_operator(nx, ny, 1.0 / 256, ksq, bnd, complex(1.0, 0.5))
+    ref = oracle.CpuLevelOp(nx, ny, 1.0 / 256, ksq, bnd, *oracle.level_kernels(1)[:4], shift=complex(1.0, 0.5),
+                            level_scale=1.0)
+    u, b = _rand(rng, shape), _rand(rng, shape)
+    mask = sum(1 << s for s in range(4) if bnd[s] == "dirichlet")
+    want = oracle.restrict(b - ref.apply(u))
+    if mask & 1:
+        want[:, 0] = 0
+    if mask & 2:
+        want[:, -1] = 0
+    if mask & 4:
+        want[0, :] = 0
+    if mask & 8:
+        want[-1, :] = 0
+    np.testing.assert_array_equal(op.residual_restrict(b, u, mask), want)
+    # and equal to the library's own unfused pair
+    np.testing.assert_array_equal(op.residual_restrict(b, u, 0), hdb.restrict_array(op.residual(b, u)))
+
+
+@pytest.mark.parametrize("shape", [(1025, 1025), (600, 2050), (129, 129)])
+@pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
+def test_jacobi_with_folded_sum_bitexact_vs_oracle(shape, bnd):
+    """The last post-smoothing sweep with the A-DEF1 sum folded in (mg.py:122 +
+    madp.py:327): both outputs equal the oracle's sweep and sweep + t bit for bit."""
+    rng = _rng(shape[0] + 5 * shape[1])
+    ny, nx = shape
+    ksq = 900.0 + 500.0 * rng.random((ny, nx))
+    ksq[ny // 2: ny // 2 + 40] = 700.0
+    op = hdb.radius1_operator(nx, ny, 1.0 / 256, ksq, bnd, complex(1.0, 0.5))
+    ref = oracle.CpuLevelOp(nx, ny, 1.0 / 256, ksq, bnd, *oracle.level_kernels(1)[:4], shift=complex(1.0, 0.5),
+                            level_scale=1.0)
+    x, b, t = _rand(rng, shape), _rand(rng, shape), _rand(rng, shape)
+    want = ref.jacobi(x, b, 0.8)
+    got, gsum = op.jacobi_add(x, b, t, 0.8)
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(gsum, want + t)
+
+
 @pytest.mark.parametrize("shape", [(129, 129), (600, 300), (1025, 1025)])
 @pytest.mark.parametrize("bnd", [("sommerfeld",) * 4, ("dirichlet", "sommerfeld", "dirichlet", "sommerfeld")])
 def test_fused_residual_norms_vs_oracle(shape, bnd):
@@ -734,3 +783,66 @@ def test_config4_synthetic_layered_vs_reference(name, h, ml):
     hb, xb = parity_bar(g)
     st = int(g["solution_stride"])
     assert np.linalg.norm(u.grid_view(hier)[::st, ::st] - g["solution_sub"]) <= xb * np.linalg.norm(g["solution_sub"])
+
+
+# ---------------------------------------------------------------- device-side setup (f3)
+def _device_setup_cases():
+    from paper_2412_04980_b200 import grid as G
+    from paper_2412_04980_b200 import models
+    return {
+        "mp1_k": lambda dev: hdb.mp1_problem(k=50.0, n=129, ml=3, boundary="dirichlet", device=dev),
+        "mp1_f": lambda dev: hdb.mp1_problem(f=9.7, n=257, ml=4, device=dev),
+        "const_c": lambda dev: G.Problem("c", hdb.build_hierarchy(((0.0, 3.0), (-1.0, 1.0)), 1.0 / 64, 3,
+                                                                 velocity=hdb.VelocityModel("constant", c=1234.5),
+                                                                 f=77.0, device=dev), None),
+        "wedge20": lambda dev: hdb.wedge_problem(f=20.0, nx=145, ml=4, device=dev),
+        "wedge_baseline": lambda dev: hdb.wedge_problem(f=10.0, nx=301, ml=3, layers=G.BASELINE_WEDGE_LAYERS,
+                                                        device=dev),
+        "marmousi": lambda dev: hdb.marmousi_problem(f=5.0, nx=737, ml=4, device=dev),
+        "layered_c4": lambda dev: models.synthetic_layered_problem(f=10.0, h=3.0, ml=4, device=dev),
+    }
+
+
+@pytest.mark.parametrize("name", ["mp1_k", "mp1_f", "const_c", "wedge20", "wedge_baseline", "marmousi", "layered_c4"])
+def test_device_setup_fields_bitexact_vs_host(name):
+    """GPU-side setup (csrc/kernels_setup.cu; grid.py:120-160, 261-287, 309-320): the k^2
+    field of every level, its maximum and the point source written on the device equal
+    the host (reference-pinned) ones bit for bit."""
+    case = _device_setup_cases()[name]
+    host, devp = case(False), case(True)
+    assert devp.hierarchy.device_ksq is not None and host.hierarchy.device_ksq is None
+    for l in range(1, host.hierarchy.ml + 1):
+        np.testing.assert_array_equal(devp.hierarchy.device_ksq_at(l).cpu().numpy(), host.hierarchy.ksq_at(l))
+        np.testing.assert_array_equal(devp.hierarchy.ksq_at(l), host.hierarchy.ksq_at(l))  # lazy host copy
+        assert devp.hierarchy.ksq_max_at(l) == host.hierarchy.ksq_at(l).max()
+        assert hdb.kh_of(l, devp.hierarchy) == hdb.kh_of(l, host.hierarchy)
+    if host.rhs is not None:
+        np.testing.assert_array_equal(devp.rhs.cpu().numpy(), host.rhs.grid_view(host.hierarchy))
+
+
+def test_device_setup_rejects_bad_models():
+    from paper_2412_04980_b200.errors import ModelError
+    with pytest.raises(ModelError):
+        hdb.build_hierarchy(((0.0, 1.0), (0.0, 1.0)), 1.0 / 32, 2,
+                            velocity=hdb.VelocityModel("gridfile", values=np.array([[1.0, np.inf], [1.0, 0.0]]),
+                                                       dx=1.0, dy=1.0), f=1.0, device=True).ksq_at(1)
+    with pytest.raises(ModelError):
+        hdb.point_source_device(hdb.mp1_problem(k=10.0, n=33, ml=2, device=True).hierarchy, (2.0, 0.5))
+
+
+@pytest.mark.parametrize("name", ["mp1_f", "wedge20"])
+def test_device_built_problem_solves_identically(name):
+    """A problem set up on the GPU (operators created from device k^2, multigrid
+    sub-levels injected on the device, device right-hand side) gives the same solve,
+    bit for bit, as the host-built one."""
+    case = _device_setup_cases()[name]
+    host, devp = case(False), case(True)
+    cfg = hdb.preset("MADP", host.hierarchy)
+    with hdb.MadpSolver(host.hierarchy, cfg) as s:
+        xh, rh = s.solve(host.rhs)
+    cfg_d = hdb.preset("MADP", devp.hierarchy)
+    with hdb.MadpSolver(devp.hierarchy, cfg_d) as s:
+        xd, rd = s.solve(devp.rhs)
+    assert rd.outer_iterations == rh.outer_iterations
+    assert list(rd.residual_history) == list(rh.residual_history)
+    np.testing.assert_array_equal(xd.cpu().numpy(), xh.grid_view(host.hierarchy))
