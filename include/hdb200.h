@@ -211,7 +211,11 @@ int hdb_op_set_separable(hdb_op* op, const double* sa, const double* sm, double 
  * reference's coefficient-by-coefficient MGS order (HDB_MGS_LS=0 likewise).
  * "rg_exact": 1 radius-2/3 operators use the reference's row-major tap order
  * (bit-identical to contract_general; HDB_RG_EXACT=1), 0 (default) the
- * separable 1D passes where the operator has them                            */
+ * separable 1D passes where the operator has them.
+ * "pinv": 1 every reduction of a level sums per-row partials in global row order
+ * and every level keeps the launch-driven Krylov path, so a solve is bit-identical
+ * on any number of ranks (reduce_dot's worker-count invariance, parallel.py:168-195;
+ * HDB_PINV=1); 0 (default) the fast per-rank reduction trees                    */
 int hdb_option(const char* name, int value);
 
 /* ---- launch accounting / timing (measurement, not on the reference API) ---- */

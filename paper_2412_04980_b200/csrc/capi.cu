@@ -295,7 +295,7 @@ int hdb_op_residual(hdb_op* op, const void* b, const void* u, void* out) {
 int hdb_op_resnorm(hdb_op* op, const void* b, const void* u, double* out2) {
   return guarded([&] {
     Engine& E = engine();
-    cd* scratch = op->op.c.radius == 1 ? nullptr : E.alloc(op->op.n);
+    cd* scratch = (op->op.c.radius == 1 && !pinv_mode()) ? nullptr : E.alloc(op->op.n);
     op->op.resnorm((const cd*)b, (const cd*)u, E.dscal + kSlotMisc, scratch);
     check_launch();
     if (!out2) {  // timing form: result stays in the device slot, no sync
@@ -658,6 +658,7 @@ int hdb_option(const char* name, int value) {
     const std::string k = name ? name : "";
     if (k == "mgs_ls") set_mgs_ls(value);
     else if (k == "rg_exact") set_rg_exact(value);
+    else if (k == "pinv") set_pinv(value);
     else throw Error(E_ARG, "unknown option " + k);
   });
 }

@@ -83,6 +83,8 @@ Engine::~Engine() {
   for (cudaEvent_t e : kp.pool) cudaEventDestroy(e);
   if (own_st) st = own_st;
   delete comm;
+  cudaFree(rowpart);
+  cudaFree(rowfull);
   cudaFree(red.partials);
   cudaFree(red.big);
   cudaFree(red.ticket);
@@ -163,6 +165,86 @@ void LevelOp::reduce(cd* slot) const {
   E.comm->allreduce((double*)slot, 2, E.st);
 }
 
+// ---- rank-count-invariant reductions (HDB_PINV=1 / hdb_option("pinv", 1)) ----------------
+// Every reduction of a level goes through per-row partials gathered in global row order
+// (kernels_blas.cu k_rowred / k_rowsum), so a solve gives the same bits on 1, 2, 4, ...
+// ranks (the reference's reduce_dot contract, parallel.py:168-195).  The mode also keeps
+// every level on the launch-driven Krylov path: the one-launch MGS steps and the
+// device-resident solvers reduce over CTA slices that depend on the local extent.
+static int g_pinv = -1;
+bool pinv_mode() {
+  if (g_pinv < 0) {
+    const char* e = getenv("HDB_PINV");
+    g_pinv = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  return g_pinv != 0;
+}
+void set_pinv(int on) { g_pinv = on ? 1 : 0; }
+
+cd* Engine::rows(int nyg) {
+  if (nyg > row_cap) {
+    free(rowpart);
+    free(rowfull);
+    row_cap = nyg;
+    rowpart = alloc(row_cap);
+    rowfull = alloc(row_cap);
+  }
+  return rowpart;
+}
+
+void LevelOp::finish_rows(cd* slot) const {
+  Engine& E = engine();
+  const cd* src = E.rowpart;
+  if (sharded) {
+    const int P = E.comm->size;
+    std::vector<size_t> off(P), bytes(P);
+    for (int r = 0; r < P; ++r) {
+      off[r] = sizeof(cd) * (size_t)slab_row0[r];
+      bytes[r] = sizeof(cd) * (size_t)slab_ny[r];
+    }
+    E.comm->allgatherv(E.rowpart, E.rowfull, off, bytes, E.st);
+    src = E.rowfull;
+  }
+  E.kl(KF_BLAS, 16.0 * g.nyg, [&] { launch_rowsum(src, g.nyg, slot, E.st); });
+}
+
+void red_dot(const LevelOp* L, const cd* u, const cd* v, long long n, cd* slot) {
+  Engine& E = engine();
+  const double bytes = (u == v ? 16.0 : 32.0) * n;
+  if (L && pinv_mode()) {
+    cd* rp = E.rows(L->g.nyg);
+    E.kl(KF_BLAS, bytes, [&] { launch_rowdot(u, v, L->g.nx, L->g.ny, rp, E.st); });
+    L->finish_rows(slot);
+    return;
+  }
+  E.kl(KF_BLAS, bytes, [&] { launch_dot(u, v, n, E.red, slot, E.st); });
+  if (L && L->sharded) L->reduce(slot);
+}
+
+void red_mgs(const LevelOp* L, cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, cd* slot, double bytes) {
+  Engine& E = engine();
+  if (L && pinv_mode()) {
+    cd* rp = E.rows(L->g.nyg);
+    E.kl(KF_MGS_CHAIN, bytes, [&] { launch_rowmgs(w, vi, hsrc, vn, L->g.nx, L->g.ny, rp, E.st); });
+    L->finish_rows(slot);
+    return;
+  }
+  E.kl(KF_MGS_CHAIN, bytes, [&] { launch_mgs(w, vi, hsrc, vn, n, E.red, slot, E.st); });
+  if (L && L->sharded) L->reduce(slot);
+}
+
+void red_subnorm(const LevelOp* L, const cd* b, const cd* t, long long n, cd* slot) {
+  Engine& E = engine();
+  if (L && pinv_mode()) {
+    cd* rp = E.rows(L->g.nyg);
+    E.kl(KF_BLAS, 32.0 * n, [&] { launch_rowsubnorm(b, t, L->g.nx, L->g.ny, rp, E.st); });
+    L->finish_rows(slot);
+    return;
+  }
+  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, t, n, E.red, slot, E.st); });
+  if (L && L->sharded) L->reduce(slot);
+}
+
 void LevelOp::apply(const cd* u, cd* out) const {
   Engine& E = engine();
   exchange(u, c.radius);
@@ -176,6 +258,13 @@ void LevelOp::residual(const cd* b, const cd* u, cd* out) const {
 void LevelOp::resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const {
   Engine& E = engine();
   exchange(u, c.radius);
+  if (pinv_mode()) {  // tile partials depend on the slab: residual, then two row-ordered norms
+    E.kl(c.radius == 1 ? KF_RESID5 : KF_GALERKIN, 56.0 * n, [&] { launch_apply(c, g, u, b, ksq, scratch, 1, E.st); });
+    red_dot(this, scratch, scratch, n, slot);
+    red_dot(this, b, b, n, E.dscal + kSlotMgB);
+    E.kl(KF_BLAS, 0.0, [&] { launch_pack_im(slot, E.dscal + kSlotMgB, E.st); });
+    return;
+  }
   if (c.radius == 1) {
     const long long G = resnorm_partials(g);
     if (G > E.red.big_cap) {  // grows once per new largest level
@@ -356,6 +445,7 @@ long long coop_mgs_min() {
 }
 
 int resident_mode(long long n, int cap) {
+  if (pinv_mode()) return -1;
   static long long small = -1, grid = -1;
   if (small < 0) {
     // cluster mode only when asked: the grid mode is faster at every config-2 level since
@@ -418,17 +508,14 @@ static const double kHappy = 1e-30;  // krylov.py:28
 KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, Stop stop, KWS& ws,
                const std::function<void(int, double)>* hook, const cd* x0, const LevelOp* dist) {
   const bool shard = dist && dist->sharded;
-  auto red = [&](cd* slot) {
-    if (shard) dist->reduce(slot);
-  };
+  const bool pinv = dist && pinv_mode();
   Engine& E = engine();
   if (stop.max_iters < 1) throw Error(E_ARG, "max_iters must be >= 1");
   if (stop.max_iters + kSlotH + 2 >= 900) throw Error(E_ARG, "Krylov iteration cap too large (max 896)");
   ws.ensure(n, stop.max_iters, M != nullptr);
   KReport rep;
 
-  E.kl(KF_BLAS, 16.0 * n, [&] { launch_dot(b, b, n, E.red, E.dscal + kSlotH, E.st); });
-  red(E.dscal + kSlotH);
+  red_dot(dist, b, b, n, E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   const double bnorm = E.fetch_norm(kSlotH);
   auto copy_x0 = [&] {
@@ -440,11 +527,8 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   double beta = bnorm;
   if (x0) {
     A(x0, ws.tmp);
-    E.kl(KF_BLAS, 64.0 * n, [&] {
-      launch_add(b, ws.tmp, ws.tmp, n, 1, E.st);
-      launch_dot(ws.tmp, ws.tmp, n, E.red, E.dscal + kSlotH, E.st);
-    }, 2);
-    red(E.dscal + kSlotH);
+    E.kl(KF_BLAS, 48.0 * n, [&] { launch_add(b, ws.tmp, ws.tmp, n, 1, E.st); });
+    red_dot(dist, ws.tmp, ws.tmp, n, E.dscal + kSlotH);
     r0 = ws.tmp;
   }
   if (bnorm == 0.0) {  // krylov.py:96-97
@@ -505,7 +589,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
         ws.dV_n++;
       }
     };
-    if (!shard && n >= coop_mgs_min()) {
+    if (!shard && !pinv && n >= coop_mgs_min()) {
       if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
       if (!ws.tg) ws.tg = E.alloc(mgs_ls_tg_elems());
       ensure_dv();
@@ -530,7 +614,8 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     // sharded levels take it at any size: two all-reduces per Arnoldi step (the (2j+1)
     // coefficient sums and ||w||^2) instead of one per MGS coefficient
     bool lsh = false;
-    if (!coop && ((shard && n >= lsh_shard_min()) || (!shard && n >= lsh_min())) && mgs_ls_on() && (j == 0 || lsh_ok) &&
+    if (!coop && !pinv && ((shard && n >= lsh_shard_min()) || (!shard && n >= lsh_min())) && mgs_ls_on() &&
+        (j == 0 || lsh_ok) &&
         stop.max_iters <= 511) {
       if (ws.tgh_cap < stop.max_iters) {
         E.free(ws.tgh);
@@ -552,18 +637,10 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     }
     lsh_ok = lsh;
     if (!coop && !lsh) {  // the fused MGS chain (algorithmic bytes booked: w + V_0, then each V_i, w out)
-      E.kl(KF_MGS_CHAIN, 32.0 * n, [&] { launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, E.dscal + kSlotH, E.st); });
-      red(E.dscal + kSlotH);
-      for (int i = 0; i < j; ++i) {
-        E.kl(KF_MGS_CHAIN, 16.0 * n, [&] {
-          launch_mgs(w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.red, E.dscal + kSlotH + i + 1, E.st);
-        });
-        red(E.dscal + kSlotH + i + 1);
-      }
-      E.kl(KF_MGS_CHAIN, 16.0 * n, [&] {
-        launch_mgs(w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.red, E.dscal + kSlotH + j + 1, E.st);
-      });
-      red(E.dscal + kSlotH + j + 1);
+      red_mgs(dist, w, nullptr, nullptr, ws.v(0), n, E.dscal + kSlotH, 32.0 * n);
+      for (int i = 0; i < j; ++i)
+        red_mgs(dist, w, ws.v(i), E.dscal + kSlotH + i, ws.v(i + 1), n, E.dscal + kSlotH + i + 1, 16.0 * n);
+      red_mgs(dist, w, ws.v(j), E.dscal + kSlotH + j, nullptr, n, E.dscal + kSlotH + j + 1, 16.0 * n);
     }
     E.fetch(kSlotH + j + 2);
     std::vector<cplx> col(j + 2);
@@ -625,8 +702,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
   E.kl(KF_BLAS, 16.0 * (m + 1 + (x0 ? 1 : 0)) * n, [&] { launch_lincomb(ws.dbasis, ws.dy, m, x0, x, n, E.st); });
   // explicit true residual (krylov.py:174)
   A(x, ws.tmp);
-  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st); });
-  red(E.dscal + kSlotH);
+  red_subnorm(dist, b, ws.tmp, n, E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   const double fin = E.fetch_norm(kSlotH) / bnorm;
   if (!std::isfinite(fin)) throw Error(E_NONFINITE, "non-finite solution");
@@ -667,7 +743,7 @@ static void ensure_vtab(KWS& ws, int upto) {
 bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int* its_dev, double* rel_dev) {
   const long long n = op->n;
   const int cap = stop.max_iters;
-  if (!gmres_device_enabled() || op->sharded || n < coop_mgs_min() || cap < 1 || cap + kSlotH + 2 >= 900 ||
+  if (!gmres_device_enabled() || pinv_mode() || op->sharded || n < coop_mgs_min() || cap < 1 || cap + kSlotH + 2 >= 900 ||
       !(stop.rel_tol < 1.0) || !mgs_grid_fits(n))
     return false;
   Engine& E = engine();
@@ -747,29 +823,21 @@ void fgmres_step1(long long n, const LinOp& A, const LinOp& M, const cd* b, cd* 
   if (level < 1 || kS1Base + 5 * level + 4 >= kSlotMgR0) throw Error(E_ARG, "one-step FGMRES level out of range");
   const int kS1B = kS1Base + 5 * level, kS1H0 = kS1B + 1, kS1HN = kS1B + 2, kS1Y = kS1B + 3, kS1F = kS1B + 4;
   ws.ensure(n, 1, true);
-  const bool shard = dist && dist->sharded;
-  auto red = [&](int slot) {
-    if (shard) dist->reduce(E.dscal + slot);
-  };
   cd* S = E.dscal;
-  E.kl(KF_BLAS, 16.0 * n, [&] { launch_dot(b, b, n, E.red, S + kS1B, E.st); });  // ||b||^2 (krylov.py:92)
-  red(kS1B);
+  red_dot(dist, b, b, n, S + kS1B);  // ||b||^2 (krylov.py:92)
   E.kl(KF_BLAS, 32.0 * n, [&] { launch_scale_dev(b, ws.v(0), S + kS1B, n, E.st); });  // V0 = r0 / beta
   M(ws.v(0), ws.z(0));
   cd* w = ws.v(1);
   A(ws.z(0), w);
-  E.kl(KF_MGS_CHAIN, 32.0 * n, [&] { launch_mgs(w, nullptr, nullptr, ws.v(0), n, E.red, S + kS1H0, E.st); });
-  red(kS1H0);
-  E.kl(KF_MGS_CHAIN, 16.0 * n, [&] { launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st); });
-  red(kS1HN);
+  red_mgs(dist, w, nullptr, nullptr, ws.v(0), n, S + kS1H0, 32.0 * n);
+  red_mgs(dist, w, ws.v(0), S + kS1H0, nullptr, n, S + kS1HN, 16.0 * n);
   E.kl(KF_CONTROL, 0.0, [&] { launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st); });
   ws.hbasis[0] = ws.z(0);
   HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*), cudaMemcpyHostToDevice, E.st));
   E.kl(KF_BLAS, 32.0 * n, [&] { launch_lincomb(ws.dbasis, S + kS1Y, 1, nullptr, x, n, E.st); });  // x = y0 Z0
   // explicit true residual: only its finiteness matters to the caller (krylov.py:174-176)
   A(x, ws.tmp);
-  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, S + kS1F, E.st); });
-  red(kS1F);
+  red_subnorm(dist, b, ws.tmp, n, S + kS1F);
   E.kl(KF_CONTROL, 0.0, [&] { launch_finite_guard(S + kS1F, S + kSlotFlag, E.st); });
 }
 
@@ -792,10 +860,8 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
   Engine& E = engine();
   ws.ensure(n);
   *breakdown = false;
-  const bool shard = dist && dist->sharded;
   auto dotv = [&](const cd* u, const cd* w) {  // conj-dot to the host (one sync)
-    E.kl(KF_BLAS, (u == w ? 16.0 : 32.0) * n, [&] { launch_dot(u, w, n, E.red, E.dscal + kSlotH, E.st); });
-    if (shard) dist->reduce(E.dscal + kSlotH);
+    red_dot(dist, u, w, n, E.dscal + kSlotH);
     E.fetch(kSlotH + 1);
     return cplx(E.hscal[kSlotH].x, E.hscal[kSlotH].y);
   };
@@ -882,8 +948,7 @@ KReport bicgstab(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x
     rho = rho_new;
   }
   A(x, ws.tmp);  // final true residual (krylov.py:275)
-  E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, E.dscal + kSlotH, E.st); });
-  if (shard) dist->reduce(E.dscal + kSlotH);
+  red_subnorm(dist, b, ws.tmp, n, E.dscal + kSlotH);
   E.fetch(kSlotH + 1);
   rep.iterations = its;
   rep.final_relres = E.fetch_norm(kSlotH) / bnorm;
@@ -999,8 +1064,7 @@ void Multigrid::vcycle(const cd* b, cd* x, const cd* x0, const cd* addt, cd* xsu
   // r0 (mg.py:131): ||b|| from zero, ||b - M x0|| otherwise
   if (x0) {
     op->residual(b, x0, R[0]);
-    E.kl(KF_BLAS, 16.0 * op->n, [&] { launch_dot(R[0], R[0], op->n, E.red, E.dscal + kSlotMgR0, E.st); });
-    op->reduce(E.dscal + kSlotMgR0);
+    red_dot(op, R[0], R[0], op->n, E.dscal + kSlotMgR0);
   }
   cycle(0, b, x, x0, addt, xsum);
   // divergence guard (mg.py:133-138), evaluated on device; raised at the next host sync.
@@ -1282,7 +1346,7 @@ void MadpSolver::solve(const cd* b, cd* x) {
       rep.outer = fgmres(n1, Aop, &Mop, lv[1].bh, lv[1].xh, outer, lv[1].ws_defl, &hook, nullptr, A1);
       HDB_CUDA(cudaMemcpyAsync(x, lv[1].xh, sizeof(cd) * n1, cudaMemcpyDeviceToDevice, E.st));
     } else {
-      rep.outer = fgmres(n1, Aop, &Mop, b, x, outer, lv[1].ws_defl, &hook);
+      rep.outer = fgmres(n1, Aop, &Mop, b, x, outer, lv[1].ws_defl, &hook, nullptr, A1);
     }
     flush_counts();
     ev_resolve();

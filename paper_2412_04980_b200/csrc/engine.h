@@ -96,6 +96,9 @@ struct Engine {
   long long launches = 0;  // kernels launched through the engine (telemetry)
   long long syncs = 0;     // host synchronisations (Hessenberg reads etc.)
   Comm* comm = nullptr;    // row-slab communicator of this rank (owned), null on one rank
+  cd *rowpart = nullptr, *rowfull = nullptr;  // per-row partials (local rows / all ranks' rows)
+  int row_cap = 0;
+  cd* rows(int nyg);       // ensures both hold nyg entries, returns rowpart
   KProf kp;                // launch accounting / optional per-launch timing
   bool debug_sync = false; // HDB_DEBUG_SYNC=1: synchronise and check after every launch (fault location)
   void check_after(int fam);
@@ -177,7 +180,20 @@ struct LevelOp {
   void resnorm(const cd* b, const cd* u, cd* slot, cd* scratch) const;
   // reductions over this level's distribution (all-reduce when sharded)
   void reduce(cd* dev_slot) const;
+  // rank-count-invariant mode: the engine's row partials of this level (all ranks' rows
+  // gathered in global row order when sharded) summed in a fixed order into the slot
+  void finish_rows(cd* dev_slot) const;
 };
+
+// rank-count-invariant reductions (HDB_PINV=1 / hdb_option("pinv", 1)); see engine.cu
+bool pinv_mode();
+void set_pinv(int on);
+// <u, v>, the fused MGS step and ||b - t||^2 of a level, reduced over its distribution:
+// flat kernels + all-reduce, or the row-ordered form in the invariant mode (L may be null:
+// a vector without grid geometry)
+void red_dot(const LevelOp* L, const cd* u, const cd* v, long long n, cd* slot);
+void red_mgs(const LevelOp* L, cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, cd* slot, double bytes);
+void red_subnorm(const LevelOp* L, const cd* b, const cd* t, long long n, cd* slot);
 
 using LinOp = std::function<void(const cd* in, cd* out)>;
 

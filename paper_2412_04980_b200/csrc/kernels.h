@@ -56,6 +56,12 @@ int setup_stats_blocks(long long n);
 void launch_setup_stats(const double* a, long long n, double* part, unsigned* ticket, double* out3, cudaStream_t st);
 void launch_setup_point(cd* rhs, long long n, long long idx, double v, cudaStream_t st);
 
+// rank-count-invariant reductions: per-row partials (one block per row), then an ordered
+// sum over the global rows (parallel.py:168-195)
+void launch_rowdot(const cd* u, const cd* v, int nx, int ny, cd* rowpart, cudaStream_t st);
+void launch_rowmgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, int nx, int ny, cd* rowpart, cudaStream_t st);
+void launch_rowsubnorm(const cd* b, const cd* t, int nx, int ny, cd* rowpart, cudaStream_t st);
+void launch_rowsum(const cd* rows, int nyg, cd* dst, cudaStream_t st);
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st);
 void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st);
 void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st);

@@ -383,6 +383,68 @@ int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, 
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Rank-count-invariant reductions (parallel.py:168-195: reduce_dot is bitwise
+// invariant to the worker count).  One block per grid ROW forms that row's
+// partial with a fixed in-row order (thread-strided sums, then the block tree:
+// a function of nx only); the row partials of ALL ranks are then gathered in
+// global row order and summed by k_rowsum in a fixed order (a function of the
+// global row count only).  A slab decomposition cuts between rows, so every
+// rank count -- one GPU included -- produces the same bits.
+// op 0: <u, v>;  op 1: the fused MGS step of k_mgs (w -= h vi, then <vn, w>);
+// op 2: ||b - t||^2.
+template <int OP>
+__global__ void __launch_bounds__(kReduceThreads) k_rowred(cd* __restrict__ w, const cd* __restrict__ a,
+                                                           const cd* hsrc, const cd* __restrict__ c, int nx,
+                                                           cd* __restrict__ rowpart) {
+  const long long base = (long long)blockIdx.x * nx;
+  const cd h = (OP == 1 && a) ? *hsrc : mkc(0.0, 0.0);
+  cd acc = mkc(0.0, 0.0);
+  for (int i = threadIdx.x; i < nx; i += kReduceThreads) {
+    const long long p = base + i;
+    if (OP == 0) {
+      acc = c_conjmul_acc(acc, a[p], c[p]);
+    } else if (OP == 1) {
+      cd x = w[p];
+      if (a) {
+        x = c_sub(x, c_mul_np(h, a[p]));
+        w[p] = x;
+      }
+      acc = c_conjmul_acc(acc, c ? c[p] : x, x);
+    } else {
+      const cd d = c_sub(a[p], c[p]);
+      acc = c_conjmul_acc(acc, d, d);
+    }
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) rowpart[blockIdx.x] = acc;
+}
+
+constexpr int kRowSumThreads = 1024;
+__global__ void __launch_bounds__(kRowSumThreads) k_rowsum(const cd* __restrict__ rows, int nyg, cd* dst) {
+  cd v = mkc(0.0, 0.0);
+  for (int q = threadIdx.x; q < nyg; q += kRowSumThreads) {
+    const cd z = rows[q];
+    v.x += z.x;
+    v.y += z.y;
+  }
+  v = block_sum<kRowSumThreads>(v);
+  if (threadIdx.x == 0) *dst = v;
+}
+
+void launch_rowdot(const cd* u, const cd* v, int nx, int ny, cd* rowpart, cudaStream_t st) {
+  k_rowred<0><<<ny, kReduceThreads, 0, st>>>(nullptr, u, nullptr, v, nx, rowpart);
+}
+void launch_rowmgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, int nx, int ny, cd* rowpart, cudaStream_t st) {
+  k_rowred<1><<<ny, kReduceThreads, 0, st>>>(w, vi, hsrc, vn, nx, rowpart);
+}
+void launch_rowsubnorm(const cd* b, const cd* t, int nx, int ny, cd* rowpart, cudaStream_t st) {
+  k_rowred<2><<<ny, kReduceThreads, 0, st>>>(nullptr, b, nullptr, t, nx, rowpart);
+}
+void launch_rowsum(const cd* rows, int nyg, cd* dst, cudaStream_t st) {
+  k_rowsum<<<1, kRowSumThreads, 0, st>>>(rows, nyg, dst);
+}
+
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
   k_dot<<<reduce_blocks(n), kReduceThreads, 0, st>>>(u, v, n, ws.partials, ws.ticket, dst);
 }

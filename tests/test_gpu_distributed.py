@@ -116,3 +116,48 @@ def test_slab_solve_large_grid_tma_transfers():
         # iterations (measured: <= 4e-15 up to iteration 15, then 2e-12, 1e-10, 3e-9)
         assert d[:15].max() <= 1e-12 and d.max() <= 1e-8
     assert np.linalg.norm(x - xref) <= 1e-5 * np.linalg.norm(xref)
+
+
+@pytest.fixture
+def pinv_mode():
+    from paper_2412_04980_b200 import _lib
+    _lib.check(_lib.lib().hdb_option(b"pinv", 1))
+    yield
+    _lib.check(_lib.lib().hdb_option(b"pinv", 0))
+
+
+@pytest.mark.parametrize("case", ["c1s", "wedge_mixed"])
+def test_rank_count_invariant_mode_is_bit_identical_across_ranks(pinv_mode, case):
+    """hdb_option("pinv", 1): every reduction sums per-row partials in global row order
+    (reduce_dot's worker-count invariance, parallel.py:168-195), so the solve on 1, 2, 3
+    and 4 row slabs gives the same residual history and the same solution BIT FOR BIT
+    (P = 3 has odd cut rows), and still matches the reference's run."""
+    if case == "c1s":
+        build = lambda: hdb.mp1_problem(k=50.0, n=129, ml=2, boundary="sommerfeld")  # noqa: E731
+        ranks = [(2, 16), (3, 8), (4, 8)]
+    else:
+        def build():
+            vel = hdb.VelocityModel(kind="wedge", layers=[(-400.0, -200.0, 2000.0), (-800.0, -600.0, 1500.0),
+                                                          (0.0, 0.0, 3000.0)])
+            hier = hdb.build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=600.0 / 144, ml=4, velocity=vel, f=20.0,
+                                       boundary=("sommerfeld", "sommerfeld", "dirichlet", "sommerfeld"))
+            return hdb.grid.Problem("wedge-mixed", hier, hdb.point_source_rhs(hier, (300.0, -300.0)))
+        ranks = [(2, 16), (4, 8)]
+    prob = build()
+    with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
+        u, ref = s.solve(prob.rhs)
+    xref = u.grid_view(prob.hierarchy)
+    for P, min_rows in ranks:
+        res = _solve_ranks(build, P, min_rows)
+        assert res[0][3] >= 2, "expected at least two sharded grid depths"
+        x = np.concatenate([r[1] for r in sorted(res, key=lambda t: t[0])], axis=0)
+        for _, _, rep, _ in res:
+            assert rep.outer_iterations == ref.outer_iterations
+            assert rep.cycle_iters == ref.cycle_iters and rep.cslp_iters == ref.cslp_iters
+            assert list(rep.residual_history) == list(ref.residual_history), f"history differs at P={P}"
+        np.testing.assert_array_equal(x, xref, err_msg=f"solution differs at P={P}")
+    if case == "c1s":
+        from gold import golden
+        g = golden("solve_c1s.npz")
+        assert np.abs(np.array(ref.residual_history) - g["residual_history"]).max() <= 1e-9
+        assert np.linalg.norm(xref - g["solution"]) <= 1e-8 * np.linalg.norm(g["solution"])
