@@ -268,10 +268,11 @@ def kernel_roofline(hdb, hier, reps=20):
 # kernel families (csrc/engine.h KFam) that stream HBM; the others are latency /
 # synchronisation work (resident Krylov solves, control kernels)
 HBM_FAMILIES = ("apply5", "residual5", "jacobi5", "resnorm5", "galerkin", "restrict", "prolong", "mgs_coop",
-                "mgs_chain", "blas1")
-FAMILY_KERNELS = {"mgs_coop": "k_mgs_grid_t / k_mgs_grid / k_mgs_grid2 (one-launch MGS step, Arnoldi of the "
-                              "launch-driven levels)",
-                  "galerkin": "k_rgv<3> / k_rgh<2> (radius-3 / radius-2 Galerkin stencils)",
+                "mgs_chain", "blas1", "resrestrict")
+FAMILY_KERNELS = {"mgs_coop": "k_mgs_ls (one-launch low-synchronisation MGS step, Arnoldi of the launch-driven "
+                              "levels; k_mgs_grid_t / k_mgs_grid2 in the MGS-order mode)",
+                  "galerkin": "k_rgs<2/3> (separable radius-2 / radius-3 Galerkin stencils)",
+                  "resrestrict": "k_resrestrict (fused MG residual + restriction)",
                   "apply5": "k_r1w<0> (5-point apply)", "residual5": "k_r1w<1> (5-point residual)",
                   "jacobi5": "k_r1w<2,3> (Jacobi sweep)", "mgs_chain": "k_mgs (fused MGS launches)",
                   "restrict": "k_restrict_t (TMA Z^T)", "prolong": "k_prolong_t (TMA Z)",

@@ -60,6 +60,10 @@ int hdb_stats(long long* launches, long long* bytes_alloc);
  * engine (hdb_thread_engine_begin) — used to test the slab path on one GPU    */
 int hdb_comm_unique_id(char* out128);
 int hdb_comm_init_nccl(const char* id128, int nranks, int rank);
+/* one-rank NCCL round trip on this engine's device (library resolution, communicator,
+   all-reduce / grouped send-recv / all-gather of the slab path, results checked): what a
+   single GPU can verify of the NCCL transport */
+int hdb_comm_selftest_nccl(void);
 int hdb_comm_init_threads(long long group, int nranks, int rank);
 /* host-only rule of the sharded -> replicated level transition: the coarse rows
  * [*row0, *row0 + *ny) this rank restricts before the all-gather, given every
@@ -215,7 +219,10 @@ int hdb_op_set_separable(hdb_op* op, const double* sa, const double* sm, double 
  * "pinv": 1 every reduction of a level sums per-row partials in global row order
  * and every level keeps the launch-driven Krylov path, so a solve is bit-identical
  * on any number of ranks (reduce_dot's worker-count invariance, parallel.py:168-195;
- * HDB_PINV=1); 0 (default) the fast per-rank reduction trees                    */
+ * HDB_PINV=1); 0 (default) the fast per-rank reduction trees.
+ * "lsh_prefer": 1 levels beyond the one-launch low-synchronisation step (> 7168
+ * points per CTA) use its HBM-streaming form instead of the MGS-order one-launch
+ * kernels (HDB_LSH_PREFER=1); 0 (default: measured equal or slower)             */
 int hdb_option(const char* name, int value);
 
 /* ---- launch accounting / timing (measurement, not on the reference API) ---- */

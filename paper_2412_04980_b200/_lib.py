@@ -37,6 +37,7 @@ SIGNATURES = {
     "hdb_comm_unique_id": [C.c_char_p],
     "hdb_comm_init_nccl": [C.c_char_p, i32, i32],
     "hdb_comm_init_threads": [i64, i32, i32],
+    "hdb_comm_selftest_nccl": [],
     "hdb_plan_gather_rows": [P(i32), i32, i32, i32, P(i32), P(i32)],
     "hdb_thread_engine_begin": [i32],
     "hdb_thread_engine_end": [],

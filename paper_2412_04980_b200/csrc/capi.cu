@@ -259,6 +259,9 @@ int hdb_comm_init_nccl(const char* id128, int nranks, int rank) {
     if (nranks > 1) E.comm = make_nccl_comm(id128, nranks, rank);
   });
 }
+int hdb_comm_selftest_nccl(void) {
+  return guarded([&] { nccl_selftest(engine().st); });
+}
 int hdb_comm_init_threads(long long group, int nranks, int rank) {
   return guarded([&] {
     Engine& E = engine();
@@ -466,6 +469,21 @@ int hdb_op_gmres(hdb_op* op, const void* b, void* x, double rel_tol, int max_ite
       *final_relres = h_rel;
       return;
     }
+    if (mode == -2) {  // the device-driven loop of large levels (Givens / stopping test on device)
+      if (!op->dres) op->dres = (int*)E.alloc_bytes(16);
+      int* dits = op->dres;
+      double* drel = (double*)(op->dres + 2);
+      if (!gmres_device(L, (const cd*)b, (cd*)x, Stop{rel_tol, max_iters}, op->ws, dits, drel))
+        throw Error(E_ARG, "level does not qualify for the device-driven GMRES loop");
+      int h_its = 0;
+      double h_rel = 0.0;
+      HDB_CUDA(cudaMemcpyAsync(&h_its, dits, sizeof(int), cudaMemcpyDeviceToHost, E.st));
+      HDB_CUDA(cudaMemcpyAsync(&h_rel, drel, sizeof(double), cudaMemcpyDeviceToHost, E.st));
+      E.fetch(1);
+      *iterations = h_its;
+      *final_relres = h_rel;
+      return;
+    }
     LinOp Aop = [L](const cd* in, cd* o) { L->apply(in, o); };
     KReport r = fgmres(L->n, Aop, nullptr, (const cd*)b, (cd*)x, Stop{rel_tol, max_iters}, op->ws);
     *iterations = r.iterations;
@@ -659,6 +677,7 @@ int hdb_option(const char* name, int value) {
     if (k == "mgs_ls") set_mgs_ls(value);
     else if (k == "rg_exact") set_rg_exact(value);
     else if (k == "pinv") set_pinv(value);
+    else if (k == "lsh_prefer") set_lsh_prefer(value);
     else throw Error(E_ARG, "unknown option " + k);
   });
 }

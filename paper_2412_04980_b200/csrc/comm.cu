@@ -3,6 +3,7 @@
 #include <condition_variable>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -124,6 +125,7 @@ struct ThreadGroup {
   std::vector<const void*> p0, p1;    // published device pointers
   std::vector<std::vector<double>> vals;
   std::vector<long long> tag;          // per-rank (kind, size) of the collective being entered
+  std::vector<int> dev;                // CUDA device of every rank (one GPU per rank thread: P2P halos)
   void barrier() {
     std::unique_lock<std::mutex> lk(m);
     const long long g = gen;
@@ -154,9 +156,29 @@ struct ThreadComm : Comm {
       g->p1.assign(n, nullptr);
       g->vals.assign(n, {});
       g->tag.assign(n, 0);
+      g->dev.assign(n, -1);
       g_groups[group] = g;
     } else {
       g = it->second;
+    }
+    cudaGetDevice(&g->dev[r]);
+  }
+  // Rank threads that own different GPUs of one node exchange halos with direct
+  // peer-to-peer copies over NVLink (cudaMemcpyAsync between peer allocations): enable
+  // peer access to the neighbours' devices once, after every rank has published its device.
+  bool peers_ready = false;
+  void enable_peers() {
+    if (peers_ready) return;
+    peers_ready = true;
+    for (int nb : {rank - 1, rank + 1}) {
+      if (nb < 0 || nb >= size || g->dev[nb] < 0 || g->dev[nb] == g->dev[rank]) continue;
+      int can = 0;
+      if (cudaDeviceCanAccessPeer(&can, g->dev[rank], g->dev[nb]) == cudaSuccess && can) {
+        const cudaError_t e = cudaDeviceEnablePeerAccess(g->dev[nb], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          throw Error(E_CUDA, std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+      }
     }
   }
   // every rank must enter the same collective: publish (kind, size), check after the barrier
@@ -186,6 +208,7 @@ struct ThreadComm : Comm {
     g->p0[rank] = su;  // my first rows (for rank-1)
     g->p1[rank] = sd;  // my last rows (for rank+1)
     enter(2, (long long)bu);
+    enable_peers();
     if (rank > 0) HDB_CUDA(cudaMemcpyAsync(ru, g->p1[rank - 1], bu, cudaMemcpyDeviceToDevice, st));
     if (rank < size - 1) HDB_CUDA(cudaMemcpyAsync(rd, g->p0[rank + 1], bd, cudaMemcpyDeviceToDevice, st));
     HDB_CUDA(cudaStreamSynchronize(st));
@@ -204,5 +227,30 @@ struct ThreadComm : Comm {
 };
 
 Comm* make_thread_comm(long long group, int n, int r) { return new ThreadComm(group, n, r); }
+
+// One-rank NCCL round trip on the calling engine's device and stream: resolves the
+// library, creates a communicator, runs the three collectives the slab path uses and
+// checks their results (a single GPU can exercise the binding, not the transport).
+void nccl_selftest(cudaStream_t st) {
+  char id[128];
+  nccl_unique_id(id);
+  std::unique_ptr<Comm> c(make_nccl_comm(id, 1, 0));
+  const int n = 6;
+  double h[n] = {1.5, -2.25, 3.0, 0.0, 1e300, -7.0}, back[2 * n];
+  double *d = nullptr, *full = nullptr;
+  HDB_CUDA(cudaMalloc(&d, sizeof(double) * n));
+  HDB_CUDA(cudaMalloc(&full, sizeof(double) * n));
+  HDB_CUDA(cudaMemcpyAsync(d, h, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  c->allreduce(d, n, st);                                            // sum over one rank: unchanged
+  c->exchange(d, d, 16, d + 2, d + 2, 16, st);                       // no neighbours: nothing moves
+  c->allgatherv(d, full, {0}, {sizeof(double) * n}, st);             // one slab: a copy
+  HDB_CUDA(cudaMemcpyAsync(back, d, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  HDB_CUDA(cudaMemcpyAsync(back + n, full, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+  HDB_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  cudaFree(full);
+  for (int i = 0; i < n; ++i)
+    if (back[i] != h[i] || back[n + i] != h[i]) throw Error(E_CUDA, "NCCL self-test: collective changed the data");
+}
 
 }  // namespace hdb

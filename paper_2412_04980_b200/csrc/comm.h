@@ -30,5 +30,6 @@ struct Comm {
 Comm* make_nccl_comm(const char* unique_id128, int nranks, int rank);  // throws on failure
 void nccl_unique_id(char* out128);
 Comm* make_thread_comm(long long group, int nranks, int rank);
+void nccl_selftest(cudaStream_t st);  // one-rank round trip through the NCCL binding (throws on failure)
 
 }  // namespace hdb

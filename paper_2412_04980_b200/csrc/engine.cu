@@ -438,6 +438,23 @@ static long long lsh_shard_min() {
   return v < 0 ? (1LL << 62) : v;
 }
 
+// Levels whose w slice does not fit the one-launch low-synchronisation step (> 7168 points per
+// CTA) CAN take the HBM-streaming form of the same algorithm instead of the MGS-order one-launch
+// kernels (hdb_option("lsh_prefer", 1) / HDB_LSH_PREFER=1; host-driven and device-driven loops).
+// Off by default: measured equal on config 5's 2049^2 level (2.59 vs 2.58 s of MGS time per
+// solve) and slower on config 4's 3065 x 1001 level (9.9 vs 9.1 s) -- two passes over the basis
+// at ~0.9 of the copy peak move as many bytes per unit time as one pass with j + 2 grid
+// barriers (profiles/r03f_bench_*.json vs r03d_bench_*.json).
+static int g_lsh_prefer = -1;
+void set_lsh_prefer(int on) { g_lsh_prefer = on ? 1 : 0; }
+bool mgs_prefers_lsh(long long n, int cap) {
+  if (g_lsh_prefer < 0) {
+    const char* e = getenv("HDB_LSH_PREFER");
+    g_lsh_prefer = (e && atoi(e) != 0) ? 1 : 0;
+  }
+  return g_lsh_prefer && mgs_ls_on() && n >= lsh_min() && cap <= 511 && !mgs_ls_fits(n, 0);
+}
+
 long long coop_mgs_min() {
   static long long v = -1;
   if (v < 0) v = env_ll("HDB_COOP_MGS_N", 2000);  // (config 3 @40 Hz: 1018 -> 997 ms vs 150000)
@@ -589,7 +606,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
         ws.dV_n++;
       }
     };
-    if (!shard && !pinv && n >= coop_mgs_min()) {
+    if (!shard && !pinv && n >= coop_mgs_min() && !mgs_prefers_lsh(n, stop.max_iters)) {
       if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
       if (!ws.tg) ws.tg = E.alloc(mgs_ls_tg_elems());
       ensure_dv();
@@ -743,11 +760,19 @@ static void ensure_vtab(KWS& ws, int upto) {
 bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int* its_dev, double* rel_dev) {
   const long long n = op->n;
   const int cap = stop.max_iters;
+  const bool lsh = mgs_prefers_lsh(n, cap);  // streaming low-synchronisation step instead of the one-launch kernels
   if (!gmres_device_enabled() || pinv_mode() || op->sharded || n < coop_mgs_min() || cap < 1 || cap + kSlotH + 2 >= 900 ||
-      !(stop.rel_tol < 1.0) || !mgs_grid_fits(n))
+      !(stop.rel_tol < 1.0) || !(lsh || mgs_grid_fits(n)))
     return false;
   Engine& E = engine();
   ws.ensure(n, cap, false);
+  if (lsh && ws.tgh_cap < cap) {
+    E.free(ws.tgh);
+    E.free(ws.lpart);
+    ws.tgh = E.alloc((long long)(cap + 1) * (cap + 2) / 2);
+    ws.lpart = E.alloc(lsh_part_elems(n, cap));
+    ws.tgh_cap = cap;
+  }
   if (!ws.gpart) ws.gpart = E.alloc(2LL * resident_grid_ctas() * (resident_vec_cap() + 1) + 2LL * (resident_vec_cap() + 1));
   if (!ws.tg) ws.tg = E.alloc(mgs_ls_tg_elems());
   if (ws.gst_cap < cap) {
@@ -779,8 +804,18 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
       E.kl(op->c.radius == 1 ? KF_APPLY5 : KF_GALERKIN, 0.0,
            [&] { launch_apply(cs, op->g, ws.v(j), nullptr, op->ksq, ws.v(j + 1), 0, E.st); });  // krylov.py:119
       int rc = 0;
-      E.kl(KF_MGS_COOP, 0.0,
-           [&] { rc = launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip, ws.tg); });
+      if (lsh) {
+        const int nl = (j == 0 ? 1 : (j + 7) / 8) + (j + 8) / 8 + 3;
+        E.kl(KF_MGS_CHAIN, 0.0, [&] {
+          rc = launch_mgs_lsh(ws.v(j + 1), (const cd* const*)ws.dV, ws.V.data(), j, n, ws.lpart, ws.tgh, hcol, E.st,
+                              std::function<void(cd*, int)>(), skip);
+          launch_scale_dev(ws.v(j + 1), ws.v(j + 1), hcol + j + 1, n, E.st, skip);  // V_{j+1} = w / ||w||
+        }, nl);
+      } else {
+        E.kl(KF_MGS_COOP, 0.0, [&] {
+          rc = launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip, ws.tg);
+        });
+      }
       if (rc != 0) {
         const cudaError_t err = cudaGetLastError();
         throw Error(E_CUDA, std::string("cooperative MGS launch: ") + cudaGetErrorString(err));
@@ -796,7 +831,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
   const int its = ws.hflags[1];
   for (int q = 0; q < its; ++q) {
     E.kp.bytes[op->c.radius == 1 ? KF_APPLY5 : KF_GALERKIN] += 40.0 * n;
-    E.kp.bytes[KF_MGS_COOP] += (16.0 * (q + 1) + 32.0) * n;
+    E.kp.bytes[lsh ? KF_MGS_CHAIN : KF_MGS_COOP] += (16.0 * (q + 1) + 32.0) * n + (lsh ? 32.0 * n : 0.0);
   }
   if (its == 0) {
     HDB_CUDA(cudaMemsetAsync(x, 0, sizeof(cd) * n, E.st));  // b = 0 (or non-finite ||b||: flag raised)

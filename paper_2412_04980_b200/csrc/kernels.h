@@ -69,7 +69,8 @@ void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st
 void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd* x, long long n, cudaStream_t st);
 void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st);
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st);
-void launch_scale_dev(const cd* x, cd* out, const cd* nrm2, long long n, cudaStream_t st);
+void launch_scale_dev(const cd* x, cd* out, const cd* nrm2, long long n, cudaStream_t st,
+                      const int* skip = nullptr);  // out = x / sqrt(nrm2) (0 when the norm is 0)
 void launch_step1(const cd* b2, const cd* h0, const cd* hn2, cd* y, int* its, cd* flag, cudaStream_t st);
 void launch_finite_guard(const cd* v, cd* flag, cudaStream_t st);
 void launch_axpy(const cd* y, cd a, const cd* x, cd* out, long long n, int sub, cudaStream_t st);
@@ -99,7 +100,13 @@ bool mgs_ls_fits(long long n, int j);
 long long lsh_part_elems(long long n, int maxj);
 // allreduce (may be empty): sums a device vector over the ranks of a sharded level, in place
 int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, long long n, cd* part, cd* Tg,
-                   cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce);
+                   cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce,
+                   const int* skip = nullptr);  // skip: device flag of a device-driven loop (nonzero: do nothing)
+// levels whose w slice does not fit the one-launch low-synchronisation step take the streaming
+// form instead of the MGS-order one-launch kernels when asked to (off by default: measured equal
+// or slower, engine.cu)
+bool mgs_prefers_lsh(long long n, int cap);
+void set_lsh_prefer(int on);
 bool mgs_ls_on();
 void set_mgs_ls(int on);
 void set_rg_exact(int on);

@@ -121,7 +121,9 @@ __global__ void __launch_bounds__(256) k_gemv(const cd* __restrict__ A, const cd
 }
 
 // out = x * (1/sqrt(max(nrm2->x, 0)))  (V0 = r0 / beta with beta on device; 0 if beta == 0)
-__global__ void k_scale_dev(const cd* __restrict__ x, cd* __restrict__ out, const cd* nrm2, long long n) {
+__global__ void k_scale_dev(const cd* __restrict__ x, cd* __restrict__ out, const cd* nrm2, long long n,
+                            const int* skip) {
+  if (skip && *skip) return;
   const double beta = sqrt(fmax(nrm2->x, 0.0));
   const double inv = beta > 0.0 ? 1.0 / beta : 0.0;
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
@@ -199,7 +201,8 @@ constexpr int kLsPE = 2 * kLsG + 1;  // partial elements per block per group
 
 __global__ void __launch_bounds__(kReduceThreads, 2) k_lsh_a(const cd* __restrict__ w, const cd* __restrict__ vj,
                                                           const cd* const* V, int k0, int kn, int with_gj,
-                                                          long long n, cd* part) {
+                                                          long long n, cd* part, const int* skip) {
+  if (skip && *skip) return;  // device-driven loops: the solve is already done
   cd g[kLsG], l[kLsG], gj = mkc(0.0, 0.0);
   const cd* vk[kLsG];
 #pragma unroll
@@ -246,7 +249,8 @@ __device__ __forceinline__ void cfma_(cd& a, cd x, cd y) {  // a += x * y
 // of 1024 threads; part: [group][block][kLsPE].  A sharded level all-reduces `sums`
 // (one collective per Arnoldi step) before k_lsh_th.
 constexpr int kLshF = 1024;
-__global__ void __launch_bounds__(kLshF) k_lsh_sum(const cd* part, int nblocks, int j, cd* sums) {
+__global__ void __launch_bounds__(kLshF) k_lsh_sum(const cd* part, int nblocks, int j, cd* sums, const int* skip) {
+  if (skip && *skip) return;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int ne = 2 * j + 1;
   for (int e = wid; e < ne; e += kLshF / 32) {
@@ -273,9 +277,10 @@ __global__ void __launch_bounds__(kLshF) k_lsh_sum(const cd* part, int nblocks, 
 }
 
 // the new T row and h = T g from the reduced sums (every rank identically)
-__global__ void __launch_bounds__(kLshF) k_lsh_th(const cd* sums, int j, cd* Tg, cd* hout) {
+__global__ void __launch_bounds__(kLshF) k_lsh_th(const cd* sums, int j, cd* Tg, cd* hout, const int* skip) {
   __shared__ cd tot[2 * 512 + 1];
   __shared__ cd trow[512];
+  if (skip && *skip) return;
   const int t = threadIdx.x;
   for (int e = t; e < 2 * j + 1; e += kLshF) tot[e] = sums[e];
   __syncthreads();
@@ -315,7 +320,9 @@ __global__ void __launch_bounds__(kLshF) k_lsh_th(const cd* sums, int j, cd* Tg,
 
 // w -= h_k V_k for k = kfirst, kfirst-1, ..., kfirst-kn+1 (descending); norm != 0: per-block ||w||^2
 __global__ void __launch_bounds__(kReduceThreads) k_lsh_b(cd* __restrict__ w, const cd* const* V, const cd* h,
-                                                          int kfirst, int kn, int norm, long long n, cd* part) {
+                                                          int kfirst, int kn, int norm, long long n, cd* part,
+                                                          const int* skip) {
+  if (skip && *skip) return;
   cd hk[kLsG];
   const cd* vk[kLsG];
 #pragma unroll
@@ -341,7 +348,8 @@ __global__ void __launch_bounds__(kReduceThreads) k_lsh_b(cd* __restrict__ w, co
   }
 }
 
-__global__ void __launch_bounds__(kReduceThreads) k_lsh_norm(const cd* part, int nblocks, cd* dst) {
+__global__ void __launch_bounds__(kReduceThreads) k_lsh_norm(const cd* part, int nblocks, cd* dst, const int* skip) {
+  if (skip && *skip) return;
   cd v = mkc(0.0, 0.0);
   for (int b = threadIdx.x; b < nblocks; b += blockDim.x) { v.x += part[b].x; v.y += part[b].y; }
   v = block_sum(v);
@@ -357,7 +365,7 @@ long long lsh_part_elems(long long n, int maxj) {
 }
 
 int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, long long n, cd* part, cd* Tg,
-                   cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce) {
+                   cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce, const int* skip) {
   if (j > 511) return 1;
   const int G = reduce_blocks(n);
   cd* sums = part;
@@ -368,17 +376,17 @@ int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, 
   for (int q = 0; q < ga; ++q) {
     const int k0 = q * kLsG, kn = j - k0 < kLsG ? j - k0 : kLsG;
     k_lsh_a<<<G, kReduceThreads, 0, st>>>(w, Vhost[j], Vtab, k0, kn > 0 ? kn : 0, q == 0, n,
-                                          apart + (long long)q * G * kLsPE);
+                                          apart + (long long)q * G * kLsPE, skip);
   }
-  k_lsh_sum<<<1, kLshF, 0, st>>>(apart, G, j, sums);
+  k_lsh_sum<<<1, kLshF, 0, st>>>(apart, G, j, sums, skip);
   if (allreduce) allreduce(sums, 2 * j + 1);
-  k_lsh_th<<<1, kLshF, 0, st>>>(sums, j, Tg, hout);
+  k_lsh_th<<<1, kLshF, 0, st>>>(sums, j, Tg, hout, skip);
   const int gb = (j + 1 + kLsG - 1) / kLsG;
   for (int q = 0; q < gb; ++q) {
     const int kfirst = j - q * kLsG, kn = kfirst + 1 < kLsG ? kfirst + 1 : kLsG;
-    k_lsh_b<<<G, kReduceThreads, 0, st>>>(w, Vtab, hout, kfirst, kn, q == gb - 1, n, npart);
+    k_lsh_b<<<G, kReduceThreads, 0, st>>>(w, Vtab, hout, kfirst, kn, q == gb - 1, n, npart, skip);
   }
-  k_lsh_norm<<<1, kReduceThreads, 0, st>>>(npart, G, hout + j + 1);
+  k_lsh_norm<<<1, kReduceThreads, 0, st>>>(npart, G, hout + j + 1, skip);
   if (allreduce) allreduce(hout + j + 1, 1);
   return 0;
 }
@@ -472,8 +480,8 @@ void launch_bicg_p(const cd* r, cd* p, const cd* v, cd beta, cd omega, long long
 void launch_gemv(const cd* A, const cd* b, cd* x, int n, cudaStream_t st) {
   k_gemv<<<(n * 32 + 255) / 256, 256, 0, st>>>(A, b, x, n);
 }
-void launch_scale_dev(const cd* x, cd* out, const cd* nrm2, long long n, cudaStream_t st) {
-  k_scale_dev<<<ew_blocks(n), 256, 0, st>>>(x, out, nrm2, n);
+void launch_scale_dev(const cd* x, cd* out, const cd* nrm2, long long n, cudaStream_t st, const int* skip) {
+  k_scale_dev<<<ew_blocks(n), 256, 0, st>>>(x, out, nrm2, n, skip);
 }
 void launch_step1(const cd* b2, const cd* h0, const cd* hn2, cd* y, int* its, cd* flag, cudaStream_t st) {
   k_step1<<<1, 1, 0, st>>>(b2, h0, hn2, y, its, flag);

@@ -1149,6 +1149,23 @@ __device__ __forceinline__ void load_slice_smem(cd* dst, const cd* src, int cnt)
   }
 }
 
+// 16-byte load with an L2 eviction-priority hint (createpolicy handle)
+__device__ __forceinline__ uint64_t l2pol_keep() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2pol_drop() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ cd ld_cd_hint(const cd* p, uint64_t pol) {
+  cd v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
 constexpr int kMgsPPT = 16;  // points per thread held in registers
 
 __global__ void __launch_bounds__(kRT) k_mgs_grid(cd* w, const cd* const* V, int j, long long n, cd* gpart,
@@ -1240,7 +1257,7 @@ __device__ __forceinline__ cd grid_reduce_small(cd v, MgsSmem& s, int& buf, cd* 
 }
 
 __global__ void __launch_bounds__(kRT) k_mgs_grid2(cd* w, const cd* const* V, int j, long long n, cd* gpart,
-                                                   cd* hout, int ks, const int* skip) {
+                                                   cd* hout, int ks, const int* skip, int hint) {
   if (skip && *skip) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   MgsSmem& s = *reinterpret_cast<MgsSmem*>(smem_raw);
@@ -1261,39 +1278,127 @@ __global__ void __launch_bounds__(kRT) k_mgs_grid2(cd* w, const cd* const* V, in
   }
   const int qg = t + (ks + kMgsReg) * kRT;  // first point of the global (L2-resident) tier
   cd* wgl = w + p0;
-  for (int i = 0; i <= j; ++i) {
-    const cd* vi = V[i] + p0;
-    cd a = mkc(0.0, 0.0);
-    for (int k = 0; k < ks; ++k) {
-      const int q = t + k * kRT;
-      if (q < cnt) a = c_conjmul_acc(a, vi[q], ws[k * kRT + t]);
+  // Every pass batches its basis loads (kB slots per thread in flight before the dependent
+  // arithmetic).  After the first dot, ONE fused pass per MGS step applies w -= h_i V_i and
+  // forms the next reduction from the updated values -- <V_{i+1}, w> or, after the last
+  // update, <w, w> -- so V_{i+1} streams from HBM while V_i is re-read (L2) and a step costs
+  // one pass and one grid reduction.  Per thread the sums keep their slot order (shared
+  // tier, register tier, global tier): bit-identical to separate dot and update passes.
+  // L2 priorities (hint != 0): a basis vector is read twice, in two consecutive passes -- first
+  // as V_{i+1} (kept: evict_last), then as V_i (its last use: evict_first) -- so one vector plus
+  // the global tier of w stay L2-resident and each pass reads one vector from HBM.
+  const uint64_t pk = l2pol_keep(), pd = l2pol_drop();
+  auto ldk = [&](const cd* p) { return hint ? ld_cd_hint(p, pk) : *p; };
+  auto ldd = [&](const cd* p) { return hint ? ld_cd_hint(p, pd) : *p; };
+  constexpr int kB = 4;   // register-tier batch
+  constexpr int kS = 4;   // shared-memory tier batch (8 measured slower: spills; profiles/r03i_bench_*.json)
+  cd a = mkc(0.0, 0.0);
+  {
+    const cd* v0 = V[0] + p0;
+    for (int k0 = 0; k0 < ks; k0 += kS) {
+      cd v[kS];
+#pragma unroll
+      for (int u = 0; u < kS; ++u) {
+        const int q = t + (k0 + u) * kRT;
+        v[u] = (k0 + u < ks && q < cnt) ? ldk(v0 + q) : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kS; ++u) {
+        const int q = t + (k0 + u) * kRT;
+        if (k0 + u < ks && q < cnt) a = c_conjmul_acc(a, v[u], ws[(k0 + u) * kRT + t]);
+      }
     }
 #pragma unroll
-    for (int k = 0; k < kMgsReg; ++k) {
-      const int q = t + (ks + k) * kRT;
-      if (q < cnt) a = c_conjmul_acc(a, vi[q], wr[k]);
+    for (int k0 = 0; k0 < kMgsReg; k0 += kB) {
+      cd v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = t + (ks + k0 + u) * kRT;
+        v[u] = q < cnt ? ldk(v0 + q) : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = t + (ks + k0 + u) * kRT;
+        if (q < cnt) a = c_conjmul_acc(a, v[u], wr[k0 + u]);
+      }
     }
-    for (int q = qg; q < cnt; q += kRT) a = c_conjmul_acc(a, vi[q], wgl[q]);
+    for (int q0 = qg; q0 < cnt; q0 += kB * kRT) {
+      cd v[kB], x[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = q0 + u * kRT;
+        v[u] = q < cnt ? ldk(v0 + q) : mkc(0.0, 0.0);
+        x[u] = q < cnt ? wgl[q] : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (q0 + u * kRT < cnt) a = c_conjmul_acc(a, v[u], x[u]);
+    }
+  }
+  for (int i = 0; i <= j; ++i) {
     const cd h = grid_reduce_small(a, s, buf, gpart, gr);
     if (rank == 0 && t == 0) hout[i] = h;
-    for (int k = 0; k < ks; ++k) {
-      const int q = t + k * kRT;
-      if (q < cnt) ws[k * kRT + t] = c_sub(ws[k * kRT + t], c_mul_np(h, vi[q]));
+    const cd* vi = V[i] + p0;
+    const bool last = i == j;               // the next reduction is <w, w>
+    const cd* vn = last ? vi : V[i + 1] + p0;  // (last: vn unused, any valid pointer)
+    a = mkc(0.0, 0.0);
+    for (int k0 = 0; k0 < ks; k0 += kS) {
+      cd v[kS], n2[kS];
+#pragma unroll
+      for (int u = 0; u < kS; ++u) {
+        const int q = t + (k0 + u) * kRT;
+        const bool ok = k0 + u < ks && q < cnt;
+        v[u] = ok ? ldd(vi + q) : mkc(0.0, 0.0);
+        n2[u] = (ok && !last) ? ldk(vn + q) : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kS; ++u) {
+        const int q = t + (k0 + u) * kRT;
+        if (k0 + u < ks && q < cnt) {
+          const cd x = c_sub(ws[(k0 + u) * kRT + t], c_mul_np(h, v[u]));
+          ws[(k0 + u) * kRT + t] = x;
+          a = c_conjmul_acc(a, last ? x : n2[u], x);
+        }
+      }
     }
 #pragma unroll
-    for (int k = 0; k < kMgsReg; ++k) {
-      const int q = t + (ks + k) * kRT;
-      if (q < cnt) wr[k] = c_sub(wr[k], c_mul_np(h, vi[q]));
+    for (int k0 = 0; k0 < kMgsReg; k0 += kB) {
+      cd v[kB], n2[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = t + (ks + k0 + u) * kRT;
+        v[u] = q < cnt ? ldd(vi + q) : mkc(0.0, 0.0);
+        n2[u] = (q < cnt && !last) ? ldk(vn + q) : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = t + (ks + k0 + u) * kRT;
+        if (q < cnt) {
+          wr[k0 + u] = c_sub(wr[k0 + u], c_mul_np(h, v[u]));
+          a = c_conjmul_acc(a, last ? wr[k0 + u] : n2[u], wr[k0 + u]);
+        }
+      }
     }
-    for (int q = qg; q < cnt; q += kRT) wgl[q] = c_sub(wgl[q], c_mul_np(h, vi[q]));
+    for (int q0 = qg; q0 < cnt; q0 += kB * kRT) {
+      cd v[kB], n2[kB], x[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = q0 + u * kRT;
+        v[u] = q < cnt ? ldd(vi + q) : mkc(0.0, 0.0);
+        n2[u] = (q < cnt && !last) ? ldk(vn + q) : mkc(0.0, 0.0);
+        x[u] = q < cnt ? wgl[q] : mkc(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int q = q0 + u * kRT;
+        if (q < cnt) {
+          const cd y = c_sub(x[u], c_mul_np(h, v[u]));
+          wgl[q] = y;
+          a = c_conjmul_acc(a, last ? y : n2[u], y);
+        }
+      }
+    }
   }
-  cd a = mkc(0.0, 0.0);
-  for (int k = 0; k < ks; ++k)
-    if (t + k * kRT < cnt) a = c_conjmul_acc(a, ws[k * kRT + t], ws[k * kRT + t]);
-#pragma unroll
-  for (int k = 0; k < kMgsReg; ++k)
-    if (t + (ks + k) * kRT < cnt) a = c_conjmul_acc(a, wr[k], wr[k]);
-  for (int q = qg; q < cnt; q += kRT) a = c_conjmul_acc(a, wgl[q], wgl[q]);
   const cd nn = grid_reduce_small(a, s, buf, gpart, gr);
   if (rank == 0 && t == 0) hout[j + 1] = nn;
   const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
@@ -1802,7 +1907,12 @@ int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart,
     const size_t sm2 = head + (size_t)ks * kRT * sizeof(cd);
     if (!ensure_smem_attr((const void*)k_mgs_grid2, sm2)) return 1;
     int ksi = (int)ks;
-    void* args2[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &ksi, (void*)&skip};
+    static const int hint2 = [] {  // HDB_MGS2_HINT=0: plain loads in the hybrid MGS step
+      const char* e = getenv("HDB_MGS2_HINT");
+      return e ? atoi(e) : 1;
+    }();
+    int hint = hint2;
+    void* args2[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &ksi, (void*)&skip, &hint};
     return cudaLaunchCooperativeKernel((void*)k_mgs_grid2, dim3(g_grid), dim3(kRT), args2, sm2, st) == cudaSuccess ? 0 : 1;
   }
   if (plan == 3) {

@@ -89,10 +89,11 @@ def synthetic_layered_problem(f: float, h: float, ml: int, seed: int = 2412, ras
     return Problem("synthetic-layered", hier, rhs)
 
 
-def c5_problem(P: int = 1, ml: int = 7, device: bool = False) -> Problem:
+def c5_problem(P: int = 1, ml: int = 7, device: bool = False, cells: int = 8192) -> Problem:
     """BASELINE configs[4] (weak scaling): [0,1] x [0,P], h = 1/8192 (8193 x (8192P+1) points,
-    SURVEY D8), k = (0.5 / h^2)^(1/3) so that k^3 h^2 = 0.5, centre source, Sommerfeld."""
-    h = 1.0 / 8192
+    SURVEY D8), k = (0.5 / h^2)^(1/3) so that k^3 h^2 = 0.5, centre source, Sommerfeld.
+    `cells` per unit length scales the instance down (the parity fixture uses 1024, P = 2)."""
+    h = 1.0 / cells
     k = (0.5 / h ** 2) ** (1.0 / 3.0)
     hier = build_hierarchy(((0.0, 1.0), (0.0, float(P))), h=h, ml=ml, k=k, boundary="sommerfeld", device=device)
     rhs = point_source_device(hier, (0.5, P / 2.0)) if device else point_source_rhs(hier, (0.5, P / 2.0))

@@ -55,6 +55,11 @@ def make(config):
         hier = build_hierarchy(((0.0, 600.0), (-1000.0, 0.0)), h=0.5, ml=5, velocity=vel, f=f)
         rhs = point_source_rhs(hier, (300.0, 0.0))
         return hier, rhs.grid_view(hier)
+    if config == "c5s":           # BASELINE configs[4] shape at reduced size: [0,1] x [0,2], h = 1/1024
+        h = 1.0 / 1024            # (1025 x 2049 points, two stacked unit squares), k^3 h^2 = 0.5, ml = 5
+        k = (0.5 / h ** 2) ** (1.0 / 3.0)
+        hier = build_hierarchy(((0.0, 1.0), (0.0, 2.0)), h=h, ml=5, k=k, boundary="sommerfeld")
+        return hier, point_source_rhs(hier, (0.5, 1.0)).grid_view(hier)
     if config.startswith("c4_h"):  # BASELINE configs[3] model (gridfile raster): c4_h6_f40 (ml 3), c4_h12_f40 (ml 2)
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
         from paper_2412_04980_b200.models import C4_DOMAIN, C4_SOURCE, synthetic_layered_velocity

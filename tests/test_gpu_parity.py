@@ -635,6 +635,44 @@ def test_lowsync_hbm_streaming_step_matches_mgs_chain():
     assert np.linalg.norm(x0 - xo) <= 1e-9 * np.linalg.norm(xo)
 
 
+def test_streaming_lowsync_step_on_levels_beyond_the_one_launch_form():
+    """Levels whose w slice exceeds the one-launch low-synchronisation step (> 7168 points per
+    CTA: config 5's 2049^2 and config 4's 3065 x 1001 CSLP levels) can run the HBM-streaming form
+    of the same algorithm (hdb_option "lsh_prefer"), host-driven (mode -1) and inside the
+    device-driven GMRES loop (mode -2): same iteration counts and solutions as the MGS-order
+    kernels (mgs_ls = 0), on a
+    1537^2 radius-2 CSLP level with GMRES(0.1, 30) and GMRES(1e-6, 45)."""
+    import ctypes as C
+    import torch
+    from paper_2412_04980_b200 import _lib
+    L = _lib.lib()
+    prob = hdb.mp1_problem(k=150.0, n=3073, ml=3)
+    op = hdb.cslp_operator(prob.hierarchy, 2, 0.5)
+    assert op.npoints > 148 * 7168
+    rng = _rng(11)
+    b = torch.from_numpy(_rand(rng, op.shape)).cuda()
+    res = {}
+    for ls in (1, 0):
+        _lib.check(L.hdb_option(b"mgs_ls", ls))
+        _lib.check(L.hdb_option(b"lsh_prefer", ls))
+        for mode in (-1, -2):
+            for tol, cap in ((0.1, 30), (1e-6, 45)):
+                x = torch.empty_like(b)
+                its, rel = C.c_int(), C.c_double()
+                _lib.check(L.hdb_op_gmres(op.handle, b.data_ptr(), x.data_ptr(), tol, cap, mode, C.byref(its),
+                                          C.byref(rel)))
+                res[(ls, mode, tol)] = (its.value, rel.value, x.cpu().numpy())
+    _lib.check(L.hdb_option(b"mgs_ls", 1))
+    _lib.check(L.hdb_option(b"lsh_prefer", 0))
+    for tol in (0.1, 1e-6):
+        i0, r0, x0 = res[(0, -1, tol)]
+        for key in ((1, -1, tol), (1, -2, tol), (0, -2, tol)):
+            i1, r1, x1 = res[key]
+            assert i1 == i0, key
+            assert abs(r1 - r0) <= 1e-9 * max(r0, 1e-300) + 1e-13, key
+            assert np.linalg.norm(x1 - x0) <= 1e-10 * np.linalg.norm(x0), key
+
+
 ROOT_DIR = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 
 
@@ -655,6 +693,27 @@ def test_config2_analogue_vs_reference():
     xs = u.grid_view(prob.hierarchy)[::st, ::st]
     ref = g["solution_sub"]
     assert np.linalg.norm(xs - ref) <= max(10 * float(g["floor_sol_rel"]), 1e-8) * np.linalg.norm(ref)
+
+
+def test_config5_reduced_instance_vs_reference():
+    """BASELINE configs[4] (weak scaling) at reduced size: two stacked unit squares,
+    h = 1/1024 (1025 x 2049 points), k^3 h^2 = 0.5, 5 levels -- the reference's own run
+    (tests/golden/solve_c5s.npz with its noise floor): outer count +-1, history and
+    solution within the BASELINE bar or 10x the reference's floor."""
+    from paper_2412_04980_b200 import models
+    g = golden("solve_c5s.npz")
+    hbar, xbar = parity_bar(g)
+    prob = models.c5_problem(P=2, ml=5, cells=1024)
+    assert prob.hierarchy.level(1).shape == (2049, 1025)
+    with hdb.MadpSolver(prob.hierarchy, hdb.preset("MADP", prob.hierarchy)) as s:
+        u, rep = s.solve(prob.rhs)
+    assert rep.converged and abs(rep.outer_iterations - int(g["outer_iterations"])) <= 1
+    h, hr = np.array(rep.residual_history), g["residual_history"]
+    n = min(len(h), len(hr))
+    assert np.abs(h[:n] - hr[:n]).max() <= hbar
+    st = int(g["solution_stride"])
+    xs = u.grid_view(prob.hierarchy)[::st, ::st]
+    assert np.linalg.norm(xs - g["solution_sub"]) <= xbar * np.linalg.norm(g["solution_sub"])
 
 
 @pytest.mark.slow
