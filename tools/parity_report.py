@@ -34,12 +34,13 @@ def builders(hdb):
         "c3_40": ("solve_c3_40.npz", lambda: hdb.wedge_problem(f=40.0, nx=1201, ml=5, layers=W), 150),
         "c4_h6_f40": ("solve_c4_h6_f40.npz", lambda: hdb.synthetic_layered_problem(40.0, 6.0, 3), 150),
         "c4_h12_f40": ("solve_c4_h12_f40.npz", lambda: hdb.synthetic_layered_problem(40.0, 12.0, 2), 150),
+        "c5s": ("solve_c5s.npz", lambda: hdb.c5_problem(P=2, ml=5, cells=1024), 150),
     }
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--cases", default="c1s,wedge20,c1_full,c2a,c3_10,c3_20,c3_40,c4_h12_f40,c2")
+    ap.add_argument("--cases", default="c1s,wedge20,c1_full,c2a,c3_10,c3_20,c3_40,c4_h12_f40,c5s,c2")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "parity.json"))
     a = ap.parse_args()
     import paper_2412_04980_b200 as hdb
