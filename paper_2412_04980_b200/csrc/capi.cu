@@ -579,7 +579,7 @@ int hdb_solver_solve(hdb_solver* s, const void* b, void* x, int host_buffers) {
       HDB_CUDA(cudaMemcpyAsync(x, s->dx, sizeof(cd) * n, cudaMemcpyDeviceToHost, E.st));
       E.sync();
     } catch (...) {
-      E.sync();
+      cudaStreamSynchronize(E.st);  // (not E.sync(): a sticky error here must not mask the original one)
       throw;
     }
   });

@@ -20,11 +20,18 @@ struct Error : std::runtime_error {
   Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
 };
 
+inline std::string src_tail(const char* path) {  // file name of a source path (error locations)
+  const std::string p(path);
+  const size_t k = p.find_last_of('/');
+  return k == std::string::npos ? p : p.substr(k + 1);
+}
+
 #define HDB_CUDA(x)                                                                         \
   do {                                                                                      \
     cudaError_t e_ = (x);                                                                   \
     if (e_ != cudaSuccess)                                                                  \
-      throw ::hdb::Error(::hdb::E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+      throw ::hdb::Error(::hdb::E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) +  \
+                                            " [" + ::hdb::src_tail(__FILE__) + ":" + std::to_string(__LINE__) + "]"); \
   } while (0)
 
 using cplx = std::complex<double>;

@@ -6,6 +6,8 @@
 // ticket) sums them in a fixed order and writes the scalar to device memory.
 // Nothing returns to the host here; the Krylov driver reads the Hessenberg
 // column once per Arnoldi step.
+#include <cstdio>
+#include <cstdlib>
 #include <functional>
 
 #include "kernels.h"
@@ -368,6 +370,18 @@ int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, 
                    cd* hout, cudaStream_t st, const std::function<void(cd*, int)>& allreduce, const int* skip) {
   if (j > 511) return 1;
   const int G = reduce_blocks(n);
+  // HDB_DEBUG_SYNC=1: synchronise after every kernel of the step and name a faulting one
+  static const bool dbg = [] {
+    const char* e = getenv("HDB_DEBUG_SYNC");
+    return e && *e && *e != '0';
+  }();
+  auto chk = [&](const char* what, int q) {
+    if (!dbg) return;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess)
+      fprintf(stderr, "lsh fault after %s (group %d): j=%d n=%lld G=%d w=%p part=%p Tg=%p hout=%p: %s\n", what, q, j, n, G,
+              (void*)w, (void*)part, (void*)Tg, (void*)hout, cudaGetErrorString(e));
+  };
   cd* sums = part;
   cd* npart = part + kLshSums;
   cd* apart = npart + G;
@@ -377,16 +391,22 @@ int launch_mgs_lsh(cd* w, const cd* const* Vtab, const cd* const* Vhost, int j, 
     const int k0 = q * kLsG, kn = j - k0 < kLsG ? j - k0 : kLsG;
     k_lsh_a<<<G, kReduceThreads, 0, st>>>(w, Vhost[j], Vtab, k0, kn > 0 ? kn : 0, q == 0, n,
                                           apart + (long long)q * G * kLsPE, skip);
+    chk("k_lsh_a", q);
   }
   k_lsh_sum<<<1, kLshF, 0, st>>>(apart, G, j, sums, skip);
+  chk("k_lsh_sum", 0);
   if (allreduce) allreduce(sums, 2 * j + 1);
+  chk("allreduce(sums)", 0);
   k_lsh_th<<<1, kLshF, 0, st>>>(sums, j, Tg, hout, skip);
+  chk("k_lsh_th", 0);
   const int gb = (j + 1 + kLsG - 1) / kLsG;
   for (int q = 0; q < gb; ++q) {
     const int kfirst = j - q * kLsG, kn = kfirst + 1 < kLsG ? kfirst + 1 : kLsG;
     k_lsh_b<<<G, kReduceThreads, 0, st>>>(w, Vtab, hout, kfirst, kn, q == gb - 1, n, npart, skip);
+    chk("k_lsh_b", q);
   }
   k_lsh_norm<<<1, kReduceThreads, 0, st>>>(npart, G, hout + j + 1, skip);
+  chk("k_lsh_norm", 0);
   if (allreduce) allreduce(hout + j + 1, 1);
   return 0;
 }
