@@ -428,13 +428,15 @@ static long long lsh_min() {
 }
 
 // sharded levels with at least this many local points take the HBM-streaming low-sync
-// step (HDB_LSH_SHARD_N; default off: with it on small sharded levels, the one-GPU thread-
-// rank emulation hit an intermittent illegal address (1 run in 3 of tools/
-// slab_sensitivity.py; never with CUDA_LAUNCH_BLOCKING=1 or with >= 10000 local points,
-// profiles/r02q_slab_lsh.log) that is not resolved -- sharded levels keep the fused chain)
+// step: two all-reduces per Arnoldi step (the 2j + 1 coefficient sums and ||w||^2) instead of
+// one per MGS coefficient (HDB_LSH_SHARD_N; default 0 = every sharded level, -1 = off).
+// (Round 2 kept it off for an intermittent illegal address in the one-GPU thread-rank
+// emulation; the cause was not this step but the radius-2/3 tile loaders, which sampled
+// rows beyond a slab's halo when the slab height is not a multiple of the tile height --
+// fixed in stencil.cuh tile_row_needed, 14 / 14 stress runs clean, profiles/r03r_*.)
 static long long lsh_shard_min() {
   static long long v = -2;
-  if (v == -2) v = env_ll("HDB_LSH_SHARD_N", -1);
+  if (v == -2) v = env_ll("HDB_LSH_SHARD_N", 0);
   return v < 0 ? (1LL << 62) : v;
 }
 

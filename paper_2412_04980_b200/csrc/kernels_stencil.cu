@@ -368,8 +368,9 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
   for (int t = tid; t < H * W; t += TX * TY) {
     const int ty = t / W, tx = t % W;
     const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
-    su[ty][tx] = upad(u, k, g, c, gj, gi);
-    sk[ty][tx] = kpad(k, g, c, gj, gi);
+    const bool need = tile_row_needed(g, gj, R);
+    su[ty][tx] = need ? upad(u, k, g, c, gj, gi) : mkc(0.0, 0.0);
+    sk[ty][tx] = need ? kpad(k, g, c, gj, gi) : 0.0;
   }
   __syncthreads();
   const int i = i0 + threadIdx.x, j = j0 + threadIdx.y;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(TX * TY) k_rg(const cd* __restrict__ u, const 
   // constant-k^2 level and a tile away from every boundary: every tap's k^2 is ku,
   // so the per-tap coefficient is the precomputed (identically rounded) ucoef
   const bool fast = c.uniform && i0 >= R && i0 + TX + R <= g.nx && g.row0 + j0 >= R &&
-                    g.row0 + j0 + TY + R <= g.nyg;
+                    g.row0 + j0 + TY + R <= g.nyg && j0 + TY <= g.ny;  // (whole tile inside the slab)
   if (fast) {
 #pragma unroll
     for (int a = 0; a < N; ++a) {
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(TX * VTY) k_rgv(const cd* __restrict__ u, cons
   __shared__ double sk[H][W];
   const int i0 = blockIdx.x * TX, j0 = blockIdx.y * VROWS;
   const bool fast = c.uniform && i0 >= R && i0 + TX + R <= g.nx && g.row0 + j0 >= R &&
-                    g.row0 + j0 + VROWS + R <= g.nyg;
+                    g.row0 + j0 + VROWS + R <= g.nyg && j0 + VROWS <= g.ny;  // (whole tile inside the slab)
   const int tid = threadIdx.y * TX + threadIdx.x;
   for (int t = tid; t < H * W; t += TX * VTY) {
     const int ty = t / W, tx = t % W;
@@ -435,8 +436,9 @@ __global__ void __launch_bounds__(TX * VTY) k_rgv(const cd* __restrict__ u, cons
     if (fast) {
       su[ty][tx] = U(u, g, gj, gi);
     } else {
-      su[ty][tx] = upad(u, k, g, c, gj, gi);
-      sk[ty][tx] = kpad(k, g, c, gj, gi);
+      const bool need = tile_row_needed(g, gj, R);
+      su[ty][tx] = need ? upad(u, k, g, c, gj, gi) : mkc(0.0, 0.0);
+      sk[ty][tx] = need ? kpad(k, g, c, gj, gi) : 0.0;
     }
   }
   __syncthreads();
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(32 * HTY) k_rgh(const cd* __restrict__ u, cons
   double* sk = reinterpret_cast<double*>(su + H * P);
   const int i0 = blockIdx.x * HTX, j0 = blockIdx.y * HTY;
   const bool fast = c.uniform && i0 >= R && i0 + HTX + R <= g.nx && g.row0 + j0 >= R &&
-                    g.row0 + j0 + HTY + R <= g.nyg;
+                    g.row0 + j0 + HTY + R <= g.nyg && j0 + HTY <= g.ny;  // (whole tile inside the slab)
   const int tid = threadIdx.y * 32 + threadIdx.x;
   for (int t = tid; t < H * W; t += 32 * HTY) {
     const int ty = t / W, tx = t % W;
@@ -535,8 +537,9 @@ __global__ void __launch_bounds__(32 * HTY) k_rgh(const cd* __restrict__ u, cons
     if (fast) {
       su[si] = U(u, g, gj, gi);
     } else {
-      su[si] = upad(u, k, g, c, gj, gi);
-      sk[si] = kpad(k, g, c, gj, gi);
+      const bool need = tile_row_needed(g, gj, R);
+      su[si] = need ? upad(u, k, g, c, gj, gi) : mkc(0.0, 0.0);
+      sk[si] = need ? kpad(k, g, c, gj, gi) : 0.0;
     }
   }
   __syncthreads();
@@ -640,7 +643,7 @@ __global__ void __launch_bounds__(256, 2) k_rgs(const cd* __restrict__ u, const 
   cd* hk = ha + TR * GS_T;                                        // (M (k u)) rows
   const int i0 = blockIdx.x * GS_T, j0 = blockIdx.y * GS_T;
   const bool fast = c.uniform && i0 >= R && i0 + GS_T + R <= g.nx && g.row0 + j0 >= R &&
-                    g.row0 + j0 + GS_T + R <= g.nyg;
+                    g.row0 + j0 + GS_T + R <= g.nyg && j0 + GS_T <= g.ny;  // (whole tile inside the slab)
   const int tid = threadIdx.x;
   constexpr int NL = (TR * TC + 255) / 256;
   if (fast) {  // interior tile: every sample in range, all NL loads in flight before the stores
@@ -662,8 +665,9 @@ __global__ void __launch_bounds__(256, 2) k_rgs(const cd* __restrict__ u, const 
       const int ty = t / TC, tx = t - ty * TC;
       const int gi = i0 + tx - R, gj = g.row0 + j0 + ty - R;
       const int si = ty * PC + gskew(tx);
-      su[si] = upad(u, k, g, c, gj, gi);
-      sk[si] = kpad(k, g, c, gj, gi);
+      const bool need = tile_row_needed(g, gj, R);
+      su[si] = need ? upad(u, k, g, c, gj, gi) : mkc(0.0, 0.0);
+      sk[si] = need ? kpad(k, g, c, gj, gi) : 0.0;
     }
   }
   __syncthreads();

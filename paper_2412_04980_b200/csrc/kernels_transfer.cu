@@ -76,6 +76,7 @@ __global__ void __launch_bounds__(256) k_restrict2(const cd* __restrict__ f, cd*
   for (int r = 0; r < 7; ++r) {
     const int y = 2 * cyg - 2 + r;
     if (y < 0 || y >= t.nfy_g) continue;
+    if (r >= 5 && cy + 1 >= t.c_ny) continue;  // rows only the absent second coarse row needs (beyond a slab's halo)
     cd v[5];
 #pragma unroll
     for (int a = 0; a < 5; ++a) {

@@ -46,6 +46,12 @@ __device__ __forceinline__ cd upad(const cd* u, const double* k, const Geom& g, 
   return mkc(0.0, 0.0);
 }
 
+// Tile loaders of the radius-2/3 kernels: a block whose outputs run past the slab's last row
+// would sample rows beyond the slab's halo (local row >= ny + R).  No valid output needs
+// them and on a row slab they are not addressable (only H >= R halo rows exist around a
+// vector; on the whole grid they are ghost rows anyway): such samples are not loaded.
+__device__ __forceinline__ bool tile_row_needed(const Geom& g, int gj, int R) { return gj - g.row0 < g.ny + R; }
+
 // padded k^2 (operators.py:78-93)
 __device__ __forceinline__ double kpad(const double* k, const Geom& g, const OpCoef& c, int gj, int i) {
   const bool xin = (i >= 0) & (i < g.nx);
