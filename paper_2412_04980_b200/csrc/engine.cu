@@ -762,11 +762,22 @@ static void ensure_vtab(KWS& ws, int upto) {
 bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int* its_dev, double* rel_dev) {
   const long long n = op->n;
   const int cap = stop.max_iters;
-  const bool lsh = mgs_prefers_lsh(n, cap);  // streaming low-synchronisation step instead of the one-launch kernels
-  if (!gmres_device_enabled() || pinv_mode() || op->sharded || n < coop_mgs_min() || cap < 1 || cap + kSlotH + 2 >= 900 ||
-      !(stop.rel_tol < 1.0) || !(lsh || mgs_grid_fits(n)))
+  // Sharded levels qualify through the streaming low-synchronisation step: its two reductions are
+  // all-reduced in-stream (NCCL), the halo exchange precedes every stencil, the Givens / stopping
+  // kernels run redundantly on every rank (identical all-reduced inputs -> identical flags), so a
+  // sharded CSLP-GMRES also runs without a host round trip per Arnoldi step (HDB_GMRES_DEV_SHARD=0:
+  // host-driven loop).  A finished solve skips its kernels; the collectives of the surplus steps
+  // of a batch still run on every rank (same sequence everywhere).
+  const bool shard = op->sharded;
+  static const bool shard_ok = env_ll("HDB_GMRES_DEV_SHARD", 1) != 0;
+  const bool lsh = shard ? (shard_ok && mgs_ls_on() && n >= lsh_shard_min() && cap <= 511)
+                         : mgs_prefers_lsh(n, cap);  // streaming step instead of the one-launch kernels
+  if (!gmres_device_enabled() || pinv_mode() || (shard && !lsh) || (!shard && n < coop_mgs_min()) || cap < 1 ||
+      cap + kSlotH + 2 >= 900 || !(stop.rel_tol < 1.0) || !(lsh || mgs_grid_fits(n)))
     return false;
   Engine& E = engine();
+  std::function<void(cd*, int)> allred;
+  if (shard) allred = [&E](cd* v, int m) { E.comm->allreduce((double*)v, 2 * m, E.st); };
   ws.ensure(n, cap, false);
   if (lsh && ws.tgh_cap < cap) {
     E.free(ws.tgh);
@@ -790,6 +801,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
   cd* flag = E.dscal + kSlotFlag;
   ensure_vtab(ws, 0);
   E.kl(KF_BLAS, 16.0 * n, [&] { launch_dot(b, b, n, E.red, hcol, E.st); });
+  op->reduce(hcol);
   E.kl(KF_CONTROL, 0.0, [&] { launch_gm_init(hcol, st, lay, flag, E.st); });
   E.kl(KF_BLAS, 32.0 * n, [&] { launch_gm_scale(b, ws.v(0), st, n, E.st); });  // krylov.py:92-115 with x0 = 0
   OpCoef cs = op->c;
@@ -803,6 +815,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
     ensure_vtab(ws, jend);
     for (; j < jend; ++j) {
       // bytes are booked after the loop for the steps that ran (later ones return at once)
+      op->exchange(ws.v(j), op->c.radius);
       E.kl(op->c.radius == 1 ? KF_APPLY5 : KF_GALERKIN, 0.0,
            [&] { launch_apply(cs, op->g, ws.v(j), nullptr, op->ksq, ws.v(j + 1), 0, E.st); });  // krylov.py:119
       int rc = 0;
@@ -810,7 +823,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
         const int nl = (j == 0 ? 1 : (j + 7) / 8) + (j + 8) / 8 + 3;
         E.kl(KF_MGS_CHAIN, 0.0, [&] {
           rc = launch_mgs_lsh(ws.v(j + 1), (const cd* const*)ws.dV, ws.V.data(), j, n, ws.lpart, ws.tgh, hcol, E.st,
-                              std::function<void(cd*, int)>(), skip);
+                              allred, skip);
           launch_scale_dev(ws.v(j + 1), ws.v(j + 1), hcol + j + 1, n, E.st, skip);  // V_{j+1} = w / ||w||
         }, nl);
       } else {
@@ -843,6 +856,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
          [&] { launch_lincomb((const cd* const*)ws.dV, gm_y(st, lay), its, nullptr, x, n, E.st); });  // 169-172
     op->apply(x, ws.tmp);                                                                           // 174
     E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, hcol, E.st); });
+    op->reduce(hcol);
   }
   E.kl(KF_CONTROL, 0.0, [&] { launch_gm_final(hcol, st, lay, its_dev, rel_dev, flag, E.st); });
   ws.last_its = its;
