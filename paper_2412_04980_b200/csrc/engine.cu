@@ -819,6 +819,7 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
       E.kl(op->c.radius == 1 ? KF_APPLY5 : KF_GALERKIN, 0.0,
            [&] { launch_apply(cs, op->g, ws.v(j), nullptr, op->ksq, ws.v(j + 1), 0, E.st); });  // krylov.py:119
       int rc = 0;
+      bool givens_fused = false;
       if (lsh) {
         const int nl = (j == 0 ? 1 : (j + 7) / 8) + (j + 8) / 8 + 3;
         E.kl(KF_MGS_CHAIN, 0.0, [&] {
@@ -827,15 +828,22 @@ bool gmres_device(const LevelOp* op, const cd* b, cd* x, Stop stop, KWS& ws, int
           launch_scale_dev(ws.v(j + 1), ws.v(j + 1), hcol + j + 1, n, E.st, skip);  // V_{j+1} = w / ||w||
         }, nl);
       } else {
+        // low-synchronisation one-launch step: the Givens / stopping update rides in its tail
+        // (HDB_LS_GIVENS=0: separate one-warp kernel)
+        static const bool fuse_on = env_ll("HDB_LS_GIVENS", 1) != 0;
+        givens_fused = fuse_on && mgs_ls_fits(n, j);
+        GmFuseArgs fa{st, lay, cap, stop.rel_tol, flag};
         E.kl(KF_MGS_COOP, 0.0, [&] {
-          rc = launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip, ws.tg);
+          rc = launch_mgs_grid(ws.v(j + 1), (const cd* const*)ws.dV, j, n, ws.gpart, hcol, E.st, skip, ws.tg,
+                               givens_fused ? &fa : nullptr);
         });
       }
       if (rc != 0) {
         const cudaError_t err = cudaGetLastError();
         throw Error(E_CUDA, std::string("cooperative MGS launch: ") + cudaGetErrorString(err));
       }
-      E.kl(KF_CONTROL, 0.0, [&] { launch_gm_givens(j, hcol, st, lay, cap, stop.rel_tol, flag, E.st); });
+      if (!givens_fused)
+        E.kl(KF_CONTROL, 0.0, [&] { launch_gm_givens(j, hcol, st, lay, cap, stop.rel_tol, flag, E.st); });
     }
     HDB_CUDA(cudaMemcpyAsync(ws.hflags, skip, 2 * sizeof(int), cudaMemcpyDeviceToHost, E.st));
     HDB_CUDA(cudaStreamSynchronize(E.st));

@@ -91,8 +91,16 @@ void resident_set_profile(long long* dev_counters);
 // tg != null: the low-synchronisation form (two grid reductions per step) where the
 // level fits it; tg holds the T = (I + L)^{-1} rows of the Arnoldi process so far
 // (mgs_ls_tg_elems() elements; every step j of the process must go through it)
+// fuse != null (device-driven GMRES, low-synchronisation form only: mgs_ls_fits(n, j)): the
+// step also runs the Givens / stopping update of k_gm_givens on the solve's device state
+struct GmFuseArgs {
+  cd* st;        // gm_state_elems(cap) state of the solve
+  int cap, maxit;
+  double tol;
+  cd* flag;
+};
 int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
-                    const int* skip = nullptr, cd* tg = nullptr);
+                    const int* skip = nullptr, cd* tg = nullptr, const GmFuseArgs* fuse = nullptr);
 bool mgs_ls_fits(long long n, int j);
 // the same low-synchronisation step as streaming passes over HBM (w too large for
 // the one-launch form): Vtab device pointer table, Vhost the same pointers on the

@@ -1571,6 +1571,17 @@ struct LsSmem {
   cd stage[kRT / 32][kLsStage];            // warp partials; reused for g, l, t-row and h
   uint64_t full[kLsRing], empty[kLsRing];
   const cd* vptr[kLsMaxJ + 1];             // basis pointers (the producer's chunk sources)
+  cd gcol[kLsMaxJ + 3];                    // fused Givens step (device-driven GMRES): Hessenberg column,
+  cd gsn[kLsMaxJ + 1];                     // earlier rotations
+  double gcs[kLsMaxJ + 1];
+};
+// Device-driven GMRES state of the solve this step belongs to (gm_state_elems layout); st ==
+// nullptr: no fused Givens (the launch-driven FGMRES reads the column on the host).
+struct GmFuse {
+  cd* st;
+  int cap, maxit;
+  double tol;
+  cd* flag;
 };
 constexpr size_t kLsHead = ((sizeof(LsSmem) + 127) / 128) * 128;
 
@@ -1579,7 +1590,7 @@ __device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
 }
 
 __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, int j, long long n, cd* gpart,
-                                                   cd* hout, cd* Tg, const int* skip) {
+                                                   cd* hout, cd* Tg, const int* skip, GmFuse gf) {
   if (skip && *skip) return;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LsSmem& s = *reinterpret_cast<LsSmem*>(smem_raw);
@@ -1822,6 +1833,67 @@ __global__ void __launch_bounds__(kRT, 1) k_mgs_ls(cd* w, const cd* const* V, in
   if (rank == 0 && t == 0) hout[j + 1] = nn;
   const double hn = sqrt(nn.x > 0.0 ? nn.x : 0.0);
   const double inv = 1.0 / hn;
+  // Fused Givens / stopping step of the device-driven GMRES (k_gm_givens's operations in the
+  // same order: bit-identical), on warp 0 of CTA 0 while every other warp writes V_{j+1}.
+  if (gf.st && rank == 0 && wid == 0) {
+    cd* g_ = gf.st + 2;
+    cd* sn_ = g_ + gf.cap + 1;
+    cd* cs_ = sn_ + gf.cap;
+    cd* R_ = cs_ + gf.cap;
+    int* fl = reinterpret_cast<int*>(gf.st + 1);
+    for (int i = lane; i < j; i += 32) {
+      s.gsn[i] = sn_[i];
+      s.gcs[i] = cs_[i].x;
+    }
+    for (int i = lane; i <= j; i += 32) s.gcol[i] = hs[i];
+    __syncwarp();
+    if (lane == 0) {
+      cd* col = s.gcol;
+      const double bnorm = gf.st[0].x;
+      const double hg = sqrt(fmax(nn.x, 0.0));
+      bool finite = isfinite(hg);
+      for (int i = 0; i <= j; ++i) finite &= isfinite(col[i].x) && isfinite(col[i].y);
+      for (int i = 0; i < j; ++i) {  // rotation i touches entries i, i+1 <= j
+        const cd ci = col[i], cn = col[i + 1];
+        const double c = s.gcs[i];
+        const cd sc = cmul_(s.gsn[i], cn);
+        const cd nb = cmul_(mkc(-s.gsn[i].x, s.gsn[i].y), ci);
+        col[i] = mkc(c * ci.x + sc.x, c * ci.y + sc.y);
+        col[i + 1] = mkc(nb.x + c * cn.x, nb.y + c * cn.y);
+      }
+      const cd h1 = col[j], h2 = mkc(hg, 0.0);
+      double c;
+      cd sn;
+      const double a1 = cabs_(h1), a2 = cabs_(h2);
+      if (a2 == 0.0) { c = 1.0; sn = mkc(0.0, 0.0); }
+      else if (a1 == 0.0) { c = 0.0; sn = mkc(1.0, 0.0); }
+      else {
+        const double tt = hypot(a1, a2);
+        c = a1 / tt;
+        const cd q = cmul_(mkc(h1.x / a1, h1.y / a1), mkc(h2.x, -h2.y));
+        sn = mkc(q.x / tt, q.y / tt);
+      }
+      cs_[j] = mkc(c, 0.0);
+      sn_[j] = sn;
+      const cd sh = cmul_(sn, h2);
+      col[j] = mkc(c * h1.x + sh.x, c * h1.y + sh.y);
+      const cd gj = g_[j];
+      g_[j + 1] = cmul_(mkc(-sn.x, sn.y), gj);
+      g_[j] = mkc(c * gj.x, c * gj.y);
+      const double rel = cabs_(g_[j + 1]) / bnorm;
+      fl[1] = j + 1;
+      if (!finite) {
+        gf.flag->x = 2.0;
+        fl[2] = 2;
+        fl[0] = 1;
+      } else if (hg < 1e-30 || rel <= gf.tol || j + 1 >= gf.maxit) {
+        fl[0] = 1;
+      }
+    }
+    __syncwarp();
+    cd* Rc = R_ + (long long)j * (j + 1) / 2;  // column j: R[0..j]
+    for (int i = lane; i <= j; i += 32) Rc[i] = s.gcol[i];
+  }
 #pragma unroll
   for (int m = 0; m < kLsSlot; ++m) {
     const int q = t + m * kRT;
@@ -1892,11 +1964,13 @@ bool mgs_ls_fits(long long n, int j) {
 
 // returns 0 when launched, 1 when the level does not fit (caller: launch chain)
 int launch_mgs_grid(cd* w, const cd* const* Vtab, int j, long long n, cd* gpart, cd* hout, cudaStream_t st,
-                    const int* skip, cd* tg) {
+                    const int* skip, cd* tg, const GmFuseArgs* fuse) {
   if (tg && mgs_ls_fits(n, j)) {
     const size_t sm = mgs_ls_smem((n + g_grid - 1) / g_grid);
     if (!ensure_smem_attr((const void*)k_mgs_ls, sm)) return 1;
-    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip};
+    GmFuse gf{nullptr, 0, 0, 0.0, nullptr};
+    if (fuse) gf = GmFuse{fuse->st, fuse->cap, fuse->maxit, fuse->tol, fuse->flag};
+    void* args[] = {&w, (void*)&Vtab, &j, &n, &gpart, &hout, &tg, (void*)&skip, &gf};
     return cudaLaunchCooperativeKernel((void*)k_mgs_ls, dim3(g_grid), dim3(kRT), args, sm, st) == cudaSuccess ? 0 : 1;
   }
   long long ks = 0;
