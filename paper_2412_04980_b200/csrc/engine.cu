@@ -359,6 +359,7 @@ void KWS::ensure(long long n_, int cap_, bool flexible) {
   if (cap_ + 1 > cap) {
     if (dbasis) { E.free(dbasis); E.free(dy); cudaFreeHost(hbasis); cudaFreeHost(hy); }
     cap = cap_ + 1;
+    dbasis0 = nullptr;
     dbasis = (cd**)E.alloc_bytes(sizeof(cd*) * cap);
     dy = (cd*)E.alloc_bytes(sizeof(cd) * cap);
     HDB_CUDA(cudaMallocHost(&hbasis, sizeof(cd*) * cap));
@@ -716,6 +717,7 @@ KReport fgmres(long long n, const LinOp& A, const LinOp* M, const cd* b, cd* x, 
     ws.hbasis[i] = M ? ws.z(i) : ws.v(i);
     ws.hy[i] = mkc(y[i].real(), y[i].imag());
   }
+  ws.dbasis0 = nullptr;  // (the one-step path's cached table entry is overwritten)
   HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*) * m, cudaMemcpyHostToDevice, E.st));
   HDB_CUDA(cudaMemcpyAsync(ws.dy, ws.hy, sizeof(cd) * m, cudaMemcpyHostToDevice, E.st));
   E.kl(KF_BLAS, 16.0 * (m + 1 + (x0 ? 1 : 0)) * n, [&] { launch_lincomb(ws.dbasis, ws.dy, m, x0, x, n, E.st); });
@@ -889,15 +891,33 @@ void fgmres_step1(long long n, const LinOp& A, const LinOp& M, const cd* b, cd* 
   cd* w = ws.v(1);
   A(ws.z(0), w);
   red_mgs(dist, w, nullptr, nullptr, ws.v(0), n, S + kS1H0, 32.0 * n);
-  red_mgs(dist, w, ws.v(0), S + kS1H0, nullptr, n, S + kS1HN, 16.0 * n);
-  E.kl(KF_CONTROL, 0.0, [&] { launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st); });
-  ws.hbasis[0] = ws.z(0);
-  HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*), cudaMemcpyHostToDevice, E.st));
+  // where the reductions finish on this rank (no all-reduce, no row-ordered mode) the scalar
+  // update and the finiteness guard ride in the launch that produces their input: the block
+  // that finishes the reduction runs them (same operations; HDB_STEP1_FUSE=0: separate kernels)
+  static const bool fuse_on = env_ll("HDB_STEP1_FUSE", 1) != 0;
+  const bool local = fuse_on && !(dist && dist->sharded) && !(dist && pinv_mode());
+  if (local) {
+    const Step1Epi epi{S + kS1B, S + kS1H0, S + kS1Y, its_dev, S + kSlotFlag};
+    E.kl(KF_MGS_CHAIN, 16.0 * n,
+         [&] { launch_mgs(w, ws.v(0), S + kS1H0, nullptr, n, E.red, S + kS1HN, E.st, &epi); });
+  } else {
+    red_mgs(dist, w, ws.v(0), S + kS1H0, nullptr, n, S + kS1HN, 16.0 * n);
+    E.kl(KF_CONTROL, 0.0, [&] { launch_step1(S + kS1B, S + kS1H0, S + kS1HN, S + kS1Y, its_dev, S + kSlotFlag, E.st); });
+  }
+  if (ws.dbasis0 != ws.z(0)) {  // the one-entry pointer table of x = y0 Z0 is constant across calls
+    ws.hbasis[0] = ws.z(0);
+    HDB_CUDA(cudaMemcpyAsync(ws.dbasis, ws.hbasis, sizeof(cd*), cudaMemcpyHostToDevice, E.st));
+    ws.dbasis0 = ws.z(0);
+  }
   E.kl(KF_BLAS, 32.0 * n, [&] { launch_lincomb(ws.dbasis, S + kS1Y, 1, nullptr, x, n, E.st); });  // x = y0 Z0
   // explicit true residual: only its finiteness matters to the caller (krylov.py:174-176)
   A(x, ws.tmp);
-  red_subnorm(dist, b, ws.tmp, n, S + kS1F);
-  E.kl(KF_CONTROL, 0.0, [&] { launch_finite_guard(S + kS1F, S + kSlotFlag, E.st); });
+  if (local) {
+    E.kl(KF_BLAS, 32.0 * n, [&] { launch_subnorm(b, ws.tmp, n, E.red, S + kS1F, E.st, S + kSlotFlag); });
+  } else {
+    red_subnorm(dist, b, ws.tmp, n, S + kS1F);
+    E.kl(KF_CONTROL, 0.0, [&] { launch_finite_guard(S + kS1F, S + kSlotFlag, E.st); });
+  }
 }
 
 // --------------------------------------------------------------- Bi-CGSTAB

@@ -219,6 +219,7 @@ struct KWS {
   int tgh_cap = 0;
   cd* tmp = nullptr;
   cd** dbasis = nullptr;   // device pointer table for the solution update
+  cd* dbasis0 = nullptr;   // the vector dbasis[0] currently points to on the device (one-step path cache)
   cd* dy = nullptr;
   cd** hbasis = nullptr;   // pinned staging
   cd* hy = nullptr;

@@ -63,8 +63,19 @@ void launch_rowmgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, int nx, in
 void launch_rowsubnorm(const cd* b, const cd* t, int nx, int ny, cd* rowpart, cudaStream_t st);
 void launch_rowsum(const cd* rows, int nyg, cd* dst, cudaStream_t st);
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st);
-void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st);
-void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st);
+// epilogue of a fused MGS launch: the one-iteration FGMRES scalar update (launch_step1) run by the
+// block that finishes the reduction, on (b2, h0, the launch's own result)
+struct Step1Epi {
+  const cd* b2;
+  const cd* h0;
+  cd* y;
+  int* its;
+  cd* flag;
+};
+void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st,
+                const Step1Epi* epi = nullptr);
+// guard != null: a non-finite ||b - t||^2 raises the flag (launch_finite_guard folded in)
+void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st, cd* guard = nullptr);
 void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st);
 void launch_lincomb(const cd* const* basis, const cd* y, int m, const cd* x0, cd* x, long long n, cudaStream_t st);
 void launch_add(const cd* a, const cd* b, cd* out, long long n, int sub, cudaStream_t st);

@@ -33,12 +33,43 @@ __global__ void __launch_bounds__(kReduceThreads) k_dot(const cd* __restrict__ u
   grid_finish(acc, partials, ticket, dst);
 }
 
+// the one-iteration FGMRES scalar update (krylov.py:126-168 for m = 1): Givens, y_0, count
+__device__ __forceinline__ void step1_update(const cd* b2, const cd* h0p, const cd* hn2, cd* y_out, int* its_out, cd* flag) {
+  const double beta = sqrt(fmax(b2->x, 0.0));
+  if (beta == 0.0) {
+    *y_out = mkc(0.0, 0.0);
+    *its_out = 0;
+    return;
+  }
+  const cd h1 = *h0p;
+  const double hn = sqrt(fmax(hn2->x, 0.0));
+  const bool finite = isfinite(h1.x) && isfinite(h1.y) && isfinite(hn) && isfinite(beta);
+  const double a1 = hypot(h1.x, h1.y), a2 = hn;
+  double c, sr, si;  // s = (sr, si)
+  if (a2 == 0.0) { c = 1.0; sr = 0.0; si = 0.0; }
+  else if (a1 == 0.0) { c = 0.0; sr = 1.0; si = 0.0; }
+  else {
+    const double t = hypot(a1, a2);
+    c = a1 / t;
+    sr = (h1.x / a1) * hn / t;  // (h1/|h1|) conj(hn) / t with hn real
+    si = (h1.y / a1) * hn / t;
+  }
+  const double rr = c * h1.x + sr * hn, ri = c * h1.y + si * hn;  // R00 = c h1 + s h2
+  const double g = c * beta;
+  const double d = rr * rr + ri * ri;
+  *y_out = mkc(g * rr / d, -g * ri / d);
+  *its_out = 1;
+  if (!finite || !(d > 0.0)) flag->x = 2.0;
+}
+
 // Fused MGS step (krylov.py:121-124):  w -= h * vi  (h = *hsrc, numpy complex
 // scalar*array then subtract);  then dst = <vn, w_new> (vn = w for the norm).
 // vi == nullptr skips the update (first dot of the chain).
+// epi.b2 != null: the block that finishes the reduction also runs the one-iteration FGMRES
+// update on (b2, h0, *dst) -- the step1 control kernel folded into the norm launch
 __global__ void __launch_bounds__(kReduceThreads) k_mgs(cd* __restrict__ w, const cd* __restrict__ vi,
                                                         const cd* hsrc, const cd* __restrict__ vn, long long n,
-                                                        cd* partials, unsigned* ticket, cd* dst) {
+                                                        cd* partials, unsigned* ticket, cd* dst, Step1Epi epi) {
   const cd h = vi ? *hsrc : mkc(0.0, 0.0);
   cd acc = mkc(0.0, 0.0);
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
@@ -51,19 +82,22 @@ __global__ void __launch_bounds__(kReduceThreads) k_mgs(cd* __restrict__ w, cons
     acc = c_conjmul_acc(acc, a, x);
   }
   acc = block_sum(acc);
-  grid_finish(acc, partials, ticket, dst);
+  if (grid_finish(acc, partials, ticket, dst) && epi.b2 && threadIdx.x == 0)
+    step1_update(epi.b2, epi.h0, dst, epi.y, epi.its, epi.flag);
 }
 
 // dst = ||b - t||^2 (real part) without storing the difference (krylov.py:174)
+// guard != null: a non-finite result raises the NumericalError flag (k_finite_guard folded in)
 __global__ void __launch_bounds__(kReduceThreads) k_subnorm(const cd* __restrict__ b, const cd* __restrict__ t,
-                                                            long long n, cd* partials, unsigned* ticket, cd* dst) {
+                                                            long long n, cd* partials, unsigned* ticket, cd* dst,
+                                                            cd* guard) {
   cd acc = mkc(0.0, 0.0);
   for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < n; p += (long long)gridDim.x * blockDim.x) {
     const cd d = c_sub(b[p], t[p]);
     acc = c_conjmul_acc(acc, d, d);
   }
   acc = block_sum(acc);
-  grid_finish(acc, partials, ticket, dst);
+  if (grid_finish(acc, partials, ticket, dst) && guard && threadIdx.x == 0 && !isfinite(dst->x)) guard->x = 2.0;
 }
 
 // out = x * inv   (numpy  x / beta  ==  (x.re * (1/beta), x.im * (1/beta)))
@@ -139,31 +173,7 @@ __global__ void k_scale_dev(const cd* __restrict__ x, cd* __restrict__ out, cons
 // recurrence residual and y0 = c*beta / (c h0 + s hn).  Writes y0, the
 // iteration count (0 when b = 0) and raises the non-finite flag (2.0).
 __global__ void k_step1(const cd* b2, const cd* h0p, const cd* hn2, cd* y_out, int* its_out, cd* flag) {
-  const double beta = sqrt(fmax(b2->x, 0.0));
-  if (beta == 0.0) {
-    *y_out = mkc(0.0, 0.0);
-    *its_out = 0;
-    return;
-  }
-  const cd h1 = *h0p;
-  const double hn = sqrt(fmax(hn2->x, 0.0));
-  const bool finite = isfinite(h1.x) && isfinite(h1.y) && isfinite(hn) && isfinite(beta);
-  const double a1 = hypot(h1.x, h1.y), a2 = hn;
-  double c, sr, si;  // s = (sr, si)
-  if (a2 == 0.0) { c = 1.0; sr = 0.0; si = 0.0; }
-  else if (a1 == 0.0) { c = 0.0; sr = 1.0; si = 0.0; }
-  else {
-    const double t = hypot(a1, a2);
-    c = a1 / t;
-    sr = (h1.x / a1) * hn / t;  // (h1/|h1|) conj(hn) / t with hn real
-    si = (h1.y / a1) * hn / t;
-  }
-  const double rr = c * h1.x + sr * hn, ri = c * h1.y + si * hn;  // R00 = c h1 + s h2
-  const double g = c * beta;
-  const double d = rr * rr + ri * ri;
-  *y_out = mkc(g * rr / d, -g * ri / d);
-  *its_out = 1;
-  if (!finite || !(d > 0.0)) flag->x = 2.0;
+  step1_update(b2, h0p, hn2, y_out, its_out, flag);
 }
 
 // non-finite guard on a device scalar (explicit final residual, krylov.py:174-176)
@@ -476,11 +486,13 @@ void launch_rowsum(const cd* rows, int nyg, cd* dst, cudaStream_t st) {
 void launch_dot(const cd* u, const cd* v, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
   k_dot<<<reduce_blocks(n), kReduceThreads, 0, st>>>(u, v, n, ws.partials, ws.ticket, dst);
 }
-void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
-  k_mgs<<<reduce_blocks(n), kReduceThreads, 0, st>>>(w, vi, hsrc, vn, n, ws.partials, ws.ticket, dst);
+void launch_mgs(cd* w, const cd* vi, const cd* hsrc, const cd* vn, long long n, RedWS& ws, cd* dst, cudaStream_t st,
+                const Step1Epi* epi) {
+  const Step1Epi e = epi ? *epi : Step1Epi{nullptr, nullptr, nullptr, nullptr, nullptr};
+  k_mgs<<<reduce_blocks(n), kReduceThreads, 0, st>>>(w, vi, hsrc, vn, n, ws.partials, ws.ticket, dst, e);
 }
-void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st) {
-  k_subnorm<<<reduce_blocks(n), kReduceThreads, 0, st>>>(b, t, n, ws.partials, ws.ticket, dst);
+void launch_subnorm(const cd* b, const cd* t, long long n, RedWS& ws, cd* dst, cudaStream_t st, cd* guard) {
+  k_subnorm<<<reduce_blocks(n), kReduceThreads, 0, st>>>(b, t, n, ws.partials, ws.ticket, dst, guard);
 }
 void launch_scale(const cd* x, cd* out, double inv, long long n, cudaStream_t st) {
   k_scale<<<ew_blocks(n), 256, 0, st>>>(x, out, inv, n);

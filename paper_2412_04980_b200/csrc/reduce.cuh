@@ -34,8 +34,10 @@ __device__ __forceinline__ cd block_sum(cd v) {
 // finish a grid reduction: every block deposits its partial; the last one
 // sums partials[0..G) in order and stores to *dst (optionally only the real
 // part as a squared norm).
+// Returns true (block-uniform) in the block that wrote *dst -- callers hang small
+// single-thread epilogues on it (the value is visible to that block's thread 0).
 template <int NT = kReduceThreads>
-__device__ __forceinline__ void grid_finish(cd part, cd* partials, unsigned* ticket, cd* dst) {
+__device__ __forceinline__ bool grid_finish(cd part, cd* partials, unsigned* ticket, cd* dst) {
   __shared__ bool last;
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = part;
@@ -44,7 +46,7 @@ __device__ __forceinline__ void grid_finish(cd part, cd* partials, unsigned* tic
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   cd v = mkc(0.0, 0.0);
   for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
@@ -57,6 +59,7 @@ __device__ __forceinline__ void grid_finish(cd part, cd* partials, unsigned* tic
     *dst = v;
     *ticket = 0u;
   }
+  return true;
 }
 
 }  // namespace hdb
